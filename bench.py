@@ -1,0 +1,320 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 collide-and-stream path (contract in the task README).
+
+Default workload (N = 1): BASELINE.json config 5 — Taylor-Green vortex, D3Q19
+BGK, fp32, 1024^3, Re = 1600, Ma = 0.2 — the largest single-GPU configuration
+and the one the north-star target (>= 80 % of the HBM roofline for D3Q19 BGK
+on one GPU) is quoted on. Strong scaling: the 1024^3 domain is split into N
+z-slabs, one per rank, linked by the fused peer-memory halo push.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1..c5]
+  python bench.py --impl reference ...     # the reference CPU solver (oracle/_ref)
+
+One JSON line is printed by rank 0. `value` is whole-job MLUPS with the state
+resident in HBM; `e2e` is the same metric through the reference-facing C ABI
+call on HOST buffers (dlb_collide_and_stream: host->device copy of the block,
+the step, device->host copy of the new state, every step).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+CONFIGS = {
+    # name: (kind, L, Re, Ma, collision, q, bits, scaling, description)
+    "c1": ("cavity", 64, 1000.0, 0.1, "BGK", 19, 64, "strong",
+           "lid-driven cavity D3Q19 BGK 64^3 fp64"),
+    "c2": ("tgv", 256, 1600.0, 0.2, "RR", 27, 64, "strong",
+           "Taylor-Green vortex Re=1600 D3Q27 recursive-regularized 256^3 fp64"),
+    "c3": ("cavity", 512, 1000.0, 0.1, "TRT", 19, 32, "weak",
+           "lid-driven cavity D3Q19 TRT 512^3 per GPU fp32 (weak scaling)"),
+    "c5": ("tgv", 1024, 1600.0, 0.2, "BGK", 19, 32, "strong",
+           "Taylor-Green vortex D3Q19 BGK 1024^3 fp32 (strong scaling)"),
+}
+
+
+def env_int(name, default):
+    v = os.environ.get(name)
+    return int(v) if v not in (None, "") else default
+
+
+def measured_peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._th = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._th = threading.Thread(target=self._run, daemon=True)
+        self._th.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._th.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if "Active" in s[2 + k]
+                          and "Not" not in s[2 + k]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def cpu_reference(kind, L, Re, Ma, collision, q, bits, warmup, steps, reps=3):
+    """The reference CPU solver (oracle/_ref, built from /root/reference) on the
+    host cores: N workers x N z-blocks, perf::measure_mlups semantics."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from pyoracle import BGK, RR, TRT, Case, Reference  # checker / baseline only
+    if not Reference.available():
+        return None
+    workers = min(os.cpu_count() or 1, L, 64)
+    case = Case(kind=kind, L=L, Re=Re, Ma=Ma, collision={"BGK": BGK, "TRT": TRT, "RR": RR}[collision])
+    mean, reps_ = Reference().bench(case, bits, workers, warmup, steps, reps)
+    return mean, reps_, workers
+
+
+def run_reference_arm(args, cfgname):
+    kind, L, Re, Ma, coll, q, bits, scaling, desc = CONFIGS[cfgname]
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return
+    if q != 19:
+        print(json.dumps({"impl": "reference", "unavailable": "the reference has no D3Q27 path"}))
+        return
+    Ls = min(L, 256 if bits == 32 else 192)
+    res = cpu_reference(kind, Ls, Re, Ma, coll, q, bits, args.warmup, args.steps, reps=1)
+    if res is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    mean, reps_, workers = res
+    sample = (f"{kind} {Ls}^3 D3Q{q} {coll} fp{bits}, {workers} workers x z-blocks, "
+              f"warmup {args.warmup} + {args.steps} steps (measure_mlups semantics)")
+    ms = Ls ** 3 / (mean * 1e6) * 1e3
+    line = {
+        "impl": "reference", "metric": "MLUPS", "value": mean, "unit": "MLUPS",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
+        "dtype": "f32" if bits == 32 else "f64", "data": "synthetic",
+        "config": {"workload": f"{cfgname}: {desc}", "sample_L": Ls},
+        "cpu_baseline": {"value": mean, "unit": "MLUPS", "cores": workers, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": mean, "unit": "MLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def e2e_block(L, bits, steps, warmup):
+    """The same metric through dlb_collide_and_stream on pinned HOST buffers
+    (reference-facing drop-in for collide_and_stream(AcceleratedBlock<T>&, ...)):
+    per step the caller refreshes the periodic envelope, the call copies the
+    block host->device, steps, and copies the new state device->host."""
+    import ctypes as C
+
+    import paper_2506_09242_b200 as dlb
+    from paper_2506_09242_b200 import _capi
+    cfg = dlb.CaseConfig(kind="tgv", L=L, Re=1600.0, Ma=0.2)
+    setup = dlb.init_tgv(cfg)
+    reg = dlb.DynamicsRegistry()
+    slot = reg.register_chain(setup.chains[0])
+    dt = np.float32 if bits == 32 else np.float64
+    e = L + 2
+    nbytes = 19 * e ** 3 * np.dtype(dt).itemsize
+    p = C.c_void_p()
+    _capi.check(_capi.lib().dlb_host_alloc(nbytes, C.byref(p)))
+    try:
+        blk = np.ctypeslib.as_array((C.c_uint8 * nbytes).from_address(p.value)).view(dt).reshape(19, e, e, e)
+        # initial state from the device path (same TGV fill), written into the block
+        run = dlb.build_run(setup, reg, precision=bits)
+        blk[:, 1:-1, 1:-1, 1:-1] = run.gather_raw().reshape(19, L, L, L)
+        del run
+        tag = np.full((e, e, e), -1, np.int32)
+        tag[1:-1, 1:-1, 1:-1] = reg.tag_of_slot(slot)
+        pidx = np.where(tag >= 0, slot, -1).astype(np.int32)
+        ds = dlb.DispatchSet.all_of(reg)
+
+        def refresh():  # refresh_envelope_periodic (accelerated_lattice.cpp:202-238)
+            blk[:, 0, :, :] = blk[:, L, :, :]
+            blk[:, L + 1, :, :] = blk[:, 1, :, :]
+            blk[:, :, 0, :] = blk[:, :, L, :]
+            blk[:, :, L + 1, :] = blk[:, :, 1, :]
+            blk[:, :, :, 0] = blk[:, :, :, L]
+            blk[:, :, :, L + 1] = blk[:, :, :, 1]
+
+        for _ in range(warmup):
+            refresh()
+            dlb.collide_and_stream(reg, blk, tag, pidx, ds)
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            refresh()
+            dlb.collide_and_stream(reg, blk, tag, pidx, ds)
+        t1 = time.perf_counter()
+        mlups = L ** 3 * steps / (t1 - t0) / 1e6
+        return {"value": mlups, "unit": "MLUPS", "h2d_bytes_per_step": int(nbytes),
+                "d2h_bytes_per_step": int(19 * L ** 3 * np.dtype(dt).itemsize),
+                "sample": f"host AcceleratedBlock {L}^3 (+envelope) fp{bits}, pinned, {steps} steps, "
+                          "wall clock incl. envelope refresh, H2D, step, D2H",
+                "finite": bool(np.isfinite(blk[:, 1:-1, 1:-1, 1:-1]).all())}
+    finally:
+        _capi.lib().dlb_host_free(p)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
+    ap.add_argument("--L", type=int, default=None, help="override the edge length (profiling only)")
+    ap.add_argument("--arith", default="exact", choices=["exact", "fast"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    if args.impl == "reference":
+        run_reference_arm(args, args.config)
+        return
+
+    import torch
+    import torch.distributed as tdist
+
+    import paper_2506_09242_b200 as dlb
+
+    rank, world = env_int("RANK", 0), env_int("WORLD_SIZE", 1)
+    local = env_int("LOCAL_RANK", 0)
+    if world > 1:
+        tdist.init_process_group("gloo")
+    torch.cuda.set_device(local)
+
+    kind, L, Re, Ma, coll, q, bits, scaling, desc = CONFIGS[args.config]
+    if scaling == "weak":
+        L = int(round(L * world ** (1.0 / 3.0)))  # perfmodel.cpp:76-85 weak sizes
+    if args.L:
+        L = args.L
+    lt = {"BGK": dlb.LinkType.BGK, "TRT": dlb.LinkType.TRT, "RR": dlb.LinkType.RR}[coll]
+    cfg = dlb.CaseConfig(kind=kind, L=L, Re=Re, Ma=Ma, collision=lt, q=q)
+    setup = dlb.init_tgv(cfg) if kind == "tgv" else dlb.init_cavity(cfg)
+    run = dlb.build_run(setup, precision=bits, arith=args.arith,
+                        dist=(rank, world) if world > 1 else None, devices=[local])
+    cells_total = run.num_cells()
+    bpc, dev_bytes, launches = run.traffic()
+
+    for _ in range(args.warmup):
+        run.advance(1)
+    run.synchronize()
+    if world > 1:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ms = run.time_steps(args.steps)  # CUDA events on the lattice stream
+        run.synchronize()
+    torch.cuda.synchronize()
+    t = torch.tensor([ms], dtype=torch.float64)
+    if world > 1:
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        tdist.barrier()
+    ms_max = float(t.item())
+    ms_step = ms_max / args.steps
+    mlups = cells_total * args.steps / (ms_max * 1e-3) / 1e6
+
+    # roofline of the dominant kernel (the fused collide-stream launch(es) of a step)
+    my_cells = run.dims[0] * run.dims[1] * sum(p[1] for k, p in enumerate(run.parts) if k in run.ranks)
+    peak, peak_kind = measured_peak_hbm()
+    achieved = bpc * my_cells / (ms / args.steps * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as f:
+                tr = json.load(f)
+            key = f"{args.config}:{run.kernel_name()}"
+            if key in tr:
+                traffic = tr[key]["bytes_per_cell"] * my_cells
+        except Exception:
+            traffic = None
+
+    if rank != 0:
+        if world > 1:
+            tdist.barrier()
+        return
+
+    cpu = None
+    if world == 1 and not args.no_cpu and q == 19:
+        Ls = min(L, 128)
+        res = cpu_reference(kind, Ls, Re, Ma, coll, q, bits, 2, 8, reps=3)
+        if res:
+            mean, reps_, workers = res
+            cpu = {"value": mean, "unit": "MLUPS", "cores": workers, "kind": "reference",
+                   "sample": f"{kind} {Ls}^3 D3Q{q} {coll} fp{bits}: reference MultiBlockRun, "
+                             f"{workers} workers x z-blocks, warmup 2, 3 reps x 8 steps"}
+    e2e = None
+    if not args.no_e2e and q == 19 and kind == "tgv":
+        del run
+        torch.cuda.empty_cache()
+        e2e = e2e_block(min(L, 512), bits, max(2, min(args.steps, 5)), 1)
+    line = {
+        "metric": "MLUPS", "value": mlups, "unit": "MLUPS", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling,
+        "vs_baseline": None, "dtype": "f32" if bits == 32 else "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {desc}", "L": L, "cells": cells_total,
+                   "parallelism": f"z-slab x{world}", "layout": "two-population SoA",
+                   "arith": args.arith, "l2": "inputs larger than L2 (state resident in HBM)",
+                   "device_bytes_per_gpu": dev_bytes},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "bytes_per_cell": bpc},
+        "gpu_launches": launches * args.steps,
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        tdist.barrier()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,178 @@
+/* dlb — B200-native collide-and-stream for the dolb lattice Boltzmann solver.
+ *
+ * C ABI of libdlb_b200.so. Plain pointers and sizes only. Conventions follow
+ * the reference C interface (proj/include/dolb/dolb.h:1-32, proj/src/capi.cpp:13-39):
+ * every call returns DLB_OK (0) or a nonzero status; dlb_last_error() (thread
+ * local) describes the failure; handles are opaque and released by their free
+ * function. Status values are numerically identical to dolb_status.
+ *
+ * What each group replaces in the reference (file:line under /root/reference/proj):
+ *   dlb_chain_* / dlb_registry_*  DynamicsRegistry + chain strings
+ *                                 (include/dolb/accelerated_lattice.hpp:32-79,
+ *                                  src/accelerated_lattice.cpp:10-84, src/chain.cpp:38-230)
+ *   dlb_lattice_*                 AcceleratedBlock<T> + collide_and_stream<T> +
+ *                                 MultiBlockRun<T>::{fill,advance,gather_populations}
+ *                                 (include/dolb/accelerated_lattice.hpp:86-127,
+ *                                  include/dolb/multiblock.hpp:119-159)
+ *   dlb_lattice_link_* / _ipc     Transport + envelope exchange of one z-slab
+ *                                 (include/dolb/multiblock.hpp:93-109, src/multiblock.cpp:289-355)
+ *   dlb_collide_and_stream        collide_and_stream<T>(AcceleratedBlock<T>&, registry,
+ *                                 recipes, dispatch, nthreads) on HOST buffers
+ *                                 (include/dolb/accelerated_lattice.hpp:124-127)
+ *   dlb_case_*                    init_tgv / init_cavity / init_porous input generators
+ *                                 (include/dolb/cases.hpp:96-98, src/cases.cpp:127-260)
+ */
+#ifndef DLB_H
+#define DLB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#define DLB_API __attribute__((visibility("default")))
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum dlb_status {
+    DLB_OK = 0,
+    DLB_ERROR_INVALID_ARGUMENT = 1,
+    DLB_ERROR_CONFIG = 2,
+    DLB_ERROR_IO = 3,
+    DLB_ERROR_DISPATCH = 4,
+    DLB_ERROR_EXCHANGE = 5,
+    DLB_ERROR_INTERNAL = 6, /* includes CUDA failures; no CPU fallback exists */
+} dlb_status;
+
+enum { DLB_LAYOUT_TWO_POP = 0, DLB_LAYOUT_AA = 1 };
+enum { DLB_ARITH_EXACT = 0, /* reference operation order, no FMA: bit-identical   */
+       DLB_ARITH_FAST = 1 };  /* FMA contraction allowed (fp64 drift <= 1e-12 rel) */
+
+DLB_API const char* dlb_version(void);
+DLB_API const char* dlb_last_error(void);
+
+/* ---- dynamics chains (src/chain.cpp:38-151) -------------------------------- */
+/* Parse + validate a chain string and write its canonical rendering. */
+DLB_API dlb_status dlb_chain_canonical(const char* chain, char* buf, size_t cap, size_t* len_out);
+
+/* ---- registry (src/accelerated_lattice.cpp:10-84) -------------------------- */
+typedef struct dlb_registry dlb_registry;
+DLB_API dlb_status dlb_registry_new(dlb_registry** out);
+DLB_API void dlb_registry_free(dlb_registry* reg);
+/* register_chain: chain string + its serialize_params record (chain.cpp:153-186).
+ * Idempotent for identical (chain, params); rejects omega outside (0, 2). */
+DLB_API dlb_status dlb_registry_register(dlb_registry* reg, const char* chain,
+                                         const double* params, size_t n_params,
+                                         int32_t* slot_out);
+DLB_API dlb_status dlb_registry_tag_for(const dlb_registry* reg, const char* chain,
+                                        int32_t* tag_out);
+DLB_API dlb_status dlb_registry_chain_for(const dlb_registry* reg, int32_t tag, char* buf,
+                                          size_t cap, size_t* len_out);
+DLB_API dlb_status dlb_registry_tag_of_slot(const dlb_registry* reg, int32_t slot,
+                                            int32_t* tag_out);
+DLB_API dlb_status dlb_registry_counts(const dlb_registry* reg, int32_t* num_tags,
+                                       int32_t* num_instances);
+DLB_API dlb_status dlb_registry_slot_params(const dlb_registry* reg, int32_t slot, double* buf,
+                                            size_t cap, size_t* len_out);
+
+/* ---- device lattice: one z-slab of the domain on one GPU -------------------- */
+typedef struct dlb_lattice dlb_lattice;
+typedef struct dlb_lattice_desc {
+    int64_t dims[3];         /* interior cells of this slab (x, y, z) */
+    int32_t periodic[3];     /* global periodicity of the domain */
+    int32_t q;               /* 19 or 27 */
+    int32_t precision_bits;  /* 32 or 64 */
+    int32_t layout;          /* DLB_LAYOUT_* */
+    int32_t arith;           /* DLB_ARITH_* */
+    int32_t device;          /* CUDA ordinal */
+    int64_t z_origin;        /* global z index of the slab's first interior plane */
+    int64_t global_nz;       /* global z extent (== dims[2] for a single slab) */
+} dlb_lattice_desc;
+
+DLB_API dlb_status dlb_lattice_create(const dlb_lattice_desc* desc, const dlb_registry* reg,
+                                      dlb_lattice** out);
+DLB_API void dlb_lattice_free(dlb_lattice* lat);
+/* Registry instance slot of every interior cell, x fastest (MultiBlockRun::fill's slot_of). */
+DLB_API dlb_status dlb_lattice_set_slots(dlb_lattice* lat, const int32_t* slots);
+DLB_API dlb_status dlb_lattice_set_uniform_slot(dlb_lattice* lat, int32_t slot);
+/* Dispatch set (accelerated_lattice.hpp:63-79). A present tag outside it makes
+ * dlb_lattice_step fail with DLB_ERROR_DISPATCH before any cell is written. */
+DLB_API dlb_status dlb_lattice_set_dispatch(dlb_lattice* lat, const int32_t* tags, size_t n);
+/* Stored state := equilibrium2<T>(T(rho), T(u)) per cell (multiblock.cpp:278-281). */
+DLB_API dlb_status dlb_lattice_fill_equilibrium(dlb_lattice* lat, const double* rho,
+                                                const double* ux, const double* uy,
+                                                const double* uz);
+/* Taylor-Green initial state of an L^3 box (cases.cpp:145-156), built on the device. */
+DLB_API dlb_status dlb_lattice_fill_tgv(dlb_lattice* lat, int64_t L, double u_inf);
+/* Canonical populations: q arrays of nx*ny*nz doubles, direction-major, x fastest
+ * (MultiBlockRun::gather_populations order, multiblock.cpp:421-441). */
+DLB_API dlb_status dlb_lattice_upload_populations(dlb_lattice* lat, const double* canon);
+DLB_API dlb_status dlb_lattice_download_populations(dlb_lattice* lat, double* canon);
+/* Same, in the storage precision (float for 32-bit lattices). */
+DLB_API dlb_status dlb_lattice_download_raw(dlb_lattice* lat, void* canon);
+/* Advance nsteps (asynchronous on the lattice stream; includes the halo exchange). */
+DLB_API dlb_status dlb_lattice_step(dlb_lattice* lat, int64_t nsteps);
+DLB_API dlb_status dlb_lattice_synchronize(dlb_lattice* lat);
+DLB_API dlb_status dlb_lattice_stream(dlb_lattice* lat, void** stream_out);
+DLB_API dlb_status dlb_lattice_steps_done(dlb_lattice* lat, int64_t* steps_out);
+/* Algorithmic bytes per cell update (2*q*sizeof(T) + slot bytes), device bytes held,
+ * and kernel launches per step (for bench accounting). */
+DLB_API dlb_status dlb_lattice_traffic(dlb_lattice* lat, int64_t* bytes_per_cell,
+                                       int64_t* device_bytes, int32_t* launches_per_step);
+/* Time nsteps with CUDA events recorded on the lattice stream (milliseconds). */
+DLB_API dlb_status dlb_lattice_time_steps(dlb_lattice* lat, int64_t nsteps, double* ms_out);
+/* Name of the kernel instantiation selected for the present dynamics. */
+DLB_API dlb_status dlb_lattice_kernel_name(dlb_lattice* lat, char* buf, size_t cap,
+                                           size_t* len_out);
+
+/* ---- z-slab halo exchange over peer memory ---------------------------------- */
+/* Same process (any devices with peer access, or one device): the top plane of
+ * `lower` feeds the bottom ghost plane of `upper` and vice versa. */
+DLB_API dlb_status dlb_lattice_link_local(dlb_lattice* lower, dlb_lattice* upper);
+/* Across processes: export an opaque blob (CUDA IPC handles), ship it with any
+ * transport (e.g. torch.distributed), link it as the lower (side 0) or upper
+ * (side 1) neighbour. */
+DLB_API dlb_status dlb_lattice_export_ipc(dlb_lattice* lat, void* blob, size_t cap,
+                                          size_t* len_out);
+DLB_API dlb_status dlb_lattice_link_ipc(dlb_lattice* lat, int32_t side, const void* blob,
+                                        size_t len);
+/* Advance several slabs of ONE process in lockstep (one step of each in turn),
+ * the single-process analogue of MultiBlockRun::advance (multiblock.cpp:376-419). */
+DLB_API dlb_status dlb_lattices_step(dlb_lattice** lats, size_t n, int64_t nsteps);
+
+/* ---- drop-in for collide_and_stream<T> on a host AcceleratedBlock ----------- */
+/* Envelope-inclusive SoA arrays exactly as AcceleratedBlock<T> holds them
+ * (accelerated_lattice.hpp:86-112): f_in/f_out q*ext[0]*ext[1]*ext[2] values,
+ * tag/param_index ext-volume int32. Pre: envelope of f_in current. Post: f_in
+ * holds the new state and f_out the previous one (the reference's swap,
+ * accelerated_lattice.cpp:199); f_out may be NULL to skip that copy. */
+typedef struct dlb_block_view {
+    int32_t precision_bits;
+    int32_t q;
+    int64_t interior[3];
+    void* f_in;
+    void* f_out;
+    const int32_t* tag;
+    const int32_t* param_index;
+} dlb_block_view;
+DLB_API dlb_status dlb_collide_and_stream(const dlb_registry* reg, dlb_block_view* block,
+                                          const int32_t* dispatch_tags, size_t n_dispatch,
+                                          int32_t nthreads);
+/* Pinned host memory for the block API (page-locked, for full-rate copies). */
+DLB_API dlb_status dlb_host_alloc(size_t bytes, void** out);
+DLB_API void dlb_host_free(void* ptr);
+
+/* ---- case input generators (src/cases.cpp) ------------------------------------ */
+/* Random Boolean sphere pack written as the reference's raw 8-bit voxel format
+ * (x fastest, 255 = solid; cases.cpp:86-111): spheres of radius r voxels with
+ * uniform centres (mt19937_64 seed) are added, periodic placement, until the
+ * porosity drops to target_porosity or below. */
+DLB_API dlb_status dlb_case_sphere_pack(int64_t nx, int64_t ny, int64_t nz, double radius,
+                                        double target_porosity, uint64_t seed, uint8_t* out,
+                                        double* porosity_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DLB_H */

@@ -1,0 +1,241 @@
+// TEST INFRASTRUCTURE ONLY — never linked into the product.
+//
+// extern "C" shim over the UNMODIFIED reference solver ("dolb",
+// /root/reference/proj), compiled from the reference sources where they lie
+// by oracle/Makefile into oracle/_ref/libdolb_refshim.so. It uses only the
+// reference's public C++ API:
+//   - case generators   init_tgv / init_cavity / init_porous  (proj/src/cases.cpp:127-260)
+//   - build_run<T>      (proj/src/cases.cpp:279-297) + MultiBlockRun<T>::advance
+//                       (proj/src/multiblock.cpp:376-419) + gather_populations (:421-441)
+//   - compile_chain<T> / ChainRecipe<T>::apply (proj/include/dolb/chain.hpp:104-187)
+//   - equilibrium2/4 (proj/include/dolb/descriptor.hpp:79-121)
+//   - perf::measure_mlups (proj/src/perfmodel.cpp:94-121)
+// Python tests and bench.py (--impl reference / cpu_baseline) call it via ctypes.
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "dolb/accelerated_lattice.hpp"
+#include "dolb/cases.hpp"
+#include "dolb/chain.hpp"
+#include "dolb/descriptor.hpp"
+#include "dolb/multiblock.hpp"
+#include "dolb/perfmodel.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+// Flat case description (mirrors dolb::CaseConfig, proj/include/dolb/cases.hpp:22-54).
+struct RefCase {
+    int32_t kind;        // 0 tgv, 1 cavity, 2 porous
+    int32_t collision;   // 0 BGK, 1 TRT, 2 RR
+    int64_t L;
+    double Re, Ma, lambda, omega_bulk_ho;
+    double smagorinsky_c;  // NaN => no LES link
+    int32_t drive;         // 0 velocity, 1 pressure
+    int32_t pad0;
+    double tau, delta_rho;
+    int64_t upstream, downstream, plate_layers;
+    int64_t voxel_dims[3];
+    const char* geometry;  // "plates" or a raw voxel path
+};
+
+dolb::LinkType base_of(int c) {
+    switch (c) {
+        case 0: return dolb::LinkType::BGK;
+        case 1: return dolb::LinkType::TRT;
+        case 2: return dolb::LinkType::RR;
+    }
+    throw std::invalid_argument("collision must be 0 (BGK), 1 (TRT) or 2 (RR)");
+}
+
+dolb::CaseSetup make_setup(const RefCase& rc) {
+    dolb::CaseConfig cfg;
+    cfg.kind = rc.kind == 0 ? dolb::CaseKind::Tgv
+             : rc.kind == 1 ? dolb::CaseKind::Cavity
+                            : dolb::CaseKind::Porous;
+    cfg.L = rc.L;
+    cfg.Re = rc.Re;
+    cfg.Ma = rc.Ma;
+    cfg.collision = base_of(rc.collision);
+    if (!std::isnan(rc.smagorinsky_c)) cfg.smagorinsky_c = rc.smagorinsky_c;
+    cfg.lambda = rc.lambda;
+    cfg.omega_bulk_ho = rc.omega_bulk_ho;
+    cfg.drive = rc.drive == 0 ? dolb::DriveKind::Velocity : dolb::DriveKind::Pressure;
+    cfg.tau = rc.tau;
+    cfg.delta_rho = rc.delta_rho;
+    cfg.upstream = rc.upstream;
+    cfg.downstream = rc.downstream;
+    cfg.plate_layers = rc.plate_layers;
+    if (rc.kind == 0) return dolb::init_tgv(cfg);
+    if (rc.kind == 1) return dolb::init_cavity(cfg);
+    cfg.geometry = rc.geometry ? rc.geometry : "";
+    std::shared_ptr<const dolb::VoxelGeometry> geom;
+    if (cfg.geometry == "plates") {
+        geom = std::make_shared<dolb::VoxelGeometry>(
+            dolb::make_plate_geometry(rc.L, rc.L, rc.plate_layers));
+    } else {
+        geom = std::make_shared<dolb::VoxelGeometry>(dolb::load_voxels(
+            cfg.geometry, {rc.voxel_dims[0], rc.voxel_dims[1], rc.voxel_dims[2]}, 0.5, 1e-6));
+    }
+    return dolb::init_porous(cfg, geom);
+}
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+    try {
+        fn();
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    } catch (...) {
+        g_err = "unknown error";
+        return 1;
+    }
+}
+
+template <typename T>
+void run_case(const RefCase& rc, const int grid[3], int workers, int64_t steps, double* out) {
+    const dolb::CaseSetup setup = make_setup(rc);
+    auto registry = std::make_shared<dolb::DynamicsRegistry>();
+    auto run = dolb::build_run<T>(setup, {grid[0], grid[1], grid[2]}, workers, registry);
+    run.advance(steps);
+    const std::vector<double> pops = run.gather_populations();
+    std::memcpy(out, pops.data(), pops.size() * sizeof(double));
+}
+
+template <typename T>
+void bench_case(const RefCase& rc, int workers, int64_t warmup, int64_t steps, int reps,
+                double* rep_mlups, double* mean) {
+    const dolb::CaseSetup setup = make_setup(rc);
+    auto registry = std::make_shared<dolb::DynamicsRegistry>();
+    // N workers and N z-blocks: the only way the reference uses N cores
+    // (MultiBlockRun never passes nthreads > 1, proj/src/multiblock.cpp:367,397).
+    auto run = dolb::build_run<T>(setup, {1, 1, workers}, workers, registry);
+    const auto report = dolb::perf::measure_mlups(
+        [&run](std::int64_t n) { run.advance(n); }, run.num_cells(), warmup, steps, reps);
+    for (int r = 0; r < reps; ++r) rep_mlups[r] = report.repetition_mlups[std::size_t(r)];
+    *mean = report.mlups;
+}
+
+template <typename T>
+void apply_chain(const char* chain_str, const double* params, size_t nparams, double* f,
+                 int64_t n) {
+    dolb::DynamicsChain chain;
+    chain.links = dolb::parse_chain_string(chain_str);
+    chain.params = dolb::deserialize_params(chain.links, params, nparams);
+    const dolb::ChainRecipe<T> recipe = dolb::compile_chain<T>(chain);
+    for (int64_t c = 0; c < n; ++c) {
+        dolb::Populations<T> p;
+        for (int i = 0; i < 19; ++i) p[i] = T(f[c * 19 + i]);
+        recipe.apply(p);
+        for (int i = 0; i < 19; ++i) f[c * 19 + i] = double(p[i]);
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+__attribute__((visibility("default"))) const char* ref_last_error(void) { return g_err.c_str(); }
+
+__attribute__((visibility("default"))) int ref_case_dims(const RefCase* rc, int64_t* dims) {
+    return guarded([&] {
+        const auto s = make_setup(*rc);
+        for (int a = 0; a < 3; ++a) dims[a] = s.dims[a];
+    });
+}
+
+// Per-cell registry tags (x fastest) plus the newline-joined sorted model list.
+__attribute__((visibility("default"))) int ref_case_tags(const RefCase* rc, int32_t* tags,
+                                                         char* models, size_t cap) {
+    return guarded([&] {
+        const auto s = make_setup(*rc);
+        dolb::DynamicsRegistry reg;
+        for (const auto& ch : s.chains) reg.register_chain(*ch);
+        int64_t k = 0;
+        for (int64_t z = 0; z < s.dims[2]; ++z)
+            for (int64_t y = 0; y < s.dims[1]; ++y)
+                for (int64_t x = 0; x < s.dims[0]; ++x, ++k)
+                    tags[k] = reg.tag_for(dolb::chain_string(*s.chain_of(x, y, z)));
+        std::string joined;
+        for (const auto& m : reg.chain_strings()) joined += m + "\n";
+        if (joined.size() + 1 > cap) throw std::invalid_argument("model buffer too small");
+        std::memcpy(models, joined.c_str(), joined.size() + 1);
+    });
+}
+
+// Runs `steps` steps of the reference accelerated path (MultiBlockRun<T>) and
+// writes gather_populations() (19*N doubles, direction-major, x fastest).
+__attribute__((visibility("default"))) int ref_case_run(const RefCase* rc, int precision_bits,
+                                                        const int* grid, int workers,
+                                                        int64_t steps, double* out) {
+    return guarded([&] {
+        if (precision_bits == 64) run_case<double>(*rc, grid, workers, steps, out);
+        else if (precision_bits == 32) run_case<float>(*rc, grid, workers, steps, out);
+        else throw std::invalid_argument("precision must be 32 or 64");
+    });
+}
+
+__attribute__((visibility("default"))) int ref_case_bench(const RefCase* rc, int precision_bits,
+                                                          int workers, int64_t warmup,
+                                                          int64_t steps, int reps,
+                                                          double* rep_mlups, double* mean) {
+    return guarded([&] {
+        if (precision_bits == 64) bench_case<double>(*rc, workers, warmup, steps, reps, rep_mlups, mean);
+        else bench_case<float>(*rc, workers, warmup, steps, reps, rep_mlups, mean);
+    });
+}
+
+// ChainRecipe<T>::apply on n population sets (input/output as doubles, cast to T).
+__attribute__((visibility("default"))) int ref_apply_chain(const char* chain_str,
+                                                           const double* params, size_t nparams,
+                                                           int precision_bits, double* f,
+                                                           int64_t n) {
+    return guarded([&] {
+        if (precision_bits == 64) apply_chain<double>(chain_str, params, nparams, f, n);
+        else apply_chain<float>(chain_str, params, nparams, f, n);
+    });
+}
+
+__attribute__((visibility("default"))) int ref_equilibrium(int order, int precision_bits,
+                                                           double rho, const double* u,
+                                                           double* out) {
+    return guarded([&] {
+        auto go = [&](auto tag) {
+            using T = decltype(tag);
+            const std::array<T, 3> uu = {T(u[0]), T(u[1]), T(u[2])};
+            const auto feq = order == 4 ? dolb::equilibrium4<T>(T(rho), uu)
+                                        : dolb::equilibrium2<T>(T(rho), uu);
+            for (int i = 0; i < 19; ++i) out[i] = double(feq[i]);
+        };
+        if (precision_bits == 64) go(double{});
+        else go(float{});
+    });
+}
+
+__attribute__((visibility("default"))) double ref_derive_omega_minus(double omega, double lambda) {
+    return dolb::CollisionParams::derive_omega_minus(omega, lambda);
+}
+
+// Registry-level behaviour, for pinning the product's host-side mirror:
+// chain string of a (chain string, params) after a parse/serialize round trip.
+__attribute__((visibility("default"))) int ref_chain_roundtrip(const char* chain_str,
+                                                               char* out, size_t cap) {
+    return guarded([&] {
+        dolb::DynamicsChain chain;
+        chain.links = dolb::parse_chain_string(chain_str);
+        dolb::validate_chain(chain);
+        const std::string s = dolb::chain_string(chain);
+        if (s.size() + 1 > cap) throw std::invalid_argument("buffer too small");
+        std::memcpy(out, s.c_str(), s.size() + 1);
+    });
+}
+
+}  // extern "C"

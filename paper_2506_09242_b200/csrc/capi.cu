@@ -1,0 +1,393 @@
+// extern "C" boundary of libdlb_b200.so (include/dlb.h). Exceptions map to
+// status codes the way the reference's C interface does (proj/src/capi.cpp:20-39);
+// the message goes to a thread-local last-error buffer (capi.cpp:13-18).
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/dlb.h"
+#include "chain.hpp"
+#include "lattice.hpp"
+
+struct dlb_registry {
+    dlb::DynamicsRegistry reg;
+};
+
+struct dlb_lattice {
+    std::unique_ptr<dlb::Lattice> lat;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+dlb_status fail(dlb_status s, const std::string& msg) {
+    g_last_error = msg;
+    return s;
+}
+
+template <typename Fn>
+dlb_status guarded(Fn&& fn) {
+    try {
+        fn();
+        return DLB_OK;
+    } catch (const dlb::DispatchError& e) {
+        return fail(DLB_ERROR_DISPATCH, e.what());
+    } catch (const dlb::ExchangeError& e) {
+        return fail(DLB_ERROR_EXCHANGE, e.what());
+    } catch (const dlb::DeviceError& e) {
+        return fail(DLB_ERROR_INTERNAL, e.what());
+    } catch (const std::invalid_argument& e) {
+        return fail(DLB_ERROR_CONFIG, e.what());
+    } catch (const std::out_of_range& e) {
+        return fail(DLB_ERROR_CONFIG, e.what());
+    } catch (const std::domain_error& e) {
+        return fail(DLB_ERROR_CONFIG, e.what());
+    } catch (const std::runtime_error& e) {
+        return fail(DLB_ERROR_IO, e.what());
+    } catch (const std::exception& e) {
+        return fail(DLB_ERROR_INTERNAL, e.what());
+    } catch (...) {
+        return fail(DLB_ERROR_INTERNAL, "unknown error");
+    }
+}
+
+#define DLB_REQUIRE(cond)                                                          \
+    do {                                                                           \
+        if (!(cond)) return fail(DLB_ERROR_INVALID_ARGUMENT, "null argument: " #cond); \
+    } while (0)
+
+void write_string(const std::string& s, char* buf, size_t cap, size_t* len_out) {
+    if (len_out) *len_out = s.size() + 1;
+    if (buf == nullptr) return;  // size query
+    if (cap < s.size() + 1) throw std::invalid_argument("buffer too small");
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+}
+
+// Cached device lattice for the host-block drop-in (one per block shape).
+struct BlockCtx {
+    std::unique_ptr<dlb::Lattice> lat;
+    const dlb_registry* reg = nullptr;
+    int instances = -1;
+    std::vector<int32_t> slots;
+};
+std::mutex g_block_mu;
+std::map<std::vector<int64_t>, BlockCtx> g_blocks;
+
+}  // namespace
+
+extern "C" {
+
+DLB_API const char* dlb_version(void) { return "dlb-b200 0.1 (sm_100a)"; }
+DLB_API const char* dlb_last_error(void) { return g_last_error.c_str(); }
+
+DLB_API dlb_status dlb_chain_canonical(const char* chain, char* buf, size_t cap, size_t* len_out) {
+    DLB_REQUIRE(chain);
+    return guarded([&] {
+        const auto links = dlb::parse_chain_string(chain);
+        dlb::validate_chain(links);
+        write_string(dlb::chain_string(links), buf, cap, len_out);
+    });
+}
+
+DLB_API dlb_status dlb_registry_new(dlb_registry** out) {
+    DLB_REQUIRE(out);
+    return guarded([&] { *out = new dlb_registry(); });
+}
+
+DLB_API void dlb_registry_free(dlb_registry* reg) { delete reg; }
+
+DLB_API dlb_status dlb_registry_register(dlb_registry* reg, const char* chain, const double* params,
+                                         size_t n_params, int32_t* slot_out) {
+    DLB_REQUIRE(reg);
+    DLB_REQUIRE(chain);
+    DLB_REQUIRE(slot_out);
+    DLB_REQUIRE(params || n_params == 0);
+    return guarded([&] {
+        dlb::DynamicsChain c;
+        c.links = dlb::parse_chain_string(chain);
+        dlb::validate_chain(c.links);
+        c.params = dlb::deserialize_params(c.links, params, n_params);
+        *slot_out = reg->reg.register_chain(c);
+    });
+}
+
+DLB_API dlb_status dlb_registry_tag_for(const dlb_registry* reg, const char* chain, int32_t* tag_out) {
+    DLB_REQUIRE(reg);
+    DLB_REQUIRE(chain);
+    DLB_REQUIRE(tag_out);
+    return guarded([&] { *tag_out = reg->reg.tag_for(chain); });
+}
+
+DLB_API dlb_status dlb_registry_chain_for(const dlb_registry* reg, int32_t tag, char* buf, size_t cap,
+                                          size_t* len_out) {
+    DLB_REQUIRE(reg);
+    return guarded([&] { write_string(reg->reg.chain_for(tag), buf, cap, len_out); });
+}
+
+DLB_API dlb_status dlb_registry_tag_of_slot(const dlb_registry* reg, int32_t slot, int32_t* tag_out) {
+    DLB_REQUIRE(reg);
+    DLB_REQUIRE(tag_out);
+    return guarded([&] { *tag_out = reg->reg.tag_of_slot(slot); });
+}
+
+DLB_API dlb_status dlb_registry_counts(const dlb_registry* reg, int32_t* num_tags, int32_t* num_instances) {
+    DLB_REQUIRE(reg);
+    return guarded([&] {
+        if (num_tags) *num_tags = reg->reg.num_tags();
+        if (num_instances) *num_instances = reg->reg.num_instances();
+    });
+}
+
+DLB_API dlb_status dlb_registry_slot_params(const dlb_registry* reg, int32_t slot, double* buf,
+                                            size_t cap, size_t* len_out) {
+    DLB_REQUIRE(reg);
+    return guarded([&] {
+        const auto& in = reg->reg.instance(slot);
+        if (len_out) *len_out = size_t(in.param_len);
+        if (!buf) return;
+        if (cap < size_t(in.param_len)) throw std::invalid_argument("buffer too small");
+        for (int64_t k = 0; k < in.param_len; ++k)
+            buf[k] = reg->reg.params_table()[size_t(in.param_offset + k)];
+    });
+}
+
+DLB_API dlb_status dlb_lattice_create(const dlb_lattice_desc* desc, const dlb_registry* reg,
+                                      dlb_lattice** out) {
+    DLB_REQUIRE(desc);
+    DLB_REQUIRE(reg);
+    DLB_REQUIRE(out);
+    return guarded([&] {
+        auto h = std::make_unique<dlb_lattice>();
+        h->lat = std::make_unique<dlb::Lattice>(*desc, reg->reg);
+        *out = h.release();
+    });
+}
+
+DLB_API void dlb_lattice_free(dlb_lattice* lat) { delete lat; }
+
+DLB_API dlb_status dlb_lattice_set_slots(dlb_lattice* lat, const int32_t* slots) {
+    DLB_REQUIRE(lat);
+    DLB_REQUIRE(slots);
+    return guarded([&] { lat->lat->set_slots(slots); });
+}
+
+DLB_API dlb_status dlb_lattice_set_uniform_slot(dlb_lattice* lat, int32_t slot) {
+    DLB_REQUIRE(lat);
+    return guarded([&] { lat->lat->set_uniform_slot(slot); });
+}
+
+DLB_API dlb_status dlb_lattice_set_dispatch(dlb_lattice* lat, const int32_t* tags, size_t n) {
+    DLB_REQUIRE(lat);
+    DLB_REQUIRE(tags || n == 0);
+    return guarded([&] { lat->lat->set_dispatch(tags, n); });
+}
+
+DLB_API dlb_status dlb_lattice_fill_equilibrium(dlb_lattice* lat, const double* rho, const double* ux,
+                                                const double* uy, const double* uz) {
+    DLB_REQUIRE(lat);
+    DLB_REQUIRE(rho && ux && uy && uz);
+    return guarded([&] { lat->lat->fill_equilibrium(rho, ux, uy, uz); });
+}
+
+DLB_API dlb_status dlb_lattice_fill_tgv(dlb_lattice* lat, int64_t L, double u_inf) {
+    DLB_REQUIRE(lat);
+    return guarded([&] { lat->lat->fill_tgv(L, u_inf); });
+}
+
+DLB_API dlb_status dlb_lattice_upload_populations(dlb_lattice* lat, const double* canon) {
+    DLB_REQUIRE(lat);
+    DLB_REQUIRE(canon);
+    return guarded([&] { lat->lat->upload(canon); });
+}
+
+DLB_API dlb_status dlb_lattice_download_populations(dlb_lattice* lat, double* canon) {
+    DLB_REQUIRE(lat);
+    DLB_REQUIRE(canon);
+    return guarded([&] {
+        lat->lat->synchronize();
+        lat->lat->download(canon);
+    });
+}
+
+DLB_API dlb_status dlb_lattice_download_raw(dlb_lattice* lat, void* canon) {
+    DLB_REQUIRE(lat);
+    DLB_REQUIRE(canon);
+    return guarded([&] {
+        lat->lat->synchronize();
+        lat->lat->download_raw(canon);
+    });
+}
+
+DLB_API dlb_status dlb_lattice_step(dlb_lattice* lat, int64_t nsteps) {
+    DLB_REQUIRE(lat);
+    return guarded([&] { lat->lat->step(nsteps); });
+}
+
+DLB_API dlb_status dlb_lattice_synchronize(dlb_lattice* lat) {
+    DLB_REQUIRE(lat);
+    return guarded([&] { lat->lat->synchronize(); });
+}
+
+DLB_API dlb_status dlb_lattice_stream(dlb_lattice* lat, void** stream_out) {
+    DLB_REQUIRE(lat);
+    DLB_REQUIRE(stream_out);
+    *stream_out = static_cast<void*>(lat->lat->stream());
+    return DLB_OK;
+}
+
+DLB_API dlb_status dlb_lattice_steps_done(dlb_lattice* lat, int64_t* steps_out) {
+    DLB_REQUIRE(lat);
+    DLB_REQUIRE(steps_out);
+    *steps_out = lat->lat->steps_done();
+    return DLB_OK;
+}
+
+DLB_API dlb_status dlb_lattice_traffic(dlb_lattice* lat, int64_t* bytes_per_cell, int64_t* device_bytes,
+                                       int32_t* launches_per_step) {
+    DLB_REQUIRE(lat);
+    if (bytes_per_cell) *bytes_per_cell = lat->lat->bytes_per_cell();
+    if (device_bytes) *device_bytes = lat->lat->device_bytes();
+    if (launches_per_step) *launches_per_step = lat->lat->launches_per_step();
+    return DLB_OK;
+}
+
+DLB_API dlb_status dlb_lattice_time_steps(dlb_lattice* lat, int64_t nsteps, double* ms_out) {
+    DLB_REQUIRE(lat);
+    DLB_REQUIRE(ms_out);
+    return guarded([&] { *ms_out = lat->lat->time_steps(nsteps); });
+}
+
+DLB_API dlb_status dlb_lattice_kernel_name(dlb_lattice* lat, char* buf, size_t cap, size_t* len_out) {
+    DLB_REQUIRE(lat);
+    return guarded([&] { write_string(lat->lat->kernel_name(), buf, cap, len_out); });
+}
+
+DLB_API dlb_status dlb_lattice_link_local(dlb_lattice* lower, dlb_lattice* upper) {
+    DLB_REQUIRE(lower);
+    DLB_REQUIRE(upper);
+    return guarded([&] { upper->lat->link_lower(*lower->lat); });
+}
+
+DLB_API dlb_status dlb_lattice_export_ipc(dlb_lattice* lat, void* blob, size_t cap, size_t* len_out) {
+    DLB_REQUIRE(lat);
+    return guarded([&] {
+        const auto b = lat->lat->export_ipc();
+        if (len_out) *len_out = b.size();
+        if (!blob) return;
+        if (cap < b.size()) throw std::invalid_argument("buffer too small");
+        std::memcpy(blob, b.data(), b.size());
+    });
+}
+
+DLB_API dlb_status dlb_lattice_link_ipc(dlb_lattice* lat, int32_t side, const void* blob, size_t len) {
+    DLB_REQUIRE(lat);
+    DLB_REQUIRE(blob);
+    if (side != 0 && side != 1) return fail(DLB_ERROR_INVALID_ARGUMENT, "side must be 0 or 1");
+    return guarded([&] { lat->lat->link_ipc(side, blob, len); });
+}
+
+// Step several slabs of one process together, one step at a time, so that no
+// slab's queued halo waits can starve another slab's launches.
+DLB_API dlb_status dlb_lattices_step(dlb_lattice** lats, size_t n, int64_t nsteps) {
+    DLB_REQUIRE(lats || n == 0);
+    return guarded([&] {
+        for (size_t k = 0; k < n; ++k) lats[k]->lat->check_dispatch();
+        for (int64_t s = 0; s < nsteps; ++s)
+            for (size_t k = 0; k < n; ++k) lats[k]->lat->enqueue_step();
+    });
+}
+
+DLB_API dlb_status dlb_collide_and_stream(const dlb_registry* reg, dlb_block_view* block,
+                                          const int32_t* dispatch_tags, size_t n_dispatch,
+                                          int32_t nthreads) {
+    DLB_REQUIRE(reg);
+    DLB_REQUIRE(block);
+    DLB_REQUIRE(block->f_in && block->tag && block->param_index);
+    DLB_REQUIRE(dispatch_tags || n_dispatch == 0);
+    (void)nthreads;  // the CUDA grid replaces the z-split threads (accelerated_lattice.cpp:183-198)
+    return guarded([&] {
+        const int64_t nx = block->interior[0], ny = block->interior[1], nz = block->interior[2];
+        if (nx < 1 || ny < 1 || nz < 1) throw std::invalid_argument("block extents must be >= 1");
+        const int64_t ext[3] = {nx + 2, ny + 2, nz + 2};
+        // Eager tag scan (accelerated_lattice.cpp:161-181): fail before any write.
+        std::vector<int32_t> slots(size_t(nx * ny * nz));
+        std::vector<char> seen_tag(size_t(reg->reg.num_tags()) + 1, 0);
+        bool untagged = false;
+        int64_t k = 0;
+        for (int64_t z = 1; z <= nz; ++z)
+            for (int64_t y = 1; y <= ny; ++y) {
+                const int64_t row = (z * ext[1] + y) * ext[0];
+                for (int64_t x = 1; x <= nx; ++x, ++k) {
+                    const int32_t t = block->tag[row + x];
+                    if (t < 0 || t >= reg->reg.num_tags()) untagged = untagged || t < 0;
+                    else seen_tag[size_t(t)] = 1;
+                    slots[size_t(k)] = block->param_index[row + x];
+                }
+            }
+        std::vector<char> allowed(seen_tag.size(), 0);
+        for (size_t d = 0; d < n_dispatch; ++d)
+            if (dispatch_tags[d] >= 0 && size_t(dispatch_tags[d]) < allowed.size())
+                allowed[size_t(dispatch_tags[d])] = 1;
+        if (untagged) throw dlb::DispatchError("<untagged cell>");
+        for (int t = 0; t < reg->reg.num_tags(); ++t)
+            if (seen_tag[size_t(t)] && !allowed[size_t(t)])
+                throw dlb::DispatchError(reg->reg.chain_for(t));
+
+        std::lock_guard<std::mutex> lock(g_block_mu);
+        const std::vector<int64_t> key = {nx, ny, nz, block->q, block->precision_bits};
+        BlockCtx& ctx = g_blocks[key];
+        if (!ctx.lat || ctx.reg != reg || ctx.instances != reg->reg.num_instances()) {
+            dlb_lattice_desc d{};
+            d.dims[0] = nx;
+            d.dims[1] = ny;
+            d.dims[2] = nz;
+            d.q = block->q;
+            d.precision_bits = block->precision_bits;
+            d.layout = DLB_LAYOUT_TWO_POP;
+            d.arith = DLB_ARITH_EXACT;
+            d.global_nz = nz;
+            ctx.lat.reset();
+            ctx.lat = std::make_unique<dlb::Lattice>(d, reg->reg);  // envelope on every axis
+            ctx.lat->set_periodic_override(false, false, false);
+            ctx.reg = reg;
+            ctx.instances = reg->reg.num_instances();
+            ctx.slots.clear();
+        }
+        if (ctx.slots != slots) {
+            ctx.lat->set_slots(slots.data());
+            ctx.slots = slots;
+        }
+        const size_t bytes = size_t(block->q) * size_t(ext[0] * ext[1] * ext[2]) *
+                             size_t(block->precision_bits / 8);
+        ctx.lat->upload_block(block->f_in, ext);
+        ctx.lat->enqueue_step();
+        if (block->f_out) std::memcpy(block->f_out, block->f_in, bytes);
+        ctx.lat->download_block_interior(block->f_in, ext, 0);
+        ctx.lat->synchronize();
+    });
+}
+
+DLB_API dlb_status dlb_host_alloc(size_t bytes, void** out) {
+    DLB_REQUIRE(out);
+    return guarded([&] { dlb::cuda_check(cudaMallocHost(out, bytes), "cudaMallocHost"); });
+}
+
+DLB_API void dlb_host_free(void* ptr) {
+    if (ptr) cudaFreeHost(ptr);
+}
+
+DLB_API dlb_status dlb_case_sphere_pack(int64_t nx, int64_t ny, int64_t nz, double radius,
+                                        double target_porosity, uint64_t seed, uint8_t* out,
+                                        double* porosity_out) {
+    DLB_REQUIRE(out);
+    return guarded([&] {
+        const double phi = dlb::sphere_pack(nx, ny, nz, radius, target_porosity, seed, out);
+        if (porosity_out) *porosity_out = phi;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,127 @@
+// Fused collide-and-stream kernels for sm_100a.
+//
+// Replaces the reference hot path collide_and_stream<T> -> step_range<T> ->
+// ChainRecipe<T>::apply (proj/src/accelerated_lattice.cpp:126-200,
+// proj/include/dolb/chain.hpp:104-144): one thread per cell pulls its q
+// populations from the neighbours' post-collision state (two-population
+// scheme, f_in -> f_out), applies the cell's dynamics from the per-slot recipe
+// table, and stores q values. Periodic axes wrap in-kernel; non-periodic axes
+// read the zero envelope (reference_lattice.cpp:240-254) or, for a z-slab of a
+// decomposed domain, the ghost plane filled by the neighbour's halo push.
+//
+// This translation unit is compiled twice: DLB_MODE = exact with -fmad=false
+// (bit-identical to the reference CPU solver) and DLB_MODE = fast with FMA
+// contraction.
+#include "kernels.cuh"
+
+#ifndef DLB_MODE
+#error "define DLB_MODE (exact or fast)"
+#endif
+
+namespace dlb {
+namespace DLB_MODE {
+
+template <typename T, int Q, unsigned KM>
+__global__ void __launch_bounds__(256) k_pull(const __grid_constant__ StepArgs<T> a) {
+    using L = Lat<Q>;
+    const Geo& g = a.g;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    const int z = a.z_begin + int(blockIdx.z) * a.z_step;
+    const bool active = x < g.nx && y < g.ny;
+    if (active) {
+        // Source coordinates of the pull f_i(x) <- f_i(x - c_i).
+        const int xm = (x == 0 && g.per_x) ? g.nx - 1 : x - 1;
+        const int xp = (x == g.nx - 1 && g.per_x) ? 0 : x + 1;
+        const int ym = (y == 0 && g.per_y) ? g.ny - 1 : y - 1;
+        const int yp = (y == g.ny - 1 && g.per_y) ? 0 : y + 1;
+        const int zm = (z == 0 && g.per_z) ? g.nz - 1 : z - 1;
+        const int zp = (z == g.nz - 1 && g.per_z) ? 0 : z + 1;
+
+        T f[Q];
+        sfor<Q>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            constexpr int cx = L::c[i][0], cy = L::c[i][1], cz = L::c[i][2];
+            const int sx = cx > 0 ? xm : (cx < 0 ? xp : x);
+            const int sy = cy > 0 ? ym : (cy < 0 ? yp : y);
+            const int sz = cz > 0 ? zm : (cz < 0 ? zp : z);
+            f[i] = __ldg(a.fin + i * g.dstride + (sz * g.plane + sy * g.pitch + sx));
+        });
+
+        int s = a.uniform_slot;
+        if (a.slot != nullptr) s = a.slot[(static_cast<long long>(z) * g.ny + y) * g.nx + x];
+        Cell<T, Q>::template apply<KM>(f, a.rec[s]);
+
+        const int center = z * g.plane + y * g.pitch + x;
+        sfor<Q>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            a.fout[i * g.dstride + center] = f[i];
+        });
+
+        if (a.push_up != nullptr && z == g.nz - 1) {
+            const int ghost = -g.plane + y * g.pitch + x;
+            sfor<Q>([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                if constexpr (L::c[i][2] > 0) a.push_up[i * a.up_dstride + ghost] = f[i];
+            });
+        }
+        if (a.push_down != nullptr && z == 0) {
+            const int ghost = a.down_ghost_z * g.plane + y * g.pitch + x;
+            sfor<Q>([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                if constexpr (L::c[i][2] < 0) a.push_down[i * a.down_dstride + ghost] = f[i];
+            });
+        }
+    }
+
+    if (a.counter != nullptr) {
+        // Publish this block's peer stores at system scope, then take a ticket.
+        __threadfence_system();
+        __syncthreads();
+        if (threadIdx.x == 0 && threadIdx.y == 0) {
+            const unsigned total = gridDim.x * gridDim.y * gridDim.z;
+            const unsigned ticket = atomicAdd(a.counter, 1u);
+            if (ticket == total - 1) {
+                __threadfence_system();
+                *a.counter = 0u;
+                const unsigned long long s = *a.my_step + 1ull;
+                *a.my_step = s;
+                if (a.sig_up != nullptr)
+                    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a.sig_up), "l"(s) : "memory");
+                if (a.sig_down != nullptr)
+                    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a.sig_down), "l"(s) : "memory");
+            }
+        }
+    }
+}
+
+#define DLB_STR2(x) #x
+#define DLB_STR(x) DLB_STR2(x)
+#define ENTRY(T, Q, KM)                                                                  \
+    KernelEntry {                                                                        \
+        int(sizeof(T) * 8), Q, unsigned(KM), LAYOUT_TWO_POP,                              \
+            reinterpret_cast<const void*>(&k_pull<T, Q, unsigned(KM)>),                   \
+            "k_pull<" #T ",D3Q" #Q "," #KM ">[" DLB_STR(DLB_MODE) "]"                      \
+    }
+
+#define Q19_SET(T)                                                                        \
+    ENTRY(T, 19, KM_BGK), ENTRY(T, 19, KM_TRT), ENTRY(T, 19, KM_RR),                      \
+        ENTRY(T, 19, KM_BGK | KM_BB | KM_MBB), ENTRY(T, 19, KM_TRT | KM_BB | KM_MBB),    \
+        ENTRY(T, 19, KM_RR | KM_BB | KM_MBB),                                             \
+        ENTRY(T, 19, KM_BGK | KM_BB | KM_NODYN | KM_REGV | KM_REGP),                      \
+        ENTRY(T, 19, KM_TRT | KM_BB | KM_NODYN | KM_REGV | KM_REGP),                      \
+        ENTRY(T, 19, KM_RR | KM_BB | KM_NODYN | KM_REGV | KM_REGP), ENTRY(T, 19, KM_ALL)
+
+#define Q27_SET(T) ENTRY(T, 27, KM_BGK), ENTRY(T, 27, KM_TRT), ENTRY(T, 27, KM_RR), ENTRY(T, 27, KM_ALL)
+
+static const KernelEntry kTable[] = {
+    Q19_SET(float), Q19_SET(double), Q27_SET(float), Q27_SET(double),
+};
+
+const KernelEntry* kernel_table(int* n) {
+    *n = int(sizeof(kTable) / sizeof(kTable[0]));
+    return kTable;
+}
+
+}  // namespace DLB_MODE
+}  // namespace dlb

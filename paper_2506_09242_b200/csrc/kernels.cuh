@@ -1,0 +1,74 @@
+// Launch-side description of the collide-and-stream kernels, shared by the
+// kernel translation units (compiled once per arithmetic mode) and the host.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "lbm_cell.cuh"
+
+namespace dlb {
+
+constexpr int kMaxSlots = 16;
+
+// Device layout of one direction array (SoA, envelope-inclusive):
+//   element (x, y, z) of direction i, with x in [-1, nx], y in [-1, ny],
+//   z in [-1, nz] (the -1 / n layers are the envelope / ghost planes), sits at
+//   base_i + z*plane + y*pitch + x, where base_i points at interior (0,0,0).
+//   pitch >= nx + 2 is a multiple of 128 B, and base_i is 128 B aligned, so
+//   every interior row starts on a cache line; x = -1 lives in the previous
+//   row's padding.
+struct Geo {
+    int nx, ny, nz;
+    int pitch;        // elements per row
+    int plane;        // pitch * (ny + 2)
+    int per_x, per_y, per_z;  // wrap in-kernel along this axis (else read the envelope)
+    long long dstride;        // elements per direction array
+};
+
+template <typename T>
+struct StepArgs {
+    const T* fin;           // direction 0, interior origin
+    T* fout;
+    const uint8_t* slot;    // nx*ny*nz registry slots (x fastest) or nullptr if uniform
+    int uniform_slot;
+    int z_begin, z_step;    // plane z = z_begin + blockIdx.z * z_step
+    Geo g;
+    // z-slab halo push over peer memory (nullptr when absent): after the
+    // collision, cells of the top plane store their c_z = +1 populations into
+    // the upper neighbour's ghost plane z = -1, cells of the bottom plane their
+    // c_z = -1 populations into the lower neighbour's ghost plane z = nz_lower.
+    T* push_up;
+    T* push_down;
+    long long up_dstride, down_dstride;
+    int down_ghost_z;
+    // Completion signal of the boundary launch (nullptr otherwise): every
+    // block fences its peer stores, the last block (ticket == gridsize - 1)
+    // increments *my_step and release-stores it into both neighbours' flags.
+    unsigned int* counter;
+    unsigned long long* my_step;
+    unsigned long long* sig_up;
+    unsigned long long* sig_down;
+    DevRecipe<T> rec[kMaxSlots];
+};
+
+enum Layout : int { LAYOUT_TWO_POP = 0, LAYOUT_AA = 1 };
+
+using StepKernelF = void (*)(StepArgs<float>);
+using StepKernelD = void (*)(StepArgs<double>);
+
+struct KernelEntry {
+    int precision_bits;
+    int q;
+    unsigned km;
+    int layout;
+    const void* fn;  // __global__ function pointer
+    const char* name;
+};
+
+// Kernel tables of the two arithmetic modes (one translation unit each).
+namespace exact { const KernelEntry* kernel_table(int* n); }
+namespace fast { const KernelEntry* kernel_table(int* n); }
+
+}  // namespace dlb

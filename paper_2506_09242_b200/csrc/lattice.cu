@@ -1,0 +1,761 @@
+// Device lattice runtime (see lattice.hpp). Compiled with -fmad=false: the
+// initialisation kernels evaluate equilibrium2<T> and the TGV state with the
+// reference's operation order (multiblock.cpp:278-281, cases.cpp:145-156).
+#include "lattice.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <random>
+
+namespace dlb {
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw DeviceError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+namespace {
+
+constexpr std::size_t kStagingBytes = std::size_t(256) << 20;
+
+// ---------------------------------------------------------------------------
+// auxiliary kernels
+
+template <typename T>
+__device__ __forceinline__ long long lin(const Geo& g, int x, int y, int z) {
+    return static_cast<long long>(z) * g.plane + static_cast<long long>(y) * g.pitch + x;
+}
+
+// Stored state := equilibrium2<T>(T(rho), T(u)) for planes [z0, z0 + nzc).
+template <typename T, int Q>
+__global__ void k_fill_eq(T* origin, Geo g, const double* rho, const double* ux,
+                          const double* uy, const double* uz, int z0, int nzc) {
+    const long long n = static_cast<long long>(g.nx) * g.ny * nzc;
+    for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
+         c += (long long)gridDim.x * blockDim.x) {
+        const int x = int(c % g.nx);
+        const int y = int((c / g.nx) % g.ny);
+        const int z = z0 + int(c / (static_cast<long long>(g.nx) * g.ny));
+        const T r = T(rho[c]);
+        const T u[3] = {T(ux[c]), T(uy[c]), T(uz[c])};
+        const T usqr = Cell<T, Q>::usqr_of(u);
+        const long long at = lin<T>(g, x, y, z);
+        sfor<Q>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            origin[i * g.dstride + at] = Cell<T, Q>::template eq2<i>(r, u, usqr);
+        });
+    }
+}
+
+// Taylor-Green vortex state (cases.cpp:145-156) from host-evaluated per-index
+// sin / cos / cos(2x) tables (glibc, as the reference), then equilibrium2<T>.
+template <typename T, int Q>
+__global__ void k_fill_tgv(T* origin, Geo g, const double* s1, const double* c1,
+                           const double* c2, long long z_origin, double u_inf) {
+    const long long n = static_cast<long long>(g.nx) * g.ny * g.nz;
+    for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
+         c += (long long)gridDim.x * blockDim.x) {
+        const int x = int(c % g.nx);
+        const int y = int((c / g.nx) % g.ny);
+        const int z = int(c / (static_cast<long long>(g.nx) * g.ny));
+        const long long k = z_origin + z;
+        const double dp = u_inf * u_inf / 16.0 * (c2[k] + 2.0) * (c2[x] + c2[y]);
+        const double rho = 1.0 + dp / (1.0 / 3.0);
+        const double ux = u_inf * s1[x] * c1[y] * c1[k];
+        const double uy = -u_inf * c1[x] * s1[y] * c1[k];
+        const T r = T(rho);
+        const T u[3] = {T(ux), T(uy), T(0.0)};
+        const T usqr = Cell<T, Q>::usqr_of(u);
+        const long long at = lin<T>(g, x, y, z);
+        sfor<Q>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            origin[i * g.dstride + at] = Cell<T, Q>::template eq2<i>(r, u, usqr);
+        });
+    }
+}
+
+// Box copy between the padded layout of one direction and a dense buffer
+// (x fastest). The box origin (bx0, by0, bz0) may be -1 (envelope).
+template <typename TD, typename TS, bool TO_LAYOUT>
+__global__ void k_box_copy(TD* dst, const TS* src, Geo g, int bx0, int by0, int bz0, int ex,
+                           int ey, int ez) {
+    const long long n = static_cast<long long>(ex) * ey * ez;
+    for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
+         c += (long long)gridDim.x * blockDim.x) {
+        const int x = bx0 + int(c % ex);
+        const int y = by0 + int((c / ex) % ey);
+        const int z = bz0 + int(c / (static_cast<long long>(ex) * ey));
+        if constexpr (TO_LAYOUT) dst[lin<TD>(g, x, y, z)] = TD(src[c]);
+        else dst[c] = TD(src[lin<TS>(g, x, y, z)]);
+    }
+}
+
+// Halo wait: block the stream until both neighbours finished the boundary
+// planes of the step this slab completed last (flags[0] from the lower,
+// flags[1] from the upper neighbour; flags[2] = own completed steps). Gives up
+// after `timeout_ns` and raises flags[3] (reported as an exchange error).
+__global__ void k_halo_wait(unsigned long long* flags, int have_lower, int have_upper,
+                            unsigned long long timeout_ns) {
+    const unsigned long long target = flags[2];
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+        unsigned long long lo = target, up = target;
+        if (have_lower) asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(lo) : "l"(flags));
+        if (have_upper)
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(up) : "l"(flags + 1));
+        if (lo >= target && up >= target) return;
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > timeout_ns) {
+            flags[3] = target + 1;
+            return;
+        }
+        __nanosleep(200);
+    }
+}
+
+int grid_for(long long n) {
+    long long b = (n + 255) / 256;
+    return int(std::min<long long>(std::max<long long>(b, 1), 148LL * 32));
+}
+
+const KernelEntry* find_kernel(int arith, int bits, int q, unsigned km, int layout) {
+    int n = 0;
+    const KernelEntry* t = arith == DLB_ARITH_FAST ? fast::kernel_table(&n) : exact::kernel_table(&n);
+    const KernelEntry* best = nullptr;
+    for (int k = 0; k < n; ++k) {
+        const KernelEntry& e = t[k];
+        if (e.precision_bits != bits || e.q != q || e.layout != layout) continue;
+        if ((e.km & km) != km) continue;
+        if (!best || __builtin_popcount(e.km) < __builtin_popcount(best->km)) best = &e;
+    }
+    return best;
+}
+
+template <typename T>
+DevRecipe<T> compile_recipe(const DynamicsChain& ch) {
+    // compile_chain<T> (chain.hpp:147-187): parameters cast to T; the TRT odd
+    // rate derived in double from the T-cast values (chain.hpp:132-135).
+    DevRecipe<T> r{};
+    const ChainParams& p = ch.params;
+    r.omega = T(p.omega);
+    r.lambda = T(p.lambda);
+    r.smagorinsky_c = T(p.smagorinsky_c);
+    r.omega_bulk_ho = T(p.omega_bulk_ho);
+    r.target_rho = T(p.target_rho);
+    for (int a = 0; a < 3; ++a) r.wall_velocity[a] = T(p.wall_velocity[a]);
+    r.omega_minus = T(derive_omega_minus(double(r.omega), double(r.lambda)));
+    r.kind = KIND_NODYN;
+    for (const ChainLink& l : ch.links) {
+        switch (l.type) {
+            case LinkType::NoDynamics: r.kind = KIND_NODYN; break;
+            case LinkType::BounceBack: r.kind = KIND_BB; break;
+            case LinkType::MovingBounceBack: r.kind = KIND_MBB; break;
+            case LinkType::BGK: r.kind = KIND_COLLIDE; r.base = BASE_BGK; break;
+            case LinkType::TRT: r.kind = KIND_COLLIDE; r.base = BASE_TRT; break;
+            case LinkType::RR: r.kind = KIND_COLLIDE; r.base = BASE_RR; break;
+            case LinkType::Smagorinsky: r.has_les = 1; break;
+            case LinkType::RegularizedVelocity:
+            case LinkType::RegularizedPressure:
+                r.has_reg = 1;
+                r.reg_is_pressure = l.type == LinkType::RegularizedPressure;
+                r.reg_axis = l.axis;
+                r.reg_orient = l.orient;
+                break;
+        }
+    }
+    return r;
+}
+
+unsigned kind_bits(const DynamicsChain& ch) {
+    unsigned km = 0;
+    for (const ChainLink& l : ch.links) {
+        switch (l.type) {
+            case LinkType::NoDynamics: km |= KM_NODYN; break;
+            case LinkType::BounceBack: km |= KM_BB; break;
+            case LinkType::MovingBounceBack: km |= KM_MBB; break;
+            case LinkType::BGK: km |= KM_BGK; break;
+            case LinkType::TRT: km |= KM_TRT; break;
+            case LinkType::RR: km |= KM_RR; break;
+            case LinkType::Smagorinsky: km |= KM_LES; break;
+            case LinkType::RegularizedVelocity: km |= KM_REGV; break;
+            case LinkType::RegularizedPressure: km |= KM_REGP; break;
+        }
+    }
+    return km;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+
+Lattice::Lattice(const dlb_lattice_desc& desc, const DynamicsRegistry& reg) : d_(desc) {
+    if (d_.q != 19 && d_.q != 27) throw std::invalid_argument("q must be 19 or 27");
+    if (d_.precision_bits != 32 && d_.precision_bits != 64)
+        throw std::invalid_argument("precision must be 32 or 64");
+    if (d_.layout != DLB_LAYOUT_TWO_POP)
+        throw std::invalid_argument("layout not supported by this build (two-population only)");
+    if (d_.arith != DLB_ARITH_EXACT && d_.arith != DLB_ARITH_FAST)
+        throw std::invalid_argument("arith must be DLB_ARITH_EXACT or DLB_ARITH_FAST");
+    for (int a = 0; a < 3; ++a)
+        if (d_.dims[a] < 1) throw std::invalid_argument("block extents must be >= 1");
+    if (d_.global_nz < d_.dims[2] || d_.z_origin < 0 || d_.z_origin + d_.dims[2] > d_.global_nz)
+        throw std::invalid_argument("slab z range outside the global domain");
+    if (reg.num_instances() > kMaxSlots)
+        throw std::invalid_argument("registry holds " + std::to_string(reg.num_instances()) +
+                                    " instances; the device recipe table holds at most " +
+                                    std::to_string(kMaxSlots));
+    for (int s = 0; s < reg.num_instances(); ++s) {
+        chains_.push_back(reg.chain_at_slot(s));
+        tag_of_slot_.push_back(reg.tag_of_slot(s));
+    }
+    for (int t = 0; t < reg.num_tags(); ++t) tag_names_.push_back(reg.chain_for(t));
+
+    device_ = d_.device;
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+    cuda_check(cudaEventCreate(&ev0_), "cudaEventCreate");
+    cuda_check(cudaEventCreate(&ev1_), "cudaEventCreate");
+
+    const int s = d_.precision_bits / 8;
+    align_ = 128 / s;
+    const long long nx = d_.dims[0], ny = d_.dims[1], nz = d_.dims[2];
+    const long long pitch = (nx + 2 + align_ - 1) / align_ * align_;
+    const long long plane = pitch * (ny + 2);
+    const long long dstride = plane * (nz + 2) + align_;  // + align: room for x = -1 of row 0
+    if (plane * (nz + 2) + 2 * align_ > (1LL << 31) - 1)
+        throw std::invalid_argument("slab too large for 32-bit in-array offsets");
+    geo_.nx = int(nx);
+    geo_.ny = int(ny);
+    geo_.nz = int(nz);
+    geo_.pitch = int(pitch);
+    geo_.plane = int(plane);
+    geo_.dstride = dstride;
+    geo_.per_x = d_.periodic[0] != 0;
+    geo_.per_y = d_.periodic[1] != 0;
+    geo_.per_z = d_.periodic[2] != 0 && !split();
+    base_off_ = align_ + plane + pitch;  // interior (0,0,0)
+
+    const std::size_t bytes = std::size_t(d_.q) * std::size_t(dstride) * std::size_t(s);
+    for (int b = 0; b < 2; ++b) {
+        cuda_check(cudaMalloc(&buf_[b], bytes), "cudaMalloc populations");
+        cuda_check(cudaMemsetAsync(buf_[b], 0, bytes, stream_), "cudaMemset populations");
+    }
+    device_bytes_ = int64_t(2 * bytes);
+    cuda_check(cudaMalloc(&d_flags_, 4 * sizeof(unsigned long long)), "cudaMalloc flags");
+    cuda_check(cudaMemsetAsync(d_flags_, 0, 4 * sizeof(unsigned long long), stream_), "memset");
+    cuda_check(cudaMalloc(&d_counter_, sizeof(unsigned int)), "cudaMalloc counter");
+    cuda_check(cudaMemsetAsync(d_counter_, 0, sizeof(unsigned int), stream_), "memset");
+    staging_bytes_ = kStagingBytes;
+    cuda_check(cudaMalloc(&staging_, staging_bytes_), "cudaMalloc staging");
+    cuda_check(cudaStreamSynchronize(stream_), "init");
+}
+
+Lattice::~Lattice() {
+    cudaSetDevice(device_);
+    if (stream_) cudaStreamSynchronize(stream_);
+    for (Peer* p : {&lower_, &upper_})
+        for (void* v : p->ipc_opened) cudaIpcCloseMemHandle(v);
+    for (void* b : buf_) cudaFree(b);
+    cudaFree(d_slot_);
+    cudaFree(d_flags_);
+    cudaFree(d_counter_);
+    cudaFree(staging_);
+    if (ev0_) cudaEventDestroy(ev0_);
+    if (ev1_) cudaEventDestroy(ev1_);
+    if (stream_) cudaStreamDestroy(stream_);
+}
+
+void* Lattice::origin(int which) const {
+    return static_cast<char*>(buf_[which]) + base_off_ * (d_.precision_bits / 8);
+}
+
+int64_t Lattice::bytes_per_cell() const {
+    // populations read once + written once; the u8 slot read when not uniform
+    return int64_t(2) * d_.q * (d_.precision_bits / 8) + (d_slot_ ? 1 : 0);
+}
+
+int Lattice::launches_per_step() const {
+    const bool linked = lower_.linked || upper_.linked;
+    if (!linked) return 1;
+    return 1 + 1 + (geo_.nz > 2 ? 1 : 0);  // wait + boundary + interior
+}
+
+void Lattice::set_periodic_override(bool x, bool y, bool z) {
+    geo_.per_x = x;
+    geo_.per_y = y;
+    geo_.per_z = z;
+}
+
+void Lattice::set_slots(const int32_t* slots) {
+    const long long n = cells();
+    std::vector<uint8_t> u8(std::size_t(n), 0);
+    std::vector<char> seen(chains_.size(), 0);
+    untagged_ = false;
+    int first = -2;
+    bool uniform = true;
+    for (long long c = 0; c < n; ++c) {
+        const int32_t s = slots[c];
+        if (s < 0) {
+            untagged_ = true;
+            uniform = false;
+            continue;
+        }
+        if (s >= int32_t(chains_.size()))
+            throw std::invalid_argument("slot " + std::to_string(s) + " is not registered");
+        seen[std::size_t(s)] = 1;
+        u8[std::size_t(c)] = uint8_t(s);
+        if (first == -2) first = s;
+        else if (s != first) uniform = false;
+    }
+    present_slots_.clear();
+    for (std::size_t s = 0; s < seen.size(); ++s)
+        if (seen[s]) present_slots_.push_back(int32_t(s));
+    cudaFree(d_slot_);
+    d_slot_ = nullptr;
+    if (uniform && first >= 0) {
+        uniform_slot_ = first;
+    } else {
+        uniform_slot_ = 0;
+        cuda_check(cudaMalloc(&d_slot_, std::size_t(n)), "cudaMalloc slots");
+        cuda_check(cudaMemcpy(d_slot_, u8.data(), std::size_t(n), cudaMemcpyHostToDevice),
+                   "upload slots");
+    }
+    slots_set_ = true;
+    select_kernel();
+}
+
+void Lattice::set_uniform_slot(int32_t slot) {
+    if (slot < 0 || slot >= int32_t(chains_.size()))
+        throw std::invalid_argument("slot " + std::to_string(slot) + " is not registered");
+    cudaFree(d_slot_);
+    d_slot_ = nullptr;
+    uniform_slot_ = slot;
+    untagged_ = false;
+    present_slots_ = {slot};
+    slots_set_ = true;
+    select_kernel();
+}
+
+void Lattice::select_kernel() {
+    km_needed_ = 0;
+    for (int32_t s : present_slots_) km_needed_ |= kind_bits(chains_[std::size_t(s)]);
+    kernel_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_, d_.layout);
+    if (!kernel_) throw std::invalid_argument("no kernel instantiation covers this dynamics set");
+}
+
+void Lattice::set_dispatch(const int32_t* tags, std::size_t n) {
+    dispatch_.clear();
+    for (std::size_t k = 0; k < n; ++k) dispatch_.insert(tags[k]);
+    dispatch_set_ = true;
+}
+
+// accelerated_lattice.cpp:161-181: fail before any write, naming the chain.
+void Lattice::check_dispatch() const {
+    if (!slots_set_) throw std::invalid_argument("cell dynamics not assigned (set slots first)");
+    if (untagged_) throw DispatchError("<untagged cell>");
+    std::set<int> present;
+    for (int32_t s : present_slots_) present.insert(tag_of_slot_[std::size_t(s)]);
+    for (int t : present) {
+        const bool ok = dispatch_set_ ? dispatch_.count(t) != 0 : true;
+        if (!ok) throw DispatchError(tag_names_[std::size_t(t)]);
+    }
+    if (split() && d_.periodic[2] && !(lower_.linked && upper_.linked))
+        throw ExchangeError("periodic z-slab is not linked to both neighbours");
+}
+
+void Lattice::fill_equilibrium(const double* rho, const double* ux, const double* uy,
+                               const double* uz) {
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    const long long plane_cells = (long long)geo_.nx * geo_.ny;
+    const int zc = int(std::max<long long>(1, (long long)(staging_bytes_ / 32) / plane_cells));
+    double* st = static_cast<double*>(staging_);
+    for (int z0 = 0; z0 < geo_.nz; z0 += zc) {
+        const int nzc = std::min(zc, geo_.nz - z0);
+        const long long n = plane_cells * nzc;
+        if (n * 32 > (long long)staging_bytes_) throw std::invalid_argument("plane too large");
+        const long long off = plane_cells * z0;
+        cuda_check(cudaMemcpyAsync(st, rho + off, n * 8, cudaMemcpyHostToDevice, stream_), "h2d");
+        cuda_check(cudaMemcpyAsync(st + n, ux + off, n * 8, cudaMemcpyHostToDevice, stream_), "h2d");
+        cuda_check(cudaMemcpyAsync(st + 2 * n, uy + off, n * 8, cudaMemcpyHostToDevice, stream_), "h2d");
+        cuda_check(cudaMemcpyAsync(st + 3 * n, uz + off, n * 8, cudaMemcpyHostToDevice, stream_), "h2d");
+        const int grid = grid_for(n);
+        void* o = origin(cur_);
+        if (d_.precision_bits == 64) {
+            if (d_.q == 19) k_fill_eq<double, 19><<<grid, 256, 0, stream_>>>((double*)o, geo_, st, st + n, st + 2 * n, st + 3 * n, z0, nzc);
+            else k_fill_eq<double, 27><<<grid, 256, 0, stream_>>>((double*)o, geo_, st, st + n, st + 2 * n, st + 3 * n, z0, nzc);
+        } else {
+            if (d_.q == 19) k_fill_eq<float, 19><<<grid, 256, 0, stream_>>>((float*)o, geo_, st, st + n, st + 2 * n, st + 3 * n, z0, nzc);
+            else k_fill_eq<float, 27><<<grid, 256, 0, stream_>>>((float*)o, geo_, st, st + n, st + 2 * n, st + 3 * n, z0, nzc);
+        }
+        cuda_check(cudaGetLastError(), "k_fill_eq");
+        cuda_check(cudaStreamSynchronize(stream_), "fill_equilibrium");
+    }
+}
+
+void Lattice::fill_tgv(int64_t L, double u_inf) {
+    if (d_.dims[0] != L || d_.dims[1] != L || d_.global_nz != L)
+        throw std::invalid_argument("TGV fill needs an L^3 domain");
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    // cases.cpp:145-156: x = 2 pi / L * (i + 0.5); glibc sin / cos on the host.
+    const double scale = 2.0 * 3.14159265358979323846 / double(L);
+    std::vector<double> tab(std::size_t(3 * L));
+    for (int64_t i = 0; i < L; ++i) {
+        const double x = scale * (double(i) + 0.5);
+        tab[std::size_t(i)] = std::sin(x);
+        tab[std::size_t(L + i)] = std::cos(x);
+        tab[std::size_t(2 * L + i)] = std::cos(2.0 * x);
+    }
+    double* st = static_cast<double*>(staging_);
+    cuda_check(cudaMemcpyAsync(st, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, stream_), "h2d");
+    const int grid = grid_for(cells());
+    void* o = origin(cur_);
+    if (d_.precision_bits == 64) {
+        if (d_.q == 19) k_fill_tgv<double, 19><<<grid, 256, 0, stream_>>>((double*)o, geo_, st, st + L, st + 2 * L, d_.z_origin, u_inf);
+        else k_fill_tgv<double, 27><<<grid, 256, 0, stream_>>>((double*)o, geo_, st, st + L, st + 2 * L, d_.z_origin, u_inf);
+    } else {
+        if (d_.q == 19) k_fill_tgv<float, 19><<<grid, 256, 0, stream_>>>((float*)o, geo_, st, st + L, st + 2 * L, d_.z_origin, u_inf);
+        else k_fill_tgv<float, 27><<<grid, 256, 0, stream_>>>((float*)o, geo_, st, st + L, st + 2 * L, d_.z_origin, u_inf);
+    }
+    cuda_check(cudaGetLastError(), "k_fill_tgv");
+    cuda_check(cudaStreamSynchronize(stream_), "fill_tgv");
+}
+
+// Canonical (direction-major, x fastest, interior only) <-> device layout,
+// chunked over z planes through the staging buffer.
+void Lattice::copy_canonical(void* host, bool to_device, bool as_double, int elem_bytes) {
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    const long long plane_cells = (long long)geo_.nx * geo_.ny;
+    const long long n = cells();
+    const int zc = int(std::max<long long>(1, (long long)staging_bytes_ / (8 * plane_cells)));
+    for (int i = 0; i < d_.q; ++i) {
+        for (int z0 = 0; z0 < geo_.nz; z0 += zc) {
+            const int nzc = std::min(zc, geo_.nz - z0);
+            const long long cnt = plane_cells * nzc;
+            char* h = static_cast<char*>(host) + (std::size_t(i) * n + plane_cells * z0) * elem_bytes;
+            const int grid = grid_for(cnt);
+            char* o = static_cast<char*>(origin(cur_)) + std::size_t(i) * geo_.dstride * (d_.precision_bits / 8);
+            if (to_device) {
+                cuda_check(cudaMemcpyAsync(staging_, h, cnt * elem_bytes, cudaMemcpyHostToDevice, stream_), "h2d");
+                if (d_.precision_bits == 64)
+                    k_box_copy<double, double, true><<<grid, 256, 0, stream_>>>((double*)o, (const double*)staging_, geo_, 0, 0, z0, geo_.nx, geo_.ny, nzc);
+                else if (as_double)
+                    k_box_copy<float, double, true><<<grid, 256, 0, stream_>>>((float*)o, (const double*)staging_, geo_, 0, 0, z0, geo_.nx, geo_.ny, nzc);
+                else
+                    k_box_copy<float, float, true><<<grid, 256, 0, stream_>>>((float*)o, (const float*)staging_, geo_, 0, 0, z0, geo_.nx, geo_.ny, nzc);
+                cuda_check(cudaGetLastError(), "k_box_copy");
+            } else {
+                if (d_.precision_bits == 64)
+                    k_box_copy<double, double, false><<<grid, 256, 0, stream_>>>((double*)staging_, (const double*)o, geo_, 0, 0, z0, geo_.nx, geo_.ny, nzc);
+                else if (as_double)
+                    k_box_copy<double, float, false><<<grid, 256, 0, stream_>>>((double*)staging_, (const float*)o, geo_, 0, 0, z0, geo_.nx, geo_.ny, nzc);
+                else
+                    k_box_copy<float, float, false><<<grid, 256, 0, stream_>>>((float*)staging_, (const float*)o, geo_, 0, 0, z0, geo_.nx, geo_.ny, nzc);
+                cuda_check(cudaGetLastError(), "k_box_copy");
+                cuda_check(cudaMemcpyAsync(h, staging_, cnt * elem_bytes, cudaMemcpyDeviceToHost, stream_), "d2h");
+            }
+            cuda_check(cudaStreamSynchronize(stream_), "copy_canonical");
+        }
+    }
+}
+
+void Lattice::upload(const double* canon) { copy_canonical(const_cast<double*>(canon), true, true, 8); }
+void Lattice::download(double* canon) { copy_canonical(canon, false, true, 8); }
+void Lattice::download_raw(void* canon) {
+    copy_canonical(canon, false, d_.precision_bits == 64, d_.precision_bits / 8);
+}
+
+// Envelope-inclusive AcceleratedBlock arrays: the whole (nx+2)(ny+2)(nz+2)
+// box of every direction, including the envelope the caller refreshed.
+void Lattice::upload_block(const void* f, const int64_t ext[3]) {
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    const int s = d_.precision_bits / 8;
+    const long long vol = ext[0] * ext[1] * ext[2];
+    const long long plane_cells = ext[0] * ext[1];
+    const int zc = int(std::max<long long>(1, (long long)staging_bytes_ / (s * plane_cells)));
+    for (int i = 0; i < d_.q; ++i) {
+        for (int z0 = 0; z0 < ext[2]; z0 += zc) {
+            const int nzc = int(std::min<long long>(zc, ext[2] - z0));
+            const long long cnt = plane_cells * nzc;
+            const char* h = static_cast<const char*>(f) + (std::size_t(i) * vol + plane_cells * z0) * s;
+            char* o = static_cast<char*>(origin(cur_)) + std::size_t(i) * geo_.dstride * s;
+            cuda_check(cudaMemcpyAsync(staging_, h, cnt * s, cudaMemcpyHostToDevice, stream_), "h2d");
+            const int grid = grid_for(cnt);
+            if (s == 8)
+                k_box_copy<double, double, true><<<grid, 256, 0, stream_>>>((double*)o, (const double*)staging_, geo_, -1, -1, z0 - 1, int(ext[0]), int(ext[1]), nzc);
+            else
+                k_box_copy<float, float, true><<<grid, 256, 0, stream_>>>((float*)o, (const float*)staging_, geo_, -1, -1, z0 - 1, int(ext[0]), int(ext[1]), nzc);
+            cuda_check(cudaGetLastError(), "k_box_copy");
+            cuda_check(cudaStreamSynchronize(stream_), "upload_block");
+        }
+    }
+}
+
+// Interior of buffer `which` (0 = current state) back into an envelope-
+// inclusive host block; the host envelope is left untouched.
+void Lattice::download_block_interior(void* f, const int64_t ext[3], int which) {
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    const int s = d_.precision_bits / 8;
+    const long long vol = ext[0] * ext[1] * ext[2];
+    const long long plane_cells = ext[0] * ext[1];
+    const int buf = which == 0 ? cur_ : 1 - cur_;
+    const int zc = int(std::max<long long>(1, (long long)staging_bytes_ / (s * plane_cells)));
+    for (int i = 0; i < d_.q; ++i) {
+        for (int z0 = 1; z0 < ext[2] - 1; z0 += zc) {
+            const int nzc = int(std::min<long long>(zc, ext[2] - 1 - z0));
+            const long long cnt = plane_cells * nzc;
+            const char* o = static_cast<const char*>(origin(buf)) + std::size_t(i) * geo_.dstride * s;
+            const int grid = grid_for(cnt);
+            // gather full rows (envelope columns included) of planes z0..z0+nzc-1
+            if (s == 8)
+                k_box_copy<double, double, false><<<grid, 256, 0, stream_>>>((double*)staging_, (const double*)o, geo_, -1, -1, z0 - 1, int(ext[0]), int(ext[1]), nzc);
+            else
+                k_box_copy<float, float, false><<<grid, 256, 0, stream_>>>((float*)staging_, (const float*)o, geo_, -1, -1, z0 - 1, int(ext[0]), int(ext[1]), nzc);
+            cuda_check(cudaGetLastError(), "k_box_copy");
+            // copy back the interior of those planes (the caller's envelope is kept)
+            cudaMemcpy3DParms p{};
+            p.srcPtr = make_cudaPitchedPtr(staging_, ext[0] * s, ext[0], ext[1]);
+            p.srcPos = make_cudaPos(s, 1, 0);
+            p.dstPtr = make_cudaPitchedPtr(f, ext[0] * s, ext[0], ext[1]);
+            p.dstPos = make_cudaPos(s, 1, z0);
+            p.extent = make_cudaExtent((ext[0] - 2) * s, ext[1] - 2, nzc);
+            p.kind = cudaMemcpyDeviceToHost;
+            cuda_check(cudaMemcpy3DAsync(&p, stream_), "d2h");
+            cuda_check(cudaStreamSynchronize(stream_), "download_block");
+        }
+    }
+}
+
+template <typename T>
+void Lattice::launch_step(int parity) {
+    StepArgs<T> a{};
+    a.fin = static_cast<const T*>(origin(parity));
+    a.fout = static_cast<T*>(origin(1 - parity));
+    a.slot = d_slot_;
+    a.uniform_slot = uniform_slot_;
+    a.g = geo_;
+    for (std::size_t s = 0; s < chains_.size(); ++s) a.rec[s] = compile_recipe<T>(chains_[s]);
+
+    const int bx = geo_.nx >= 128 ? 128 : (geo_.nx > 32 ? 64 : 32);
+    const int by = 256 / bx;
+    const dim3 block(bx, by, 1);
+    const unsigned gx = unsigned((geo_.nx + bx - 1) / bx);
+    const unsigned gy = unsigned((geo_.ny + by - 1) / by);
+    const void* fn = kernel_->fn;
+
+    const bool linked = lower_.linked || upper_.linked;
+    if (!linked) {
+        a.z_begin = 0;
+        a.z_step = 1;
+        void* args[] = {&a};
+        cuda_check(cudaLaunchKernel(fn, dim3(gx, gy, geo_.nz), block, args, 0, stream_), "launch");
+        return;
+    }
+    // 1. wait until both neighbours completed the boundary planes of the previous step
+    k_halo_wait<<<1, 1, 0, stream_>>>(d_flags_, lower_.linked, upper_.linked,
+                                      20ull * 1000 * 1000 * 1000);
+    cuda_check(cudaGetLastError(), "k_halo_wait");
+    // 2. boundary planes with the fused halo push + completion signal
+    StepArgs<T> b = a;
+    b.z_begin = 0;
+    b.z_step = geo_.nz > 1 ? geo_.nz - 1 : 1;
+    if (upper_.linked) {
+        b.push_up = static_cast<T*>(upper_.buf[1 - parity]);
+        b.up_dstride = upper_.dstride;
+        b.sig_up = upper_.flag;
+    }
+    if (lower_.linked) {
+        b.push_down = static_cast<T*>(lower_.buf[1 - parity]);
+        b.down_dstride = lower_.dstride;
+        b.down_ghost_z = lower_.nz;
+        b.sig_down = lower_.flag;
+    }
+    b.counter = d_counter_;
+    b.my_step = d_flags_ + 2;
+    {
+        void* args[] = {&b};
+        cuda_check(cudaLaunchKernel(fn, dim3(gx, gy, geo_.nz > 1 ? 2 : 1), block, args, 0, stream_),
+                   "launch boundary");
+    }
+    // 3. interior planes (independent of the ghost planes)
+    if (geo_.nz > 2) {
+        a.z_begin = 1;
+        a.z_step = 1;
+        void* args[] = {&a};
+        cuda_check(cudaLaunchKernel(fn, dim3(gx, gy, geo_.nz - 2), block, args, 0, stream_),
+                   "launch interior");
+    }
+}
+
+void Lattice::enqueue_step() {
+    if (d_.precision_bits == 64) launch_step<double>(cur_);
+    else launch_step<float>(cur_);
+    cur_ = 1 - cur_;
+    ++steps_;
+}
+
+void Lattice::step(int64_t nsteps) {
+    if (nsteps <= 0) return;
+    check_dispatch();
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    for (int64_t k = 0; k < nsteps; ++k) enqueue_step();
+}
+
+void Lattice::check_error_flag() {
+    if (!(lower_.linked || upper_.linked)) return;
+    unsigned long long err = 0;
+    cuda_check(cudaMemcpy(&err, d_flags_ + 3, sizeof(err), cudaMemcpyDeviceToHost), "read flags");
+    if (err)
+        throw ExchangeError("halo exchange timed out waiting for a neighbour at step " +
+                            std::to_string(err));
+}
+
+void Lattice::synchronize() {
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    cuda_check(cudaStreamSynchronize(stream_), "step");
+    check_error_flag();
+}
+
+double Lattice::time_steps(int64_t nsteps) {
+    check_dispatch();
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    cuda_check(cudaEventRecord(ev0_, stream_), "event");
+    for (int64_t k = 0; k < nsteps; ++k) enqueue_step();
+    cuda_check(cudaEventRecord(ev1_, stream_), "event");
+    cuda_check(cudaEventSynchronize(ev1_), "event sync");
+    float ms = 0.f;
+    cuda_check(cudaEventElapsedTime(&ms, ev0_, ev1_), "elapsed");
+    check_error_flag();
+    return double(ms);
+}
+
+void Lattice::link_lower(Lattice& lower) {
+    // `lower` sits directly below this slab: lower's top plane feeds our ghost
+    // z = -1, our bottom plane feeds lower's ghost z = lower.nz.
+    if (lower.geo_.nx != geo_.nx || lower.geo_.ny != geo_.ny || lower.d_.q != d_.q ||
+        lower.d_.precision_bits != d_.precision_bits)
+        throw std::invalid_argument("linked slabs must share nx, ny, q and precision");
+    if (lower.device_ != device_) {
+        int ok = 0;
+        cuda_check(cudaDeviceCanAccessPeer(&ok, device_, lower.device_), "peer query");
+        if (!ok) throw ExchangeError("devices have no peer access");
+        cudaSetDevice(device_);
+        cudaDeviceEnablePeerAccess(lower.device_, 0);
+        cudaSetDevice(lower.device_);
+        cudaDeviceEnablePeerAccess(device_, 0);
+        cudaGetLastError();
+    }
+    lower_.linked = true;
+    lower_.buf[0] = lower.origin(0);
+    lower_.buf[1] = lower.origin(1);
+    lower_.dstride = lower.geo_.dstride;
+    lower_.nz = lower.geo_.nz;
+    lower_.flag = lower.d_flags_ + 1;  // we are lower's upper neighbour
+    lower.upper_.linked = true;
+    lower.upper_.buf[0] = origin(0);
+    lower.upper_.buf[1] = origin(1);
+    lower.upper_.dstride = geo_.dstride;
+    lower.upper_.nz = geo_.nz;
+    lower.upper_.flag = d_flags_ + 0;  // lower is our lower neighbour
+}
+
+namespace {
+struct IpcBlob {
+    uint32_t magic;
+    int32_t q, bits, nx, ny, nz;
+    long long dstride, base_off_bytes;
+    cudaIpcMemHandle_t buf[2];
+    cudaIpcMemHandle_t flags;
+};
+constexpr uint32_t kIpcMagic = 0x444c4231;  // "DLB1"
+}  // namespace
+
+std::vector<uint8_t> Lattice::export_ipc() const {
+    IpcBlob b{};
+    b.magic = kIpcMagic;
+    b.q = d_.q;
+    b.bits = d_.precision_bits;
+    b.nx = geo_.nx;
+    b.ny = geo_.ny;
+    b.nz = geo_.nz;
+    b.dstride = geo_.dstride;
+    b.base_off_bytes = base_off_ * (d_.precision_bits / 8);
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    for (int k = 0; k < 2; ++k) cuda_check(cudaIpcGetMemHandle(&b.buf[k], buf_[k]), "ipc handle");
+    cuda_check(cudaIpcGetMemHandle(&b.flags, d_flags_), "ipc handle");
+    std::vector<uint8_t> out(sizeof(b));
+    std::memcpy(out.data(), &b, sizeof(b));
+    return out;
+}
+
+void Lattice::link_ipc(int side, const void* blob, std::size_t len) {
+    if (len != sizeof(IpcBlob)) throw std::invalid_argument("bad IPC blob size");
+    IpcBlob b;
+    std::memcpy(&b, blob, sizeof(b));
+    if (b.magic != kIpcMagic) throw std::invalid_argument("bad IPC blob");
+    if (b.nx != geo_.nx || b.ny != geo_.ny || b.q != d_.q || b.bits != d_.precision_bits)
+        throw std::invalid_argument("linked slabs must share nx, ny, q and precision");
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    Peer& p = side == 0 ? lower_ : upper_;
+    void* bases[3];
+    for (int k = 0; k < 2; ++k)
+        cuda_check(cudaIpcOpenMemHandle(&bases[k], b.buf[k], cudaIpcMemLazyEnablePeerAccess), "ipc open");
+    cuda_check(cudaIpcOpenMemHandle(&bases[2], b.flags, cudaIpcMemLazyEnablePeerAccess), "ipc open");
+    p.ipc_opened = {bases[0], bases[1], bases[2]};
+    p.linked = true;
+    p.buf[0] = static_cast<char*>(bases[0]) + b.base_off_bytes;
+    p.buf[1] = static_cast<char*>(bases[1]) + b.base_off_bytes;
+    p.dstride = b.dstride;
+    p.nz = b.nz;
+    // we are the peer's upper neighbour if it is our lower one, and vice versa
+    p.flag = static_cast<unsigned long long*>(bases[2]) + (side == 0 ? 1 : 0);
+}
+
+// ---------------------------------------------------------------------------
+// Random Boolean sphere pack: spheres of radius r with
+// uniform centres (mt19937_64, periodic placement) are added until the pore
+// fraction drops to target or below; written as raw u8, 255 = solid, x fastest.
+double sphere_pack(int64_t nx, int64_t ny, int64_t nz, double radius, double target_porosity,
+                   uint64_t seed, uint8_t* out) {
+    if (nx < 1 || ny < 1 || nz < 1 || radius <= 0 || target_porosity <= 0 || target_porosity >= 1)
+        throw std::invalid_argument("invalid sphere-pack parameters");
+    const int64_t n = nx * ny * nz;
+    std::memset(out, 0, std::size_t(n));
+    std::mt19937_64 rng(seed);
+    std::uniform_real_distribution<double> ux(0.0, double(nx)), uy(0.0, double(ny)), uz(0.0, double(nz));
+    int64_t solid = 0;
+    const int r = int(std::ceil(radius));
+    const double r2 = radius * radius;
+    while (double(n - solid) / double(n) > target_porosity) {
+        const double cx = ux(rng), cy = uy(rng), cz = uz(rng);
+        for (int dz = -r - 1; dz <= r + 1; ++dz) {
+            const int64_t z = int64_t(std::floor(cz)) + dz;
+            const double ddz = (double(z) + 0.5) - cz;
+            if (ddz * ddz > r2) continue;
+            const int64_t zz = ((z % nz) + nz) % nz;
+            for (int dy = -r - 1; dy <= r + 1; ++dy) {
+                const int64_t y = int64_t(std::floor(cy)) + dy;
+                const double ddy = (double(y) + 0.5) - cy;
+                if (ddz * ddz + ddy * ddy > r2) continue;
+                const int64_t yy = ((y % ny) + ny) % ny;
+                for (int dx = -r - 1; dx <= r + 1; ++dx) {
+                    const int64_t x = int64_t(std::floor(cx)) + dx;
+                    const double ddx = (double(x) + 0.5) - cx;
+                    if (ddz * ddz + ddy * ddy + ddx * ddx > r2) continue;
+                    const int64_t xx = ((x % nx) + nx) % nx;
+                    uint8_t& v = out[std::size_t((zz * ny + yy) * nx + xx)];
+                    if (!v) {
+                        v = 255;
+                        ++solid;
+                    }
+                }
+            }
+        }
+    }
+    return double(n - solid) / double(n);
+}
+
+}  // namespace dlb

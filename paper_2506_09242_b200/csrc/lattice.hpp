@@ -1,0 +1,123 @@
+// Device lattice runtime: one z-slab of the domain resident in HBM.
+//
+// Mirrors the reference's AcceleratedBlock<T> + collide_and_stream<T> +
+// MultiBlockRun<T> (proj/include/dolb/accelerated_lattice.hpp:86-127,
+// proj/include/dolb/multiblock.hpp:119-176) with B200-native storage: padded
+// SoA direction arrays with a one-cell envelope, u8 slot array, recipes in
+// kernel parameter space, and a z-slab halo pushed over peer memory.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <array>
+#include <cstdint>
+#include <memory>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "../../include/dlb.h"
+#include "chain.hpp"
+#include "kernels.cuh"
+
+namespace dlb {
+
+void cuda_check(cudaError_t e, const char* what);
+
+// Halo neighbour of a slab (the lower one at z = -1, the upper at z = nz).
+struct Peer {
+    bool linked = false;
+    void* buf[2] = {nullptr, nullptr};   // peer populations, interior origin of direction 0
+    long long dstride = 0;
+    int nz = 0;
+    unsigned long long* flag = nullptr;  // where to signal our progress in the peer's memory
+    std::vector<void*> ipc_opened;       // bases opened through CUDA IPC (closed on free)
+};
+
+class Lattice {
+  public:
+    Lattice(const dlb_lattice_desc& desc, const DynamicsRegistry& reg);
+    ~Lattice();
+    Lattice(const Lattice&) = delete;
+    Lattice& operator=(const Lattice&) = delete;
+
+    void set_slots(const int32_t* slots);
+    void set_uniform_slot(int32_t slot);
+    void set_dispatch(const int32_t* tags, std::size_t n);
+    void fill_equilibrium(const double* rho, const double* ux, const double* uy, const double* uz);
+    void fill_tgv(int64_t L, double u_inf);
+    void upload(const double* canon);
+    void download(double* canon);
+    void download_raw(void* canon);
+    // Envelope-inclusive host block (AcceleratedBlock layout) in the storage type.
+    void upload_block(const void* f, const int64_t ext[3]);
+    void download_block_interior(void* f, const int64_t ext[3], int which);
+    void step(int64_t nsteps);
+    void enqueue_step();  // one step, no dispatch check (group stepping)
+    void check_dispatch() const;
+    void synchronize();
+    double time_steps(int64_t nsteps);
+
+    void link_lower(Lattice& lower);  // same process
+    std::vector<uint8_t> export_ipc() const;
+    void link_ipc(int side, const void* blob, std::size_t len);
+
+    cudaStream_t stream() const { return stream_; }
+    int64_t steps_done() const { return steps_; }
+    int64_t bytes_per_cell() const;
+    int64_t device_bytes() const { return device_bytes_; }
+    int launches_per_step() const;
+    const char* kernel_name() const { return kernel_ ? kernel_->name : "<none>"; }
+    int64_t cells() const { return int64_t(d_.dims[0]) * d_.dims[1] * d_.dims[2]; }
+    int bits() const { return d_.precision_bits; }
+    int q() const { return d_.q; }
+    void set_periodic_override(bool x, bool y, bool z);
+
+  private:
+    friend struct LatticeAccess;
+    void select_kernel();
+    template <typename T>
+    void launch_step(int parity);
+    void copy_canonical(void* host, bool to_device, bool as_double, int elem_bytes);
+    void* origin(int which) const;  // interior origin of direction 0 of buffer `which`
+    bool split() const { return d_.global_nz != d_.dims[2]; }
+    void check_error_flag();
+
+    dlb_lattice_desc d_;
+    int device_ = 0;
+    cudaStream_t stream_ = nullptr;
+    cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+    Geo geo_{};
+    int align_ = 32;            // elements per 128 B
+    long long base_off_ = 0;    // elements from array start to the interior origin
+    void* buf_[2] = {nullptr, nullptr};
+    int cur_ = 0;               // buffer holding the current state (f_in)
+    uint8_t* d_slot_ = nullptr;
+    int uniform_slot_ = -1;
+    bool slots_set_ = false;
+    std::vector<int32_t> present_slots_;
+    bool untagged_ = false;
+    std::set<int> dispatch_;
+    bool dispatch_set_ = false;
+    // snapshot of the registry (MultiBlockRun compiles recipes at construction,
+    // multiblock.cpp:419)
+    std::vector<DynamicsChain> chains_;
+    std::vector<int> tag_of_slot_;
+    std::vector<std::string> tag_names_;
+    unsigned km_needed_ = 0;
+    const KernelEntry* kernel_ = nullptr;
+    // halo
+    Peer lower_, upper_;
+    unsigned long long* d_flags_ = nullptr;  // [0] from lower, [1] from upper, [2] my step, [3] error
+    unsigned int* d_counter_ = nullptr;      // last-block ticket of the boundary launch
+    int64_t steps_ = 0;
+    int64_t device_bytes_ = 0;
+    void* staging_ = nullptr;
+    std::size_t staging_bytes_ = 0;
+};
+
+// Sphere-pack porous medium generator (cases.cpp raw voxel format).
+double sphere_pack(int64_t nx, int64_t ny, int64_t nz, double radius, double target_porosity,
+                   uint64_t seed, uint8_t* out);
+
+}  // namespace dlb

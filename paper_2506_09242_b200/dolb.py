@@ -1,0 +1,518 @@
+"""Reference-facing interface of the B200 collide-and-stream path.
+
+Mirrors the names, argument meaning and error behaviour of the reference's
+dynamics / data-processor API so that code written against it ports directly:
+
+  LinkType, ChainLink, CollisionParams, ChainParams, DynamicsChain
+        proj/include/dolb/chain.hpp:14-53, collision.hpp:12-31
+  make_collision_chain / make_bounce_back / make_no_dynamics /
+  make_moving_bounce_back / make_regularized_velocity / make_regularized_pressure
+        proj/src/chain.cpp:249-297
+  chain_string / parse_chain_string / serialize_params
+        proj/src/chain.cpp:87-186
+  DynamicsRegistry, DispatchSet, DispatchError
+        proj/include/dolb/accelerated_lattice.hpp:16-79
+  DeviceRun (the device twin of MultiBlockRun<T>: fill, advance,
+  gather_populations, gather_macroscopic)   proj/include/dolb/multiblock.hpp:119-176
+  partition (balanced split)                proj/src/multiblock.cpp:10-49
+  collide_and_stream on a host block        proj/include/dolb/accelerated_lattice.hpp:124-127
+
+Everything below the Python surface runs in libdlb_b200.so (C++ host runtime +
+sm_100a kernels); this module only marshals arguments.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+from . import _capi
+from ._capi import (ARITH_EXACT, ARITH_FAST, LAYOUT_TWO_POP, ConfigError, DispatchError, DlbError,
+                    ExchangeError, check)
+
+__all__ = [
+    "LinkType", "ChainLink", "CollisionParams", "ChainParams", "DynamicsChain",
+    "make_collision_chain", "make_bounce_back", "make_no_dynamics", "make_moving_bounce_back",
+    "make_regularized_velocity", "make_regularized_pressure", "chain_string", "serialize_params",
+    "DynamicsRegistry", "DispatchSet", "DispatchError", "ExchangeError", "ConfigError", "DlbError",
+    "DeviceRun", "partition", "collide_and_stream", "D3Q19", "D3Q27",
+]
+
+
+class LinkType(enum.Enum):
+    NoDynamics = "NoDynamics"
+    BounceBack = "BounceBack"
+    MovingBounceBack = "MovingBounceBack"
+    BGK = "COLL_BGK"
+    TRT = "COLL_TRT"
+    RR = "COLL_RR"
+    Smagorinsky = "LES_Smagorinsky"
+    RegularizedVelocity = "Boundary_RegularizedVelocity"
+    RegularizedPressure = "Boundary_RegularizedPressure"
+
+
+BASES = (LinkType.BGK, LinkType.TRT, LinkType.RR)
+
+
+@dataclass(frozen=True)
+class ChainLink:
+    type: LinkType
+    axis: int = 0
+    orient: int = 1
+
+    def link_id(self) -> str:
+        if self.type in (LinkType.RegularizedVelocity, LinkType.RegularizedPressure):
+            return f"{self.type.value}_{self.axis}_{'1' if self.orient > 0 else 'M1'}"
+        return self.type.value
+
+
+def derive_omega_minus(omega: float, lam: float) -> float:
+    """collision.hpp:19-22"""
+    half_minus = lam / (1.0 / omega - 0.5)
+    return 1.0 / (half_minus + 0.5)
+
+
+@dataclass
+class CollisionParams:
+    omega: float = 1.0
+    omega_minus: float = 1.0
+    lambda_: float = 3.0 / 16.0
+    smagorinsky_c: float = 0.0
+    omega_bulk_ho: float = 1.0
+
+    def set_trt(self, omega: float, lam: float):
+        self.omega, self.lambda_ = omega, lam
+        self.omega_minus = derive_omega_minus(omega, lam)
+        return self
+
+
+@dataclass
+class ChainParams:
+    collision: CollisionParams = field(default_factory=CollisionParams)
+    wall_velocity: tuple = (0.0, 0.0, 0.0)
+    target_rho: float = 1.0
+
+
+@dataclass
+class DynamicsChain:
+    links: list
+    params: ChainParams = field(default_factory=ChainParams)
+
+    def chain_string(self) -> str:
+        return chain_string(self)
+
+
+def chain_string(chain: DynamicsChain) -> str:
+    """Canonical chain string (chain.cpp:87-98), rendered by the C++ runtime."""
+    raw = "|".join(l.link_id() for l in chain.links)
+    return _capi.get_string(_capi.lib().dlb_chain_canonical, raw.encode())
+
+
+def serialize_params(chain: DynamicsChain) -> list:
+    """Parameter record, each link appending the values it consumes (chain.cpp:153-186)."""
+    p = chain.params
+    out = []
+    for l in chain.links:
+        t = l.type
+        if t == LinkType.BGK:
+            out.append(p.collision.omega)
+        elif t == LinkType.TRT:
+            out += [p.collision.omega, p.collision.lambda_]
+        elif t == LinkType.RR:
+            out += [p.collision.omega, p.collision.omega_bulk_ho]
+        elif t == LinkType.Smagorinsky:
+            out.append(p.collision.smagorinsky_c)
+        elif t in (LinkType.MovingBounceBack, LinkType.RegularizedVelocity):
+            out += [float(v) for v in p.wall_velocity]
+        elif t == LinkType.RegularizedPressure:
+            out.append(p.target_rho)
+    return out
+
+
+def _canonical_collision(base: LinkType, params: CollisionParams) -> CollisionParams:
+    """chain.cpp:236-245: keep only what the base consumes."""
+    c = CollisionParams(omega=params.omega)
+    if base == LinkType.TRT:
+        c.set_trt(params.omega, params.lambda_)
+    elif base == LinkType.RR:
+        c.omega_bulk_ho = params.omega_bulk_ho
+    return c
+
+
+def make_collision_chain(base: LinkType, params: CollisionParams, smagorinsky_c=None) -> DynamicsChain:
+    coll = _canonical_collision(base, params)
+    links = []
+    if smagorinsky_c is not None:
+        coll.smagorinsky_c = smagorinsky_c
+        links.append(ChainLink(LinkType.Smagorinsky))
+    links.append(ChainLink(base))
+    return DynamicsChain(links, ChainParams(collision=coll))
+
+
+def make_bounce_back() -> DynamicsChain:
+    return DynamicsChain([ChainLink(LinkType.BounceBack)])
+
+
+def make_no_dynamics() -> DynamicsChain:
+    return DynamicsChain([ChainLink(LinkType.NoDynamics)])
+
+
+def make_moving_bounce_back(u_wall) -> DynamicsChain:
+    return DynamicsChain([ChainLink(LinkType.MovingBounceBack)],
+                         ChainParams(wall_velocity=tuple(float(v) for v in u_wall)))
+
+
+def make_regularized_velocity(axis, orient, u, base, params) -> DynamicsChain:
+    return DynamicsChain([ChainLink(LinkType.RegularizedVelocity, axis, orient), ChainLink(base)],
+                         ChainParams(collision=_canonical_collision(base, params),
+                                     wall_velocity=tuple(float(v) for v in u)))
+
+
+def make_regularized_pressure(axis, orient, rho, base, params) -> DynamicsChain:
+    return DynamicsChain([ChainLink(LinkType.RegularizedPressure, axis, orient), ChainLink(base)],
+                         ChainParams(collision=_canonical_collision(base, params), target_rho=rho))
+
+
+class DynamicsRegistry:
+    """Chain strings <-> tags plus the parameter table (accelerated_lattice.hpp:32-60).
+    Tags are indices into the sorted chain-string set; slots are (chain, params) instances."""
+
+    def __init__(self):
+        h = C.c_void_p()
+        check(_capi.lib().dlb_registry_new(C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _capi._lib is not None:
+            _capi._lib.dlb_registry_free(self._h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def register_chain(self, chain: DynamicsChain) -> int:
+        raw = "|".join(l.link_id() for l in chain.links)
+        rec = np.asarray(serialize_params(chain), np.float64)
+        slot = C.c_int32()
+        check(_capi.lib().dlb_registry_register(self._h, raw.encode(),
+                                                rec.ctypes.data if rec.size else None,
+                                                rec.size, C.byref(slot)))
+        return slot.value
+
+    def tag_for(self, chain_str: str) -> int:
+        t = C.c_int32()
+        check(_capi.lib().dlb_registry_tag_for(self._h, chain_str.encode(), C.byref(t)))
+        return t.value
+
+    def chain_for(self, tag: int) -> str:
+        return _capi.get_string(_capi.lib().dlb_registry_chain_for, self._h, tag)
+
+    def tag_of_slot(self, slot: int) -> int:
+        t = C.c_int32()
+        check(_capi.lib().dlb_registry_tag_of_slot(self._h, slot, C.byref(t)))
+        return t.value
+
+    def _counts(self):
+        a, b = C.c_int32(), C.c_int32()
+        check(_capi.lib().dlb_registry_counts(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def num_tags(self) -> int:
+        return self._counts()[0]
+
+    def num_instances(self) -> int:
+        return self._counts()[1]
+
+    def chain_strings(self) -> list:
+        return [self.chain_for(t) for t in range(self.num_tags())]
+
+    def slot_params(self, slot: int) -> list:
+        n = C.c_size_t()
+        check(_capi.lib().dlb_registry_slot_params(self._h, slot, None, 0, C.byref(n)))
+        buf = np.zeros(max(n.value, 1))
+        check(_capi.lib().dlb_registry_slot_params(self._h, slot, buf.ctypes.data, buf.size, C.byref(n)))
+        return list(buf[:n.value])
+
+
+class DispatchSet:
+    """Explicit subset of registry tags admitted by the step kernel."""
+
+    def __init__(self, tags=()):
+        self.tags = set(int(t) for t in tags)
+
+    @staticmethod
+    def all_of(registry: DynamicsRegistry) -> "DispatchSet":
+        return DispatchSet(range(registry.num_tags()))
+
+    @staticmethod
+    def from_strings(registry: DynamicsRegistry, names) -> "DispatchSet":
+        return DispatchSet(registry.tag_for(n) for n in names)
+
+    def contains(self, tag: int) -> bool:
+        return tag in self.tags
+
+
+def partition(n: int, k: int):
+    """Balanced split: the first n % k parts are one cell longer (multiblock.cpp:24-31).
+    Returns [(origin, extent), ...]."""
+    if k < 1 or k > n:
+        raise ValueError("partition: block grid must be between 1 and the extent")
+    out, at = [], 0
+    for b in range(k):
+        ln = n // k + (1 if b < n % k else 0)
+        out.append((at, ln))
+        at += ln
+    return out
+
+
+class _Lattice:
+    """One z-slab handle."""
+
+    def __init__(self, desc: _capi.LatticeDesc, registry: DynamicsRegistry):
+        h = C.c_void_p()
+        check(_capi.lib().dlb_lattice_create(C.byref(desc), registry.handle, C.byref(h)))
+        self._h = h
+        self.desc = desc
+        self.registry = registry  # keep alive
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _capi._lib is not None:
+            _capi._lib.dlb_lattice_free(self._h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def ncells(self):
+        d = self.desc.dims
+        return int(d[0] * d[1] * d[2])
+
+
+class DeviceRun:
+    """Device twin of MultiBlockRun<T> for a z-slab decomposition.
+
+    ``slabs`` z-slabs are created in this process (on ``devices``, default all
+    on device 0) and linked through peer memory; ``dist=(rank, world)`` instead
+    creates only this rank's slab and links it to its neighbours' slabs in
+    other processes via CUDA IPC handles exchanged over torch.distributed.
+    """
+
+    def __init__(self, dims, periodic, registry: DynamicsRegistry, dispatch: DispatchSet | None = None,
+                 q: int = 19, precision: int = 64, slabs: int = 1, devices=None, arith: str = "exact",
+                 dist=None):
+        self.dims = tuple(int(v) for v in dims)
+        self.periodic = tuple(int(bool(p)) for p in periodic)
+        self.registry = registry
+        self.q, self.precision = q, precision
+        self.dist = dist
+        world = dist[1] if dist else slabs
+        parts = partition(self.dims[2], world)
+        self.parts = parts
+        mine = [dist[0]] if dist else list(range(world))
+        if devices is None:
+            devices = [0] * len(mine)
+        self.slabs = []
+        for k, r in enumerate(mine):
+            d = _capi.LatticeDesc()
+            d.dims[0], d.dims[1], d.dims[2] = self.dims[0], self.dims[1], parts[r][1]
+            for a in range(3):
+                d.periodic[a] = self.periodic[a]
+            d.q, d.precision_bits = q, precision
+            d.layout = LAYOUT_TWO_POP
+            d.arith = ARITH_FAST if arith == "fast" else ARITH_EXACT
+            d.device = devices[k]
+            d.z_origin, d.global_nz = parts[r][0], self.dims[2]
+            self.slabs.append(_Lattice(d, registry))
+        self.ranks = mine
+        if dist is None and world > 1:
+            for r in range(world - 1):
+                check(_capi.lib().dlb_lattice_link_local(self.slabs[r].handle, self.slabs[r + 1].handle))
+            if self.periodic[2]:
+                check(_capi.lib().dlb_lattice_link_local(self.slabs[world - 1].handle, self.slabs[0].handle))
+        elif dist is not None and world > 1:
+            self._link_distributed()
+        self.set_dispatch(dispatch if dispatch is not None else DispatchSet.all_of(registry))
+
+    # -- distributed linking over torch.distributed (plumbing only) --------------
+    def _link_distributed(self):
+        import torch.distributed as dist
+        rank, world = self.dist
+        lat = self.slabs[0]
+        n = C.c_size_t()
+        check(_capi.lib().dlb_lattice_export_ipc(lat.handle, None, 0, C.byref(n)))
+        buf = (C.c_uint8 * n.value)()
+        check(_capi.lib().dlb_lattice_export_ipc(lat.handle, buf, n.value, C.byref(n)))
+        blobs = [None] * world
+        dist.all_gather_object(blobs, bytes(buf))
+        lower = rank - 1 if rank > 0 else (world - 1 if self.periodic[2] else None)
+        upper = rank + 1 if rank < world - 1 else (0 if self.periodic[2] else None)
+        for side, nb in ((0, lower), (1, upper)):
+            if nb is None:
+                continue
+            b = blobs[nb]
+            cb = (C.c_uint8 * len(b)).from_buffer_copy(b)
+            check(_capi.lib().dlb_lattice_link_ipc(lat.handle, side, cb, len(b)))
+        dist.barrier()
+
+    # -- setup ------------------------------------------------------------------
+    def set_dispatch(self, dispatch: DispatchSet):
+        self.dispatch = dispatch
+        tags = np.asarray(sorted(dispatch.tags), np.int32)
+        for s in self.slabs:
+            check(_capi.lib().dlb_lattice_set_dispatch(s.handle, tags.ctypes.data if tags.size else None, tags.size))
+
+    def _slab_range(self, k):
+        r = self.ranks[k]
+        return self.parts[r]
+
+    def fill_slots(self, slots: np.ndarray | int):
+        """slots: (nz, ny, nx) registry slots over the GLOBAL domain, or one slot for all."""
+        for k, s in enumerate(self.slabs):
+            if np.isscalar(slots):
+                check(_capi.lib().dlb_lattice_set_uniform_slot(s.handle, int(slots)))
+                continue
+            z0, nz = self._slab_range(k)
+            part = np.ascontiguousarray(np.asarray(slots, np.int32)[z0:z0 + nz])
+            check(_capi.lib().dlb_lattice_set_slots(s.handle, part.ctypes.data))
+
+    def fill_state(self, rho=None, ux=None, uy=None, uz=None):
+        """Equilibrium from per-cell (rho, u) over the global domain; default rest."""
+        for k, s in enumerate(self.slabs):
+            z0, nz = self._slab_range(k)
+            n = self.dims[0] * self.dims[1] * nz
+            sl = slice(z0 * self.dims[0] * self.dims[1], (z0 + nz) * self.dims[0] * self.dims[1])
+
+            def part(a, default):
+                if a is None:
+                    return np.full(n, default, np.float64)
+                return np.ascontiguousarray(np.asarray(a, np.float64).reshape(-1)[sl])
+            arrs = [part(rho, 1.0), part(ux, 0.0), part(uy, 0.0), part(uz, 0.0)]
+            check(_capi.lib().dlb_lattice_fill_equilibrium(s.handle, *[a.ctypes.data for a in arrs]))
+
+    def fill_tgv(self, L: int, u_inf: float):
+        for s in self.slabs:
+            check(_capi.lib().dlb_lattice_fill_tgv(s.handle, L, u_inf))
+
+    def fill(self, slot_of, state):
+        """MultiBlockRun::fill analogue: slot_of array/scalar, state = ('tgv', L, u) | ('rest',) |
+        (rho, ux, uy, uz) arrays."""
+        self.fill_slots(slot_of)
+        if isinstance(state, tuple) and state and state[0] == "tgv":
+            self.fill_tgv(state[1], state[2])
+        elif isinstance(state, tuple) and state and state[0] == "rest":
+            self.fill_state()
+        else:
+            self.fill_state(*state)
+
+    def upload_populations(self, canon: np.ndarray):
+        canon = np.asarray(canon, np.float64).reshape(self.q, -1)
+        nxy = self.dims[0] * self.dims[1]
+        for k, s in enumerate(self.slabs):
+            z0, nz = self._slab_range(k)
+            part = np.ascontiguousarray(canon[:, z0 * nxy:(z0 + nz) * nxy])
+            check(_capi.lib().dlb_lattice_upload_populations(s.handle, part.ctypes.data))
+
+    # -- stepping ---------------------------------------------------------------
+    def advance(self, nsteps: int):
+        if len(self.slabs) == 1:
+            check(_capi.lib().dlb_lattice_step(self.slabs[0].handle, nsteps))
+        else:
+            arr = (C.c_void_p * len(self.slabs))(*[s.handle.value for s in self.slabs])
+            check(_capi.lib().dlb_lattices_step(arr, len(self.slabs), nsteps))
+
+    def synchronize(self):
+        for s in self.slabs:
+            check(_capi.lib().dlb_lattice_synchronize(s.handle))
+
+    def time_steps(self, nsteps: int) -> float:
+        """CUDA-event milliseconds for nsteps on the (single) slab's stream."""
+        ms = C.c_double()
+        check(_capi.lib().dlb_lattice_time_steps(self.slabs[0].handle, nsteps, C.byref(ms)))
+        return ms.value
+
+    def stream_handle(self, k: int = 0) -> int:
+        p = C.c_void_p()
+        check(_capi.lib().dlb_lattice_stream(self.slabs[k].handle, C.byref(p)))
+        return p.value or 0
+
+    def kernel_name(self, k: int = 0) -> str:
+        return _capi.get_string(_capi.lib().dlb_lattice_kernel_name, self.slabs[k].handle)
+
+    def traffic(self, k: int = 0):
+        b, d, l = C.c_int64(), C.c_int64(), C.c_int32()
+        check(_capi.lib().dlb_lattice_traffic(self.slabs[k].handle, C.byref(b), C.byref(d), C.byref(l)))
+        return b.value, d.value, l.value
+
+    def num_cells(self) -> int:
+        return self.dims[0] * self.dims[1] * self.dims[2]
+
+    # -- gathers ----------------------------------------------------------------
+    def gather_populations(self) -> np.ndarray:
+        """Canonical order (direction-major, x fastest) over the cells this process owns."""
+        nxy = self.dims[0] * self.dims[1]
+        z_lo = self._slab_range(0)[0]
+        z_hi = sum(self._slab_range(len(self.slabs) - 1))
+        out = np.zeros((self.q, (z_hi - z_lo) * nxy), np.float64)
+        for k, s in enumerate(self.slabs):
+            z0, nz = self._slab_range(k)
+            buf = np.zeros(self.q * nz * nxy, np.float64)
+            check(_capi.lib().dlb_lattice_download_populations(s.handle, buf.ctypes.data))
+            out[:, (z0 - z_lo) * nxy:(z0 - z_lo + nz) * nxy] = buf.reshape(self.q, -1)
+        return out.reshape(-1)
+
+    def gather_raw(self) -> np.ndarray:
+        """Like gather_populations but in the storage precision."""
+        dt = np.float64 if self.precision == 64 else np.float32
+        nxy = self.dims[0] * self.dims[1]
+        parts = []
+        for k, s in enumerate(self.slabs):
+            _, nz = self._slab_range(k)
+            buf = np.zeros(self.q * nz * nxy, dt)
+            check(_capi.lib().dlb_lattice_download_raw(s.handle, buf.ctypes.data))
+            parts.append(buf.reshape(self.q, -1))
+        return np.concatenate(parts, axis=1).reshape(-1)
+
+
+def collide_and_stream(registry: DynamicsRegistry, f_in: np.ndarray, tag: np.ndarray,
+                       param_index: np.ndarray, dispatch: DispatchSet, f_out: np.ndarray | None = None,
+                       q: int = 19):
+    """Drop-in for collide_and_stream<T>(AcceleratedBlock<T>&, ...) on host arrays
+    (accelerated_lattice.hpp:124-127). f_in: (q, ez, ey, ex) envelope-inclusive,
+    tag / param_index: (ez, ey, ex). On return f_in holds the new state and f_out
+    (if given) the previous one."""
+    assert f_in.flags.c_contiguous and f_in.ndim == 4
+    ez, ey, ex = f_in.shape[1:]
+    v = _capi.BlockView()
+    v.precision_bits = 64 if f_in.dtype == np.float64 else 32
+    v.q = q
+    v.interior[0], v.interior[1], v.interior[2] = ex - 2, ey - 2, ez - 2
+    v.f_in = f_in.ctypes.data
+    v.f_out = f_out.ctypes.data if f_out is not None else None
+    tag = np.ascontiguousarray(tag, np.int32)
+    pidx = np.ascontiguousarray(param_index, np.int32)
+    v.tag, v.param_index = tag.ctypes.data, pidx.ctypes.data
+    tags = np.asarray(sorted(dispatch.tags), np.int32)
+    check(_capi.lib().dlb_collide_and_stream(registry.handle, C.byref(v),
+                                             tags.ctypes.data if tags.size else None, tags.size, 1))
+
+
+def _descriptor(q):
+    if q == 19:
+        c = [(0, 0, 0), (-1, 0, 0), (1, 0, 0), (0, -1, 0), (0, 1, 0), (0, 0, -1), (0, 0, 1),
+             (-1, -1, 0), (1, 1, 0), (-1, 1, 0), (1, -1, 0), (-1, 0, -1), (1, 0, 1), (-1, 0, 1),
+             (1, 0, -1), (0, -1, -1), (0, 1, 1), (0, -1, 1), (0, 1, -1)]
+        w = [1 / 3] + [1 / 18] * 6 + [1 / 36] * 12
+    else:
+        c = _descriptor(19)[0].tolist() + [(-1, -1, -1), (1, 1, 1), (-1, -1, 1), (1, 1, -1),
+                                           (-1, 1, -1), (1, -1, 1), (1, -1, -1), (-1, 1, 1)]
+        w = [8 / 27] + [2 / 27] * 6 + [1 / 54] * 12 + [1 / 216] * 8
+    return np.asarray(c, np.int64), np.asarray(w)
+
+
+D3Q19 = _descriptor(19)
+D3Q27 = _descriptor(27)

@@ -1,0 +1,57 @@
+"""Generate tests/golden/golden.json from the UNMODIFIED reference solver.
+
+Run in the build container (needs oracle/_ref/libdolb_refshim.so, built from
+/root/reference/proj by `make -C oracle ref`):
+
+    python tests/golden/make_golden.py
+
+Each entry records the reference's gather_populations() after `steps` steps
+(MultiBlockRun<T>, 8 workers x z-blocks — decomposition does not change the
+bits, test_multiblock.cpp:234-256) as a sha256 of the float64 values with -0
+folded to +0, plus summary values. Porous entries read sphere48.raw, a mask
+written by the product's seeded sphere-pack generator in the reference's raw
+voxel format (committed next to this file).
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+sys.path.insert(0, HERE)
+from pyoracle import Reference, canonical_hash  # noqa: E402
+from golden_cases import CASES, make_case  # noqa: E402
+
+
+def main():
+    ref = Reference()
+    out = {}
+    for name, spec in CASES.items():
+        case = make_case(spec)
+        t = time.time()
+        pops = ref.run_case(case, spec["bits"], spec["steps"], grid=(1, 1, spec.get("workers", 4)),
+                            workers=spec.get("workers", 4))
+        dt = time.time() - t
+        q = 19
+        n = pops.size // q
+        idx = np.linspace(0, pops.size - 1, 16).astype(np.int64)
+        out[name] = {
+            "spec": spec,
+            "sha256": canonical_hash(pops),
+            "sum": float(pops.sum()),
+            "absmax": float(np.abs(pops).max()),
+            "mass": float(pops.reshape(q, n).sum()),
+            "sample_index": idx.tolist(),
+            "sample": [float(v) for v in pops[idx]],
+        }
+        print(f"{name}: {dt:.1f}s sha={out[name]['sha256'][:16]}", flush=True)
+    with open(os.path.join(HERE, "golden.json"), "w") as f:
+        json.dump(out, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
