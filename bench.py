@@ -210,6 +210,7 @@ def main():
     ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
     ap.add_argument("--L", type=int, default=None, help="override the edge length (profiling only)")
     ap.add_argument("--arith", default="exact", choices=["exact", "fast"])
+    ap.add_argument("--layout", default="twopop", choices=["twopop", "aa"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -237,8 +238,9 @@ def main():
     lt = {"BGK": dlb.LinkType.BGK, "TRT": dlb.LinkType.TRT, "RR": dlb.LinkType.RR}[coll]
     cfg = dlb.CaseConfig(kind=kind, L=L, Re=Re, Ma=Ma, collision=lt, q=q)
     setup = dlb.init_tgv(cfg) if kind == "tgv" else dlb.init_cavity(cfg)
+    layout = args.layout if world == 1 else "twopop"  # AA runs single-slab lattices
     run = dlb.build_run(setup, precision=bits, arith=args.arith,
-                        dist=(rank, world) if world > 1 else None, devices=[local])
+                        dist=(rank, world) if world > 1 else None, devices=[local], layout=layout)
     cells_total = run.num_cells()
     bpc, dev_bytes, launches = run.traffic()
 
@@ -300,7 +302,8 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "f32" if bits == 32 else "f64", "data": "synthetic",
         "config": {"workload": f"{args.config}: {desc}", "L": L, "cells": cells_total,
-                   "parallelism": f"z-slab x{world}", "layout": "two-population SoA",
+                   "parallelism": f"z-slab x{world}",
+                   "layout": "AA in-place SoA" if layout == "aa" else "two-population SoA",
                    "arith": args.arith, "l2": "inputs larger than L2 (state resident in HBM)",
                    "device_bytes_per_gpu": dev_bytes},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -129,6 +129,11 @@ DLB_API dlb_status dlb_lattice_kernel_name(dlb_lattice* lat, char* buf, size_t c
 /* Same process (any devices with peer access, or one device): the top plane of
  * `lower` feeds the bottom ghost plane of `upper` and vice versa. */
 DLB_API dlb_status dlb_lattice_link_local(dlb_lattice* lower, dlb_lattice* upper);
+/* Envelope exchange only (MultiBlockRun::exchange, multiblock.hpp:142-143):
+ * copy this slab's boundary planes into the linked neighbours' ghost planes of
+ * the current state. Call on every slab after filling / uploading the state and
+ * before the first step (steps then push the halo themselves). */
+DLB_API dlb_status dlb_lattice_exchange(dlb_lattice* lat);
 /* Across processes: export an opaque blob (CUDA IPC handles), ship it with any
  * transport (e.g. torch.distributed), link it as the lower (side 0) or upper
  * (side 1) neighbour. */

@@ -272,6 +272,14 @@ DLB_API dlb_status dlb_lattice_link_local(dlb_lattice* lower, dlb_lattice* upper
     return guarded([&] { upper->lat->link_lower(*lower->lat); });
 }
 
+DLB_API dlb_status dlb_lattice_exchange(dlb_lattice* lat) {
+    DLB_REQUIRE(lat);
+    return guarded([&] {
+        lat->lat->synchronize();
+        lat->lat->exchange();
+    });
+}
+
 DLB_API dlb_status dlb_lattice_export_ipc(dlb_lattice* lat, void* blob, size_t cap, size_t* len_out) {
     DLB_REQUIRE(lat);
     return guarded([&] {

@@ -22,7 +22,7 @@ namespace dlb {
 namespace DLB_MODE {
 
 template <typename T, int Q, unsigned KM>
-__global__ void __launch_bounds__(256) k_pull(const __grid_constant__ StepArgs<T> a) {
+__global__ void __launch_bounds__(256, 2) k_pull(const __grid_constant__ StepArgs<T> a) {
     using L = Lat<Q>;
     const Geo& g = a.g;
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(256) k_pull(const __grid_constant__ StepArgs<T
             const int sx = cx > 0 ? xm : (cx < 0 ? xp : x);
             const int sy = cy > 0 ? ym : (cy < 0 ? yp : y);
             const int sz = cz > 0 ? zm : (cz < 0 ? zp : z);
-            f[i] = __ldg(a.fin + i * g.dstride + (sz * g.plane + sy * g.pitch + sx));
+            f[i] = __ldg(a.fin[i] + (sz * g.plane + sy * g.pitch + sx));
         });
 
         int s = a.uniform_slot;
@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(256) k_pull(const __grid_constant__ StepArgs<T
         const int center = z * g.plane + y * g.pitch + x;
         sfor<Q>([&](auto I) {
             constexpr int i = decltype(I)::value;
-            a.fout[i * g.dstride + center] = f[i];
+            a.fout[i][center] = f[i];
         });
 
         if (a.push_up != nullptr && z == g.nz - 1) {
@@ -95,6 +95,87 @@ __global__ void __launch_bounds__(256) k_pull(const __grid_constant__ StepArgs<T
     }
 }
 
+
+// AA-pattern in-place streaming (PAPER.md:104 future work): one
+// population array A, two alternating kernels, every location read and
+// written by the same thread (race-free in place), the same 2*q*sizeof(T)
+// bytes per cell as the two-population scheme with half the memory.
+//   even step: f_i = A[i][x];            collide; A[opp(i)][x]       = f_i
+//   odd  step: f_i = A[opp(i)][x - c_i]; collide; A[i][x + c_i]      = f_i
+// After an even step the canonical state is f_i(x) = A[opp(i)][x], after an
+// odd step (and at upload) f_i(x) = A[i][x + c_i]. Pulls from outside a
+// non-periodic face read 0: the odd step reads nothing there and zeroes
+// A[i][x] (the location the next even step reads for that link); pushes
+// across a non-periodic face land in the envelope, where they stay part of the
+// canonical state but are never read.
+template <typename T, int Q, unsigned KM, bool ODD>
+__global__ void __launch_bounds__(256, 2) k_aa(const __grid_constant__ StepArgs<T> a) {
+    using L = Lat<Q>;
+    const Geo& g = a.g;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    const int z = a.z_begin + int(blockIdx.z) * a.z_step;
+    if (x >= g.nx || y >= g.ny) return;
+    const int center = z * g.plane + y * g.pitch + x;
+    T f[Q];
+    if constexpr (!ODD) {
+        sfor<Q>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            f[i] = a.fin[i][center];
+        });
+    } else {
+        const int xm = (x == 0 && g.per_x) ? g.nx - 1 : x - 1;
+        const int xp = (x == g.nx - 1 && g.per_x) ? 0 : x + 1;
+        const int ym = (y == 0 && g.per_y) ? g.ny - 1 : y - 1;
+        const int yp = (y == g.ny - 1 && g.per_y) ? 0 : y + 1;
+        const int zm = (z == 0 && g.per_z) ? g.nz - 1 : z - 1;
+        const int zp = (z == g.nz - 1 && g.per_z) ? 0 : z + 1;
+        const bool xlo = xm < 0, xhi = xp >= g.nx, ylo = ym < 0, yhi = yp >= g.ny;
+        const bool zlo = zm < 0, zhi = zp >= g.nz;
+        sfor<Q>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            constexpr int cx = L::c[i][0], cy = L::c[i][1], cz = L::c[i][2];
+            const bool out = (cx > 0 && xlo) || (cx < 0 && xhi) || (cy > 0 && ylo) ||
+                             (cy < 0 && yhi) || (cz > 0 && zlo) || (cz < 0 && zhi);
+            const int sx = cx > 0 ? xm : (cx < 0 ? xp : x);
+            const int sy = cy > 0 ? ym : (cy < 0 ? yp : y);
+            const int sz = cz > 0 ? zm : (cz < 0 ? zp : z);
+            f[i] = out ? T(0) : a.fin[opp_of(i)][sz * g.plane + sy * g.pitch + sx];
+        });
+    }
+    int s = a.uniform_slot;
+    if (a.slot != nullptr) s = a.slot[(static_cast<long long>(z) * g.ny + y) * g.nx + x];
+    Cell<T, Q>::template apply<KM>(f, a.rec[s]);
+    if constexpr (!ODD) {
+        sfor<Q>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            a.fout[opp_of(i)][center] = f[i];
+        });
+    } else {
+        const int xm = (x == 0 && g.per_x) ? g.nx - 1 : x - 1;
+        const int xp = (x == g.nx - 1 && g.per_x) ? 0 : x + 1;
+        const int ym = (y == 0 && g.per_y) ? g.ny - 1 : y - 1;
+        const int yp = (y == g.ny - 1 && g.per_y) ? 0 : y + 1;
+        const int zm = (z == 0 && g.per_z) ? g.nz - 1 : z - 1;
+        const int zp = (z == g.nz - 1 && g.per_z) ? 0 : z + 1;
+        const bool xlo = xm < 0, xhi = xp >= g.nx, ylo = ym < 0, yhi = yp >= g.ny;
+        const bool zlo = zm < 0, zhi = zp >= g.nz;
+        sfor<Q>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            constexpr int cx = L::c[i][0], cy = L::c[i][1], cz = L::c[i][2];
+            const int dx = cx > 0 ? xp : (cx < 0 ? xm : x);
+            const int dy = cy > 0 ? yp : (cy < 0 ? ym : y);
+            const int dz = cz > 0 ? zp : (cz < 0 ? zm : z);
+            a.fout[i][dz * g.plane + dy * g.pitch + dx] = f[i];
+            if constexpr (i != 0) {
+                const bool out = (cx > 0 && xlo) || (cx < 0 && xhi) || (cy > 0 && ylo) ||
+                                 (cy < 0 && yhi) || (cz > 0 && zlo) || (cz < 0 && zhi);
+                if (out) a.fout[i][center] = T(0);
+            }
+        });
+    }
+}
+
 #define DLB_STR2(x) #x
 #define DLB_STR(x) DLB_STR2(x)
 #define ENTRY(T, Q, KM)                                                                  \
@@ -103,6 +184,18 @@ __global__ void __launch_bounds__(256) k_pull(const __grid_constant__ StepArgs<T
             reinterpret_cast<const void*>(&k_pull<T, Q, unsigned(KM)>),                   \
             "k_pull<" #T ",D3Q" #Q "," #KM ">[" DLB_STR(DLB_MODE) "]"                      \
     }
+
+#define AA_ENTRY(T, Q, KM, ODD)                                                          \
+    KernelEntry {                                                                        \
+        int(sizeof(T) * 8), Q, unsigned(KM), ODD ? LAYOUT_AA_ODD : LAYOUT_AA,               \
+            reinterpret_cast<const void*>(&k_aa<T, Q, unsigned(KM), ODD>),                \
+            "k_aa_" #ODD "<" #T ",D3Q" #Q "," #KM ">[" DLB_STR(DLB_MODE) "]"                  \
+    }
+#define AA_PAIR(T, Q, KM) AA_ENTRY(T, Q, KM, false), AA_ENTRY(T, Q, KM, true)
+#define AA_SET(T)                                                                         \
+    AA_PAIR(T, 19, KM_BGK), AA_PAIR(T, 19, KM_TRT), AA_PAIR(T, 19, KM_RR),               \
+        AA_PAIR(T, 19, KM_TRT | KM_BB | KM_MBB), AA_PAIR(T, 19, KM_ALL), AA_PAIR(T, 27, KM_RR), \
+        AA_PAIR(T, 27, KM_ALL)
 
 #define Q19_SET(T)                                                                        \
     ENTRY(T, 19, KM_BGK), ENTRY(T, 19, KM_TRT), ENTRY(T, 19, KM_RR),                      \
@@ -115,7 +208,7 @@ __global__ void __launch_bounds__(256) k_pull(const __grid_constant__ StepArgs<T
 #define Q27_SET(T) ENTRY(T, 27, KM_BGK), ENTRY(T, 27, KM_TRT), ENTRY(T, 27, KM_RR), ENTRY(T, 27, KM_ALL)
 
 static const KernelEntry kTable[] = {
-    Q19_SET(float), Q19_SET(double), Q27_SET(float), Q27_SET(double),
+    Q19_SET(float), Q19_SET(double), Q27_SET(float), Q27_SET(double), AA_SET(float), AA_SET(double),
 };
 
 const KernelEntry* kernel_table(int* n) {

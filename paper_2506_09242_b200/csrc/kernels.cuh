@@ -27,10 +27,14 @@ struct Geo {
     long long dstride;        // elements per direction array
 };
 
+constexpr int kMaxQ = 27;
+
 template <typename T>
 struct StepArgs {
-    const T* fin;           // direction 0, interior origin
-    T* fout;
+    // per-direction interior origins (host-computed: keeps the 64-bit
+    // direction offsets out of the per-thread address arithmetic)
+    const T* fin[kMaxQ];
+    T* fout[kMaxQ];
     const uint8_t* slot;    // nx*ny*nz registry slots (x fastest) or nullptr if uniform
     int uniform_slot;
     int z_begin, z_step;    // plane z = z_begin + blockIdx.z * z_step
@@ -53,7 +57,7 @@ struct StepArgs {
     DevRecipe<T> rec[kMaxSlots];
 };
 
-enum Layout : int { LAYOUT_TWO_POP = 0, LAYOUT_AA = 1 };
+enum Layout : int { LAYOUT_TWO_POP = 0, LAYOUT_AA = 1, LAYOUT_AA_ODD = 2 };  // AA: even / odd kernel
 
 using StepKernelF = void (*)(StepArgs<float>);
 using StepKernelD = void (*)(StepArgs<double>);

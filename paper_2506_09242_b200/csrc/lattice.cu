@@ -19,6 +19,15 @@ void cuda_check(cudaError_t e, const char* what) {
 namespace {
 
 constexpr std::size_t kStagingBytes = std::size_t(256) << 20;
+constexpr int kCz19[19] = {0, 0, 0, 0, 0, -1, 1, 0, 0, 0, 0, -1, 1, 1, -1, -1, 1, 1, -1};
+constexpr int kCz27[27] = {0, 0, 0, 0, 0, -1, 1, 0, 0, 0, 0, -1, 1, 1, -1, -1, 1, 1, -1,
+                           -1, 1, 1, -1, -1, 1, -1, 1};
+constexpr int kCx19[19] = {0, -1, 1, 0, 0, 0, 0, -1, 1, -1, 1, -1, 1, -1, 1, 0, 0, 0, 0};
+constexpr int kCy19[19] = {0, 0, 0, -1, 1, 0, 0, -1, 1, 1, -1, 0, 0, 0, 0, -1, 1, -1, 1};
+constexpr int kCx27[27] = {0, -1, 1, 0, 0, 0, 0, -1, 1, -1, 1, -1, 1, -1, 1, 0, 0, 0, 0,
+                           -1, 1, -1, 1, -1, 1, 1, -1};
+constexpr int kCy27[27] = {0, 0, 0, -1, 1, 0, 0, -1, 1, 1, -1, 0, 0, 0, 0, -1, 1, -1, 1,
+                           -1, 1, -1, 1, 1, -1, -1, 1};
 
 // ---------------------------------------------------------------------------
 // auxiliary kernels
@@ -28,10 +37,29 @@ __device__ __forceinline__ long long lin(const Geo& g, int x, int y, int z) {
     return static_cast<long long>(z) * g.plane + static_cast<long long>(y) * g.pitch + x;
 }
 
+// Position of canonical f_i(x, y, z) in the AA array after an odd step /
+// at upload: A[i][x + c_i] (wrapped on periodic axes, envelope otherwise).
+__device__ __forceinline__ long long shifted(const Geo& g, int x, int y, int z, int cx, int cy,
+                                             int cz) {
+    int X = x + cx, Y = y + cy, Z = z + cz;
+    if (g.per_x) X = X < 0 ? X + g.nx : (X >= g.nx ? X - g.nx : X);
+    if (g.per_y) Y = Y < 0 ? Y + g.ny : (Y >= g.ny ? Y - g.ny : Y);
+    if (g.per_z) Z = Z < 0 ? Z + g.nz : (Z >= g.nz ? Z - g.nz : Z);
+    return static_cast<long long>(Z) * g.plane + static_cast<long long>(Y) * g.pitch + X;
+}
+
+template <int Q, int i>
+__device__ __forceinline__ long long fill_pos(const Geo& g, int x, int y, int z, bool aa) {
+    using L = Lat<Q>;
+    constexpr int cx = L::c[i][0], cy = L::c[i][1], cz = L::c[i][2];
+    if (aa) return shifted(g, x, y, z, cx, cy, cz);
+    return static_cast<long long>(z) * g.plane + static_cast<long long>(y) * g.pitch + x;
+}
+
 // Stored state := equilibrium2<T>(T(rho), T(u)) for planes [z0, z0 + nzc).
 template <typename T, int Q>
 __global__ void k_fill_eq(T* origin, Geo g, const double* rho, const double* ux,
-                          const double* uy, const double* uz, int z0, int nzc) {
+                          const double* uy, const double* uz, int z0, int nzc, bool aa) {
     const long long n = static_cast<long long>(g.nx) * g.ny * nzc;
     for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
          c += (long long)gridDim.x * blockDim.x) {
@@ -41,10 +69,9 @@ __global__ void k_fill_eq(T* origin, Geo g, const double* rho, const double* ux,
         const T r = T(rho[c]);
         const T u[3] = {T(ux[c]), T(uy[c]), T(uz[c])};
         const T usqr = Cell<T, Q>::usqr_of(u);
-        const long long at = lin<T>(g, x, y, z);
         sfor<Q>([&](auto I) {
             constexpr int i = decltype(I)::value;
-            origin[i * g.dstride + at] = Cell<T, Q>::template eq2<i>(r, u, usqr);
+            origin[i * g.dstride + fill_pos<Q, i>(g, x, y, z, aa)] = Cell<T, Q>::template eq2<i>(r, u, usqr);
         });
     }
 }
@@ -53,7 +80,7 @@ __global__ void k_fill_eq(T* origin, Geo g, const double* rho, const double* ux,
 // sin / cos / cos(2x) tables (glibc, as the reference), then equilibrium2<T>.
 template <typename T, int Q>
 __global__ void k_fill_tgv(T* origin, Geo g, const double* s1, const double* c1,
-                           const double* c2, long long z_origin, double u_inf) {
+                           const double* c2, long long z_origin, double u_inf, bool aa) {
     const long long n = static_cast<long long>(g.nx) * g.ny * g.nz;
     for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
          c += (long long)gridDim.x * blockDim.x) {
@@ -68,27 +95,28 @@ __global__ void k_fill_tgv(T* origin, Geo g, const double* s1, const double* c1,
         const T r = T(rho);
         const T u[3] = {T(ux), T(uy), T(0.0)};
         const T usqr = Cell<T, Q>::usqr_of(u);
-        const long long at = lin<T>(g, x, y, z);
         sfor<Q>([&](auto I) {
             constexpr int i = decltype(I)::value;
-            origin[i * g.dstride + at] = Cell<T, Q>::template eq2<i>(r, u, usqr);
+            origin[i * g.dstride + fill_pos<Q, i>(g, x, y, z, aa)] = Cell<T, Q>::template eq2<i>(r, u, usqr);
         });
     }
 }
 
 // Box copy between the padded layout of one direction and a dense buffer
 // (x fastest). The box origin (bx0, by0, bz0) may be -1 (envelope).
+// (sx, sy, sz) shifts the layout position (AA odd layout), wrapped on periodic axes.
 template <typename TD, typename TS, bool TO_LAYOUT>
 __global__ void k_box_copy(TD* dst, const TS* src, Geo g, int bx0, int by0, int bz0, int ex,
-                           int ey, int ez) {
+                           int ey, int ez, int sx = 0, int sy = 0, int sz = 0) {
     const long long n = static_cast<long long>(ex) * ey * ez;
     for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
          c += (long long)gridDim.x * blockDim.x) {
         const int x = bx0 + int(c % ex);
         const int y = by0 + int((c / ex) % ey);
         const int z = bz0 + int(c / (static_cast<long long>(ex) * ey));
-        if constexpr (TO_LAYOUT) dst[lin<TD>(g, x, y, z)] = TD(src[c]);
-        else dst[c] = TD(src[lin<TS>(g, x, y, z)]);
+        const long long at = (sx | sy | sz) ? shifted(g, x, y, z, sx, sy, sz) : lin<TD>(g, x, y, z);
+        if constexpr (TO_LAYOUT) dst[at] = TD(src[c]);
+        else dst[c] = TD(src[at]);
     }
 }
 
@@ -196,8 +224,10 @@ Lattice::Lattice(const dlb_lattice_desc& desc, const DynamicsRegistry& reg) : d_
     if (d_.q != 19 && d_.q != 27) throw std::invalid_argument("q must be 19 or 27");
     if (d_.precision_bits != 32 && d_.precision_bits != 64)
         throw std::invalid_argument("precision must be 32 or 64");
-    if (d_.layout != DLB_LAYOUT_TWO_POP)
-        throw std::invalid_argument("layout not supported by this build (two-population only)");
+    if (d_.layout != DLB_LAYOUT_TWO_POP && d_.layout != DLB_LAYOUT_AA)
+        throw std::invalid_argument("layout must be DLB_LAYOUT_TWO_POP or DLB_LAYOUT_AA");
+    if (d_.layout == DLB_LAYOUT_AA && d_.global_nz != d_.dims[2])
+        throw std::invalid_argument("the AA layout runs single-slab lattices (use two-population for z-slabs)");
     if (d_.arith != DLB_ARITH_EXACT && d_.arith != DLB_ARITH_FAST)
         throw std::invalid_argument("arith must be DLB_ARITH_EXACT or DLB_ARITH_FAST");
     for (int a = 0; a < 3; ++a)
@@ -240,11 +270,13 @@ Lattice::Lattice(const dlb_lattice_desc& desc, const DynamicsRegistry& reg) : d_
     base_off_ = align_ + plane + pitch;  // interior (0,0,0)
 
     const std::size_t bytes = std::size_t(d_.q) * std::size_t(dstride) * std::size_t(s);
-    for (int b = 0; b < 2; ++b) {
+    const int nbuf = d_.layout == DLB_LAYOUT_AA ? 1 : 2;
+    for (int b = 0; b < nbuf; ++b) {
         cuda_check(cudaMalloc(&buf_[b], bytes), "cudaMalloc populations");
         cuda_check(cudaMemsetAsync(buf_[b], 0, bytes, stream_), "cudaMemset populations");
     }
-    device_bytes_ = int64_t(2 * bytes);
+    if (nbuf == 1) buf_[1] = buf_[0];
+    device_bytes_ = int64_t(nbuf * bytes);
     cuda_check(cudaMalloc(&d_flags_, 4 * sizeof(unsigned long long)), "cudaMalloc flags");
     cuda_check(cudaMemsetAsync(d_flags_, 0, 4 * sizeof(unsigned long long), stream_), "memset");
     cuda_check(cudaMalloc(&d_counter_, sizeof(unsigned int)), "cudaMalloc counter");
@@ -259,7 +291,8 @@ Lattice::~Lattice() {
     if (stream_) cudaStreamSynchronize(stream_);
     for (Peer* p : {&lower_, &upper_})
         for (void* v : p->ipc_opened) cudaIpcCloseMemHandle(v);
-    for (void* b : buf_) cudaFree(b);
+    cudaFree(buf_[0]);
+    if (buf_[1] != buf_[0]) cudaFree(buf_[1]);
     cudaFree(d_slot_);
     cudaFree(d_flags_);
     cudaFree(d_counter_);
@@ -343,7 +376,15 @@ void Lattice::set_uniform_slot(int32_t slot) {
 void Lattice::select_kernel() {
     km_needed_ = 0;
     for (int32_t s : present_slots_) km_needed_ |= kind_bits(chains_[std::size_t(s)]);
-    kernel_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_, d_.layout);
+    if (aa()) {
+        kernel_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_, LAYOUT_AA);
+        kernel_odd_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_, LAYOUT_AA_ODD);
+        if (kernel_ && kernel_odd_ && kernel_->km != kernel_odd_->km) kernel_odd_ = nullptr;
+        if (!kernel_ || !kernel_odd_)
+            throw std::invalid_argument("no AA kernel instantiation covers this dynamics set");
+        return;
+    }
+    kernel_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_, LAYOUT_TWO_POP);
     if (!kernel_) throw std::invalid_argument("no kernel instantiation covers this dynamics set");
 }
 
@@ -367,9 +408,17 @@ void Lattice::check_dispatch() const {
         throw ExchangeError("periodic z-slab is not linked to both neighbours");
 }
 
+void Lattice::reset_aa() {
+    if (!aa()) return;
+    const std::size_t bytes = std::size_t(d_.q) * std::size_t(geo_.dstride) * (d_.precision_bits / 8);
+    cuda_check(cudaMemsetAsync(buf_[0], 0, bytes, stream_), "memset");
+    aa_odd_layout_ = true;
+}
+
 void Lattice::fill_equilibrium(const double* rho, const double* ux, const double* uy,
                                const double* uz) {
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    reset_aa();
     const long long plane_cells = (long long)geo_.nx * geo_.ny;
     const int zc = int(std::max<long long>(1, (long long)(staging_bytes_ / 32) / plane_cells));
     double* st = static_cast<double*>(staging_);
@@ -385,11 +434,11 @@ void Lattice::fill_equilibrium(const double* rho, const double* ux, const double
         const int grid = grid_for(n);
         void* o = origin(cur_);
         if (d_.precision_bits == 64) {
-            if (d_.q == 19) k_fill_eq<double, 19><<<grid, 256, 0, stream_>>>((double*)o, geo_, st, st + n, st + 2 * n, st + 3 * n, z0, nzc);
-            else k_fill_eq<double, 27><<<grid, 256, 0, stream_>>>((double*)o, geo_, st, st + n, st + 2 * n, st + 3 * n, z0, nzc);
+            if (d_.q == 19) k_fill_eq<double, 19><<<grid, 256, 0, stream_>>>((double*)o, geo_, st, st + n, st + 2 * n, st + 3 * n, z0, nzc, aa());
+            else k_fill_eq<double, 27><<<grid, 256, 0, stream_>>>((double*)o, geo_, st, st + n, st + 2 * n, st + 3 * n, z0, nzc, aa());
         } else {
-            if (d_.q == 19) k_fill_eq<float, 19><<<grid, 256, 0, stream_>>>((float*)o, geo_, st, st + n, st + 2 * n, st + 3 * n, z0, nzc);
-            else k_fill_eq<float, 27><<<grid, 256, 0, stream_>>>((float*)o, geo_, st, st + n, st + 2 * n, st + 3 * n, z0, nzc);
+            if (d_.q == 19) k_fill_eq<float, 19><<<grid, 256, 0, stream_>>>((float*)o, geo_, st, st + n, st + 2 * n, st + 3 * n, z0, nzc, aa());
+            else k_fill_eq<float, 27><<<grid, 256, 0, stream_>>>((float*)o, geo_, st, st + n, st + 2 * n, st + 3 * n, z0, nzc, aa());
         }
         cuda_check(cudaGetLastError(), "k_fill_eq");
         cuda_check(cudaStreamSynchronize(stream_), "fill_equilibrium");
@@ -400,6 +449,7 @@ void Lattice::fill_tgv(int64_t L, double u_inf) {
     if (d_.dims[0] != L || d_.dims[1] != L || d_.global_nz != L)
         throw std::invalid_argument("TGV fill needs an L^3 domain");
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    reset_aa();
     // cases.cpp:145-156: x = 2 pi / L * (i + 0.5); glibc sin / cos on the host.
     const double scale = 2.0 * 3.14159265358979323846 / double(L);
     std::vector<double> tab(std::size_t(3 * L));
@@ -414,11 +464,11 @@ void Lattice::fill_tgv(int64_t L, double u_inf) {
     const int grid = grid_for(cells());
     void* o = origin(cur_);
     if (d_.precision_bits == 64) {
-        if (d_.q == 19) k_fill_tgv<double, 19><<<grid, 256, 0, stream_>>>((double*)o, geo_, st, st + L, st + 2 * L, d_.z_origin, u_inf);
-        else k_fill_tgv<double, 27><<<grid, 256, 0, stream_>>>((double*)o, geo_, st, st + L, st + 2 * L, d_.z_origin, u_inf);
+        if (d_.q == 19) k_fill_tgv<double, 19><<<grid, 256, 0, stream_>>>((double*)o, geo_, st, st + L, st + 2 * L, d_.z_origin, u_inf, aa());
+        else k_fill_tgv<double, 27><<<grid, 256, 0, stream_>>>((double*)o, geo_, st, st + L, st + 2 * L, d_.z_origin, u_inf, aa());
     } else {
-        if (d_.q == 19) k_fill_tgv<float, 19><<<grid, 256, 0, stream_>>>((float*)o, geo_, st, st + L, st + 2 * L, d_.z_origin, u_inf);
-        else k_fill_tgv<float, 27><<<grid, 256, 0, stream_>>>((float*)o, geo_, st, st + L, st + 2 * L, d_.z_origin, u_inf);
+        if (d_.q == 19) k_fill_tgv<float, 19><<<grid, 256, 0, stream_>>>((float*)o, geo_, st, st + L, st + 2 * L, d_.z_origin, u_inf, aa());
+        else k_fill_tgv<float, 27><<<grid, 256, 0, stream_>>>((float*)o, geo_, st, st + L, st + 2 * L, d_.z_origin, u_inf, aa());
     }
     cuda_check(cudaGetLastError(), "k_fill_tgv");
     cuda_check(cudaStreamSynchronize(stream_), "fill_tgv");
@@ -428,32 +478,42 @@ void Lattice::fill_tgv(int64_t L, double u_inf) {
 // chunked over z planes through the staging buffer.
 void Lattice::copy_canonical(void* host, bool to_device, bool as_double, int elem_bytes) {
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    if (to_device) reset_aa();
     const long long plane_cells = (long long)geo_.nx * geo_.ny;
     const long long n = cells();
     const int zc = int(std::max<long long>(1, (long long)staging_bytes_ / (8 * plane_cells)));
+    const int* cz_tab = d_.q == 19 ? kCz19 : kCz27;
     for (int i = 0; i < d_.q; ++i) {
+        // canonical direction i lives in layout direction li, shifted by sh (AA)
+        int li = i, sx = 0, sy = 0, sz = 0;
+        if (aa() && !aa_odd_layout_) li = i == 0 ? 0 : ((i & 1) ? i + 1 : i - 1);
+        if (aa() && aa_odd_layout_) {
+            sx = (d_.q == 19 ? kCx19 : kCx27)[i];
+            sy = (d_.q == 19 ? kCy19 : kCy27)[i];
+            sz = cz_tab[i];
+        }
         for (int z0 = 0; z0 < geo_.nz; z0 += zc) {
             const int nzc = std::min(zc, geo_.nz - z0);
             const long long cnt = plane_cells * nzc;
             char* h = static_cast<char*>(host) + (std::size_t(i) * n + plane_cells * z0) * elem_bytes;
             const int grid = grid_for(cnt);
-            char* o = static_cast<char*>(origin(cur_)) + std::size_t(i) * geo_.dstride * (d_.precision_bits / 8);
+            char* o = static_cast<char*>(origin(cur_)) + std::size_t(li) * geo_.dstride * (d_.precision_bits / 8);
             if (to_device) {
                 cuda_check(cudaMemcpyAsync(staging_, h, cnt * elem_bytes, cudaMemcpyHostToDevice, stream_), "h2d");
                 if (d_.precision_bits == 64)
-                    k_box_copy<double, double, true><<<grid, 256, 0, stream_>>>((double*)o, (const double*)staging_, geo_, 0, 0, z0, geo_.nx, geo_.ny, nzc);
+                    k_box_copy<double, double, true><<<grid, 256, 0, stream_>>>((double*)o, (const double*)staging_, geo_, 0, 0, z0, geo_.nx, geo_.ny, nzc, sx, sy, sz);
                 else if (as_double)
-                    k_box_copy<float, double, true><<<grid, 256, 0, stream_>>>((float*)o, (const double*)staging_, geo_, 0, 0, z0, geo_.nx, geo_.ny, nzc);
+                    k_box_copy<float, double, true><<<grid, 256, 0, stream_>>>((float*)o, (const double*)staging_, geo_, 0, 0, z0, geo_.nx, geo_.ny, nzc, sx, sy, sz);
                 else
-                    k_box_copy<float, float, true><<<grid, 256, 0, stream_>>>((float*)o, (const float*)staging_, geo_, 0, 0, z0, geo_.nx, geo_.ny, nzc);
+                    k_box_copy<float, float, true><<<grid, 256, 0, stream_>>>((float*)o, (const float*)staging_, geo_, 0, 0, z0, geo_.nx, geo_.ny, nzc, sx, sy, sz);
                 cuda_check(cudaGetLastError(), "k_box_copy");
             } else {
                 if (d_.precision_bits == 64)
-                    k_box_copy<double, double, false><<<grid, 256, 0, stream_>>>((double*)staging_, (const double*)o, geo_, 0, 0, z0, geo_.nx, geo_.ny, nzc);
+                    k_box_copy<double, double, false><<<grid, 256, 0, stream_>>>((double*)staging_, (const double*)o, geo_, 0, 0, z0, geo_.nx, geo_.ny, nzc, sx, sy, sz);
                 else if (as_double)
-                    k_box_copy<double, float, false><<<grid, 256, 0, stream_>>>((double*)staging_, (const float*)o, geo_, 0, 0, z0, geo_.nx, geo_.ny, nzc);
+                    k_box_copy<double, float, false><<<grid, 256, 0, stream_>>>((double*)staging_, (const float*)o, geo_, 0, 0, z0, geo_.nx, geo_.ny, nzc, sx, sy, sz);
                 else
-                    k_box_copy<float, float, false><<<grid, 256, 0, stream_>>>((float*)staging_, (const float*)o, geo_, 0, 0, z0, geo_.nx, geo_.ny, nzc);
+                    k_box_copy<float, float, false><<<grid, 256, 0, stream_>>>((float*)staging_, (const float*)o, geo_, 0, 0, z0, geo_.nx, geo_.ny, nzc, sx, sy, sz);
                 cuda_check(cudaGetLastError(), "k_box_copy");
                 cuda_check(cudaMemcpyAsync(h, staging_, cnt * elem_bytes, cudaMemcpyDeviceToHost, stream_), "d2h");
             }
@@ -519,7 +579,8 @@ void Lattice::download_block_interior(void* f, const int64_t ext[3], int which) 
             cudaMemcpy3DParms p{};
             p.srcPtr = make_cudaPitchedPtr(staging_, ext[0] * s, ext[0], ext[1]);
             p.srcPos = make_cudaPos(s, 1, 0);
-            p.dstPtr = make_cudaPitchedPtr(f, ext[0] * s, ext[0], ext[1]);
+            p.dstPtr = make_cudaPitchedPtr(static_cast<char*>(f) + std::size_t(i) * vol * s, ext[0] * s,
+                                           ext[0], ext[1]);
             p.dstPos = make_cudaPos(s, 1, z0);
             p.extent = make_cudaExtent((ext[0] - 2) * s, ext[1] - 2, nzc);
             p.kind = cudaMemcpyDeviceToHost;
@@ -532,8 +593,10 @@ void Lattice::download_block_interior(void* f, const int64_t ext[3], int which) 
 template <typename T>
 void Lattice::launch_step(int parity) {
     StepArgs<T> a{};
-    a.fin = static_cast<const T*>(origin(parity));
-    a.fout = static_cast<T*>(origin(1 - parity));
+    for (int i = 0; i < d_.q; ++i) {
+        a.fin[i] = static_cast<const T*>(origin(parity)) + i * geo_.dstride;
+        a.fout[i] = static_cast<T*>(origin(1 - parity)) + i * geo_.dstride;
+    }
     a.slot = d_slot_;
     a.uniform_slot = uniform_slot_;
     a.g = geo_;
@@ -547,6 +610,15 @@ void Lattice::launch_step(int parity) {
     const void* fn = kernel_->fn;
 
     const bool linked = lower_.linked || upper_.linked;
+    if (aa()) {
+        a.z_begin = 0;
+        a.z_step = 1;
+        void* args[] = {&a};
+        const void* kfn = aa_odd_layout_ ? kernel_->fn : kernel_odd_->fn;  // odd layout -> even kernel
+        cuda_check(cudaLaunchKernel(kfn, dim3(gx, gy, geo_.nz), block, args, 0, stream_), "launch");
+        aa_odd_layout_ = !aa_odd_layout_;
+        return;
+    }
     if (!linked) {
         a.z_begin = 0;
         a.z_step = 1;
@@ -593,7 +665,7 @@ void Lattice::launch_step(int parity) {
 void Lattice::enqueue_step() {
     if (d_.precision_bits == 64) launch_step<double>(cur_);
     else launch_step<float>(cur_);
-    cur_ = 1 - cur_;
+    if (!aa()) cur_ = 1 - cur_;
     ++steps_;
 }
 
@@ -602,6 +674,34 @@ void Lattice::step(int64_t nsteps) {
     check_dispatch();
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
     for (int64_t k = 0; k < nsteps; ++k) enqueue_step();
+}
+
+// MultiBlockRun::exchange (multiblock.hpp:142-143) for a z-slab: copy this
+// slab's top / bottom interior planes into the neighbours' ghost planes of the
+// CURRENT state buffer (whole planes; only the c_z-crossing directions are
+// read from there). Needed once before the first step after (re)filling the
+// state; afterwards every step's boundary launch pushes the halo itself.
+// Neighbours must be quiescent (lockstep, as in the reference).
+void Lattice::exchange() {
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    const int s = d_.precision_bits / 8;
+    const std::size_t plane_bytes = std::size_t(geo_.plane) * s;
+    auto plane_ptr = [&](void* origin_dir0, long long dstride, int i, int z) {
+        return static_cast<char*>(origin_dir0) +
+               (std::size_t(i) * dstride + std::size_t(z) * geo_.plane - geo_.pitch - 1) * s;
+    };
+    for (int i = 0; i < d_.q; ++i) {
+        const int cz = i == 0 ? 0 : (d_.q == 19 ? kCz19[i] : kCz27[i]);
+        if (cz > 0 && upper_.linked)
+            cuda_check(cudaMemcpyAsync(plane_ptr(upper_.buf[cur_], upper_.dstride, i, -1),
+                                       plane_ptr(origin(cur_), geo_.dstride, i, geo_.nz - 1),
+                                       plane_bytes, cudaMemcpyDefault, stream_), "halo exchange");
+        if (cz < 0 && lower_.linked)
+            cuda_check(cudaMemcpyAsync(plane_ptr(lower_.buf[cur_], lower_.dstride, i, lower_.nz),
+                                       plane_ptr(origin(cur_), geo_.dstride, i, 0),
+                                       plane_bytes, cudaMemcpyDefault, stream_), "halo exchange");
+    }
+    cuda_check(cudaStreamSynchronize(stream_), "halo exchange");
 }
 
 void Lattice::check_error_flag() {
@@ -633,6 +733,7 @@ double Lattice::time_steps(int64_t nsteps) {
 }
 
 void Lattice::link_lower(Lattice& lower) {
+    if (aa() || lower.aa()) throw std::invalid_argument("AA-layout lattices cannot be linked");
     // `lower` sits directly below this slab: lower's top plane feeds our ghost
     // z = -1, our bottom plane feeds lower's ghost z = lower.nz.
     if (lower.geo_.nx != geo_.nx || lower.geo_.ny != geo_.ny || lower.d_.q != d_.q ||
@@ -692,6 +793,7 @@ std::vector<uint8_t> Lattice::export_ipc() const {
 }
 
 void Lattice::link_ipc(int side, const void* blob, std::size_t len) {
+    if (aa()) throw std::invalid_argument("AA-layout lattices cannot be linked");
     if (len != sizeof(IpcBlob)) throw std::invalid_argument("bad IPC blob size");
     IpcBlob b;
     std::memcpy(&b, blob, sizeof(b));

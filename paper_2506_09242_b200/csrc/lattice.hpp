@@ -59,6 +59,7 @@ class Lattice {
     double time_steps(int64_t nsteps);
 
     void link_lower(Lattice& lower);  // same process
+    void exchange();                  // prime the neighbours' ghost planes
     std::vector<uint8_t> export_ipc() const;
     void link_ipc(int side, const void* blob, std::size_t len);
 
@@ -81,6 +82,8 @@ class Lattice {
     void copy_canonical(void* host, bool to_device, bool as_double, int elem_bytes);
     void* origin(int which) const;  // interior origin of direction 0 of buffer `which`
     bool split() const { return d_.global_nz != d_.dims[2]; }
+    bool aa() const { return d_.layout == DLB_LAYOUT_AA; }
+    void reset_aa();
     void check_error_flag();
 
     dlb_lattice_desc d_;
@@ -106,6 +109,8 @@ class Lattice {
     std::vector<std::string> tag_names_;
     unsigned km_needed_ = 0;
     const KernelEntry* kernel_ = nullptr;
+    const KernelEntry* kernel_odd_ = nullptr;  // AA: odd-step kernel (kernel_ is the even one)
+    bool aa_odd_layout_ = true;                // AA: state is in the odd / upload layout
     // halo
     Peer lower_, upper_;
     unsigned long long* d_flags_ = nullptr;  // [0] from lower, [1] from upper, [2] my step, [3] error

@@ -257,14 +257,34 @@ struct Cell {
         });
     }
 
+    // equilibrium2 of an opposite pair (i, i+1) sharing the terms that are
+    // exactly equal: cu_i = -cu_{i+1}, so 3 cu_i = -(3 cu_{i+1}) and
+    // (4.5 cu_i) cu_i = (4.5 cu_{i+1}) cu_{i+1} bit for bit; the series are then
+    // formed with the reference's association ((3cu + q) - 1.5 usqr).
+    template <int i>
+    static __device__ __forceinline__ void eq2_pair(T rho, const T (&u)[3], T u15, T& ei, T& ej) {
+        constexpr double wd = L::w[i];
+        const T w = T(wd);
+        const T cu = cdot<i + 1>(u);
+        const T t3 = T(3) * cu;
+        const T q = T(4.5) * cu * cu;
+        const T base = w * (rho - T(1));
+        const T wr = w * rho;
+        ej = base + wr * ((t3 + q) - u15);
+        ei = base + wr * ((q - t3) - u15);
+    }
+
     // collision.hpp:85-101, evaluated per opposite pair: the j member uses
     // fm_j = -fm_i and em_j = -em_i, which is exact in IEEE arithmetic.
     static __device__ __forceinline__ void trt(T (&f)[Q], T omega, T omega_minus) {
         T rho, u[3];
         rho_u(f, rho, u);
         const T usqr = usqr_of(u);
+        const T u15 = T(1.5) * usqr;
         {
-            const T e0 = eq2<0>(rho, u, usqr);
+            constexpr double wd0 = L::w[0];
+            const T w0 = T(wd0);
+            const T e0 = w0 * (rho - T(1)) + w0 * rho * (-u15);
             const T fp = (f[0] + f[0]) * T(0.5);
             const T fm = (f[0] - f[0]) * T(0.5);
             const T ep = (e0 + e0) * T(0.5);
@@ -273,8 +293,8 @@ struct Cell {
         }
         sfor<(Q - 1) / 2>([&](auto P) {
             constexpr int i = 2 * decltype(P)::value + 1;
-            const T ei = eq2<i>(rho, u, usqr);
-            const T ej = eq2<i + 1>(rho, u, usqr);
+            T ei, ej;
+            eq2_pair<i>(rho, u, u15, ei, ej);
             const T fi = f[i], fj = f[i + 1];
             const T fp = (fi + fj) * T(0.5);
             const T fm = (fi - fj) * T(0.5);
@@ -287,20 +307,29 @@ struct Cell {
         });
     }
 
-    // collision.hpp:108-164
+    // collision.hpp:108-164. f is overwritten by feq4 as soon as f_i - feq_i
+    // has entered the second moment (same per-component accumulation order),
+    // so only one q-array is live.
     static __device__ __forceinline__ void rr(T (&f)[Q], T omega, T omega_bulk_ho) {
         T rho, u[3];
         rho_u(f, rho, u);
         const T usqr = usqr_of(u);
-        T feq[Q];
-        T fn[Q];
+        Acc<T> acc[6];
         sfor<Q>([&](auto I) {
             constexpr int i = decltype(I)::value;
-            feq[i] = eq4<i>(rho, u, usqr);
-            fn[i] = f[i] - feq[i];
+            constexpr int cx = L::c[i][0], cy = L::c[i][1], cz = L::c[i][2];
+            const T feq = eq4<i>(rho, u, usqr);
+            const T fn = f[i] - feq;
+            if constexpr (cx * cx != 0) acc[0].add(1, fn);
+            if constexpr (cx * cy != 0) acc[1].add(cx * cy, fn);
+            if constexpr (cx * cz != 0) acc[2].add(cx * cz, fn);
+            if constexpr (cy * cy != 0) acc[3].add(1, fn);
+            if constexpr (cy * cz != 0) acc[4].add(cy * cz, fn);
+            if constexpr (cz * cz != 0) acc[5].add(1, fn);
+            f[i] = feq;
         });
         T a2[6];
-        second_moment(fn, a2);
+        for (int k = 0; k < 6; ++k) a2[k] = acc[k].get();
         const T trace3 = (a2[0] + a2[3] + a2[5]) / T(3);
         const T gdev = T(1) - omega;
         const T ghob = T(1) - omega_bulk_ho;
@@ -321,7 +350,7 @@ struct Cell {
             constexpr int i = decltype(I)::value;
             constexpr int cx = L::c[i][0], cy = L::c[i][1], cz = L::c[i][2];
             constexpr double wd = L::w[i];
-        const T wi = T(wd);
+            const T wi = T(wd);
             const T hxx = herm<cx>(), hyy = herm<cy>(), hzz = herm<cz>();
             const T second = h2_contract<i>(a2r);
             Acc<T> third;
@@ -333,7 +362,7 @@ struct Cell {
             if constexpr (cy != 0) third.add(cy, hzz * a3_zzy);
             T inner = T(4.5) * second;
             if (third.any) inner = inner + T(13.5) * third.s;
-            f[i] = feq[i] + wi * inner;
+            f[i] = f[i] + wi * inner;
         });
     }
 

@@ -268,6 +268,24 @@ def partition(n: int, k: int):
     return out
 
 
+def halo_neighbours(rank: int, world: int, periodic_z: bool):
+    """(lower, upper) neighbour ranks of a z-slab (None at a non-periodic end).
+    The plan of the reference's z sweep (multiblock.cpp:51-101) restricted to
+    one block per rank along z."""
+    lower = rank - 1 if rank > 0 else (world - 1 if periodic_z and world > 1 else None)
+    upper = rank + 1 if rank < world - 1 else (0 if periodic_z and world > 1 else None)
+    return lower, upper
+
+
+def exchange_blobs(blob: bytes):
+    """All-gather one opaque byte blob per rank over torch.distributed (the
+    transport for CUDA IPC handles; the data path itself is peer memory)."""
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, blob)
+    return out
+
+
 class _Lattice:
     """One z-slab handle."""
 
@@ -304,7 +322,7 @@ class DeviceRun:
 
     def __init__(self, dims, periodic, registry: DynamicsRegistry, dispatch: DispatchSet | None = None,
                  q: int = 19, precision: int = 64, slabs: int = 1, devices=None, arith: str = "exact",
-                 dist=None):
+                 dist=None, layout: str = "twopop"):
         self.dims = tuple(int(v) for v in dims)
         self.periodic = tuple(int(bool(p)) for p in periodic)
         self.registry = registry
@@ -323,7 +341,7 @@ class DeviceRun:
             for a in range(3):
                 d.periodic[a] = self.periodic[a]
             d.q, d.precision_bits = q, precision
-            d.layout = LAYOUT_TWO_POP
+            d.layout = _capi.LAYOUT_AA if layout == "aa" else LAYOUT_TWO_POP
             d.arith = ARITH_FAST if arith == "fast" else ARITH_EXACT
             d.device = devices[k]
             d.z_origin, d.global_nz = parts[r][0], self.dims[2]
@@ -340,23 +358,20 @@ class DeviceRun:
 
     # -- distributed linking over torch.distributed (plumbing only) --------------
     def _link_distributed(self):
-        import torch.distributed as dist
         rank, world = self.dist
         lat = self.slabs[0]
         n = C.c_size_t()
         check(_capi.lib().dlb_lattice_export_ipc(lat.handle, None, 0, C.byref(n)))
         buf = (C.c_uint8 * n.value)()
         check(_capi.lib().dlb_lattice_export_ipc(lat.handle, buf, n.value, C.byref(n)))
-        blobs = [None] * world
-        dist.all_gather_object(blobs, bytes(buf))
-        lower = rank - 1 if rank > 0 else (world - 1 if self.periodic[2] else None)
-        upper = rank + 1 if rank < world - 1 else (0 if self.periodic[2] else None)
-        for side, nb in ((0, lower), (1, upper)):
+        blobs = exchange_blobs(bytes(buf))
+        for side, nb in enumerate(halo_neighbours(rank, world, bool(self.periodic[2]))):
             if nb is None:
                 continue
             b = blobs[nb]
             cb = (C.c_uint8 * len(b)).from_buffer_copy(b)
             check(_capi.lib().dlb_lattice_link_ipc(lat.handle, side, cb, len(b)))
+        import torch.distributed as dist
         dist.barrier()
 
     # -- setup ------------------------------------------------------------------
@@ -408,6 +423,19 @@ class DeviceRun:
             self.fill_state()
         else:
             self.fill_state(*state)
+        self.exchange()
+
+    def exchange(self):
+        """Envelope (halo) exchange only, valid before the first step
+        (MultiBlockRun::exchange, multiblock.hpp:142-143). Called after every
+        state fill / upload of a decomposed run."""
+        if len(self.slabs) == 1 and self.dist is None:
+            return
+        for s in self.slabs:
+            check(_capi.lib().dlb_lattice_exchange(s.handle))
+        if self.dist is not None and self.dist[1] > 1:
+            import torch.distributed as dist
+            dist.barrier()
 
     def upload_populations(self, canon: np.ndarray):
         canon = np.asarray(canon, np.float64).reshape(self.q, -1)
@@ -416,6 +444,7 @@ class DeviceRun:
             z0, nz = self._slab_range(k)
             part = np.ascontiguousarray(canon[:, z0 * nxy:(z0 + nz) * nxy])
             check(_capi.lib().dlb_lattice_upload_populations(s.handle, part.ctypes.data))
+        self.exchange()
 
     # -- stepping ---------------------------------------------------------------
     def advance(self, nsteps: int):

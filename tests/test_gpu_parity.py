@@ -240,3 +240,52 @@ def test_mass_conservation_long_run():
     m1 = run.gather_populations().sum()
     n = 32 ** 3
     assert abs((n + m1) - (n + m0)) / n <= 1e-12
+
+
+# ---------------------------------------------------------------- AA pattern
+@pytest.mark.parametrize("name", ["tgv16_bgk_f64", "cavity32_trt_f32", "plates16_trt_vel_f64",
+                                  "tgv32_rr_f32", "sphere48_trt_f64_c4", "cavity64_bgk_f64_c1"])
+def test_aa_layout_bit_identical_to_reference(golden, name):
+    """In-place AA streaming (one array, half the memory) reproduces the
+    reference after the golden step count (canonical state recovered from the
+    even / odd layout on download)."""
+    setup, bits, steps = product_setup(CASES[name])
+    run = dlb.build_run(setup, precision=bits, layout="aa")
+    run.advance(steps)
+    assert canonical_hash(run.gather_populations()) == golden[name]["sha256"], run.kernel_name()
+    assert "k_aa" in run.kernel_name()
+
+
+@pytest.mark.parametrize("spec,steps", [
+    (dict(kind="tgv", L=12, Re=50.0, Ma=0.1, collision=TRT, bits=64), 7),
+    (dict(kind="cavity", L=18, Re=100.0, Ma=0.1, collision=BGK, bits=64), 13),
+    (dict(kind="porous", L=12, Ma=0.01, collision=TRT, bits=32, plate_layers=4, upstream=3,
+          downstream=3, drive="pressure"), 9),
+    (dict(kind="tgv", L=14, Re=400.0, Ma=0.2, collision=RR, q=27, bits=64), 5),
+])
+def test_aa_odd_and_even_counts_vs_oracle(oracle, spec, steps):
+    from golden_cases import make_case
+    setup, bits, _ = product_setup(dict(spec, steps=0))
+    run = dlb.build_run(setup, precision=bits, layout="aa")
+    case = make_case(dict(spec, steps=0))
+    dt = np.float64 if bits == 64 else np.float32
+    f = oracle.initial_state(case, dt)
+    dims, per, rec, slot = case.setup()
+    for chunk in (1, steps - 1, 1, 2):  # stop at odd and even counts, download each time
+        run.advance(chunk)
+        oracle.step(case.q, dims, per, rec, slot, f, chunk)
+        assert np.array_equal(run.gather_populations(), f.astype(np.float64))
+
+
+def test_aa_upload_mid_run(oracle):
+    case = Case(kind="tgv", L=10, Re=20.0, Ma=0.1, collision=BGK)
+    dims, per, rec, slot = case.setup()
+    f = oracle.initial_state(case, np.float64)
+    oracle.step(19, dims, per, rec, slot, f, 3)
+    setup, _, _ = product_setup(dict(kind="tgv", L=10, Re=20.0, Ma=0.1, collision=BGK, bits=64, steps=0))
+    run = dlb.build_run(setup, precision=64, layout="aa")
+    run.advance(1)  # leave the even layout, then overwrite the state
+    run.upload_populations(f)
+    run.advance(5)
+    oracle.step(19, dims, per, rec, slot, f, 5)
+    assert np.array_equal(run.gather_populations(), f)
