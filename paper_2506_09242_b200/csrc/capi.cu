@@ -6,6 +6,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/dlb.h"
@@ -321,29 +322,42 @@ DLB_API dlb_status dlb_collide_and_stream(const dlb_registry* reg, dlb_block_vie
         const int64_t nx = block->interior[0], ny = block->interior[1], nz = block->interior[2];
         if (nx < 1 || ny < 1 || nz < 1) throw std::invalid_argument("block extents must be >= 1");
         const int64_t ext[3] = {nx + 2, ny + 2, nz + 2};
-        // Eager tag scan (accelerated_lattice.cpp:161-181): fail before any write.
+        // Eager tag scan (accelerated_lattice.cpp:161-181): fail before any
+        // write. Parallel over z; each worker also extracts the slot indices.
+        const int ntags = reg->reg.num_tags();
         std::vector<int32_t> slots(size_t(nx * ny * nz));
-        std::vector<char> seen_tag(size_t(reg->reg.num_tags()) + 1, 0);
-        bool untagged = false;
-        int64_t k = 0;
-        for (int64_t z = 1; z <= nz; ++z)
-            for (int64_t y = 1; y <= ny; ++y) {
-                const int64_t row = (z * ext[1] + y) * ext[0];
-                for (int64_t x = 1; x <= nx; ++x, ++k) {
-                    const int32_t t = block->tag[row + x];
-                    if (t < 0 || t >= reg->reg.num_tags()) untagged = untagged || t < 0;
-                    else seen_tag[size_t(t)] = 1;
-                    slots[size_t(k)] = block->param_index[row + x];
-                }
-            }
-        std::vector<char> allowed(seen_tag.size(), 0);
+        const int nw = int(std::max<int64_t>(1, std::min<int64_t>(nz, std::thread::hardware_concurrency())));
+        std::vector<std::vector<char>> seen(size_t(nw), std::vector<char>(size_t(ntags), 0));
+        std::vector<char> untagged(size_t(nw), 0), unknown(size_t(nw), 0);
+        std::vector<std::thread> th;
+        for (int w = 0; w < nw; ++w) {
+            th.emplace_back([&, w] {
+                for (int64_t z = 1 + nz * w / nw; z < 1 + nz * (w + 1) / nw; ++z)
+                    for (int64_t y = 1; y <= ny; ++y) {
+                        const int64_t row = (z * ext[1] + y) * ext[0];
+                        int64_t k = ((z - 1) * ny + (y - 1)) * nx;
+                        for (int64_t x = 1; x <= nx; ++x, ++k) {
+                            const int32_t t = block->tag[row + x];
+                            if (t >= 0 && t < ntags) seen[size_t(w)][size_t(t)] = 1;
+                            else if (t < 0) untagged[size_t(w)] = 1;
+                            else unknown[size_t(w)] = 1;
+                            slots[size_t(k)] = block->param_index[row + x];
+                        }
+                    }
+            });
+        }
+        for (auto& t : th) t.join();
+        std::vector<char> allowed(size_t(ntags), 0);
         for (size_t d = 0; d < n_dispatch; ++d)
-            if (dispatch_tags[d] >= 0 && size_t(dispatch_tags[d]) < allowed.size())
-                allowed[size_t(dispatch_tags[d])] = 1;
-        if (untagged) throw dlb::DispatchError("<untagged cell>");
-        for (int t = 0; t < reg->reg.num_tags(); ++t)
-            if (seen_tag[size_t(t)] && !allowed[size_t(t)])
-                throw dlb::DispatchError(reg->reg.chain_for(t));
+            if (dispatch_tags[d] >= 0 && dispatch_tags[d] < ntags) allowed[size_t(dispatch_tags[d])] = 1;
+        for (int w = 0; w < nw; ++w) {
+            if (untagged[size_t(w)]) throw dlb::DispatchError("<untagged cell>");
+            if (unknown[size_t(w)]) throw std::out_of_range("block holds a tag that is not registered");
+        }
+        for (int t = 0; t < ntags; ++t)
+            for (int w = 0; w < nw; ++w)
+                if (seen[size_t(w)][size_t(t)] && !allowed[size_t(t)])
+                    throw dlb::DispatchError(reg->reg.chain_for(t));
 
         std::lock_guard<std::mutex> lock(g_block_mu);
         const std::vector<int64_t> key = {nx, ny, nz, block->q, block->precision_bits};
@@ -367,15 +381,25 @@ DLB_API dlb_status dlb_collide_and_stream(const dlb_registry* reg, dlb_block_vie
         }
         if (ctx.slots != slots) {
             ctx.lat->set_slots(slots.data());
-            ctx.slots = slots;
+            ctx.slots.swap(slots);
         }
         const size_t bytes = size_t(block->q) * size_t(ext[0] * ext[1] * ext[2]) *
                              size_t(block->precision_bits / 8);
-        ctx.lat->upload_block(block->f_in, ext);
-        ctx.lat->enqueue_step();
         if (block->f_out) std::memcpy(block->f_out, block->f_in, bytes);
-        ctx.lat->download_block_interior(block->f_in, ext, 0);
-        ctx.lat->synchronize();
+        cudaPointerAttributes attr{};
+        const bool pinned = cudaPointerGetAttributes(&attr, block->f_in) == cudaSuccess &&
+                            attr.type == cudaMemoryTypeHost && attr.devicePointer == block->f_in;
+        cudaGetLastError();
+        if (pinned) {
+            // zero-copy: PCIe pulls + overlapped copy-back (Lattice::step_host_block)
+            ctx.lat->step_host_block(block->f_in, ext);
+        } else {
+            // pageable memory: staged copies through device memory
+            ctx.lat->upload_block(block->f_in, ext);
+            ctx.lat->enqueue_step();
+            ctx.lat->download_block_interior(block->f_in, ext, 0);
+            ctx.lat->synchronize();
+        }
     });
 }
 

@@ -297,6 +297,9 @@ Lattice::~Lattice() {
     cudaFree(d_flags_);
     cudaFree(d_counter_);
     cudaFree(staging_);
+    cudaFree(blk_out_);
+    for (cudaEvent_t e : blk_ev_) cudaEventDestroy(e);
+    if (copy_stream_) cudaStreamDestroy(copy_stream_);
     if (ev0_) cudaEventDestroy(ev0_);
     if (ev1_) cudaEventDestroy(ev1_);
     if (stream_) cudaStreamDestroy(stream_);
@@ -588,6 +591,87 @@ void Lattice::download_block_interior(void* f, const int64_t ext[3], int which) 
             cuda_check(cudaStreamSynchronize(stream_), "download_block");
         }
     }
+}
+
+template <typename T>
+void Lattice::fill_recipes(StepArgs<T>& a) const {
+    a.slot = d_slot_;
+    a.uniform_slot = uniform_slot_;
+    for (std::size_t s = 0; s < chains_.size(); ++s) a.rec[s] = compile_recipe<T>(chains_[s]);
+}
+
+template <typename T>
+void Lattice::launch_host_block(void* f_in, const int64_t ext[3]) {
+    const long long vol = ext[0] * ext[1] * ext[2];
+    Geo hg{};
+    hg.nx = geo_.nx;
+    hg.ny = geo_.ny;
+    hg.nz = geo_.nz;
+    hg.pitch = int(ext[0]);
+    hg.plane = int(ext[0] * ext[1]);
+    hg.dstride = vol;
+    hg.per_x = hg.per_y = hg.per_z = 0;  // the caller's envelope is authoritative
+    const std::size_t bytes = std::size_t(d_.q) * vol * sizeof(T);
+    if (blk_out_bytes_ < bytes) {
+        cudaFree(blk_out_);
+        blk_out_ = nullptr;
+        cuda_check(cudaMalloc(&blk_out_, bytes), "cudaMalloc block mirror");
+        blk_out_bytes_ = bytes;
+    }
+    if (!copy_stream_) cuda_check(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking), "stream");
+    StepArgs<T> a{};
+    fill_recipes(a);
+    a.g = hg;
+    const long long org = hg.plane + hg.pitch + 1;
+    for (int i = 0; i < d_.q; ++i) {
+        a.fin[i] = static_cast<const T*>(f_in) + i * vol + org;
+        a.fout[i] = static_cast<T*>(blk_out_) + i * vol + org;
+    }
+    const int bx = hg.nx >= 128 ? 128 : (hg.nx > 32 ? 64 : 32);
+    const int by = 256 / bx;
+    const dim3 block(bx, by, 1);
+    const unsigned gx = unsigned((hg.nx + bx - 1) / bx), gy = unsigned((hg.ny + by - 1) / by);
+    // ~8 chunks: the copy-back of chunk k overlaps the PCIe pulls of chunk k + 1
+    const int zc = std::max(1, (hg.nz + 7) / 8);
+    const int nchunks = (hg.nz + zc - 1) / zc;
+    while (int(blk_ev_.size()) < nchunks) {
+        cudaEvent_t e;
+        cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        blk_ev_.push_back(e);
+    }
+    const std::size_t plane_bytes = std::size_t(hg.plane) * sizeof(T);
+    int written = 0;  // interior planes [0, written) already copied back
+    auto copy_back = [&](int upto) {
+        if (upto <= written) return;
+        for (int i = 0; i < d_.q; ++i) {
+            const std::size_t off = (std::size_t(i) * vol + std::size_t(written + 1) * hg.plane) * sizeof(T);
+            cuda_check(cudaMemcpyAsync(static_cast<char*>(f_in) + off, static_cast<char*>(blk_out_) + off,
+                                       std::size_t(upto - written) * plane_bytes, cudaMemcpyDeviceToHost,
+                                       copy_stream_), "d2h");
+        }
+        written = upto;
+    };
+    for (int c = 0; c < nchunks; ++c) {
+        const int z0 = c * zc, z1 = std::min(hg.nz, z0 + zc);
+        a.z_begin = z0;
+        a.z_step = 1;
+        void* args[] = {&a};
+        cuda_check(cudaLaunchKernel(kernel_->fn, dim3(gx, gy, z1 - z0), block, args, 0, stream_), "launch");
+        cuda_check(cudaEventRecord(blk_ev_[c], stream_), "event");
+        // plane p of the old state is read by planes p-1..p+1: planes < z1 - 1 are free
+        cuda_check(cudaStreamWaitEvent(copy_stream_, blk_ev_[c], 0), "wait");
+        copy_back(z1 == hg.nz ? hg.nz : z1 - 1);
+    }
+    cuda_check(cudaStreamSynchronize(copy_stream_), "block copy-back");
+    cuda_check(cudaStreamSynchronize(stream_), "block step");
+}
+
+void Lattice::step_host_block(void* f_in, const int64_t ext[3]) {
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    if (aa()) throw std::invalid_argument("host-block stepping uses the two-population layout");
+    if (d_.precision_bits == 64) launch_host_block<double>(f_in, ext);
+    else launch_host_block<float>(f_in, ext);
+    ++steps_;
 }
 
 template <typename T>

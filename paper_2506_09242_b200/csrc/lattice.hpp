@@ -52,6 +52,13 @@ class Lattice {
     // Envelope-inclusive host block (AcceleratedBlock layout) in the storage type.
     void upload_block(const void* f, const int64_t ext[3]);
     void download_block_interior(void* f, const int64_t ext[3], int which);
+    // One step of a caller-owned, page-locked AcceleratedBlock (envelope
+    // included, refreshed by the caller): the kernel pulls f_in straight from
+    // host memory across PCIe (mapped pinned memory), writes the new state to
+    // a device mirror, and finished z-chunks are copied back into f_in on a
+    // second stream as soon as no later plane still reads them, so the PCIe
+    // reads and writes overlap.
+    void step_host_block(void* f_in, const int64_t ext[3]);
     void step(int64_t nsteps);
     void enqueue_step();  // one step, no dispatch check (group stepping)
     void check_dispatch() const;
@@ -119,6 +126,15 @@ class Lattice {
     int64_t device_bytes_ = 0;
     void* staging_ = nullptr;
     std::size_t staging_bytes_ = 0;
+    // host-block (zero-copy) path
+    void* blk_out_ = nullptr;
+    std::size_t blk_out_bytes_ = 0;
+    cudaStream_t copy_stream_ = nullptr;
+    std::vector<cudaEvent_t> blk_ev_;
+    template <typename T>
+    void fill_recipes(StepArgs<T>& a) const;
+    template <typename T>
+    void launch_host_block(void* f_in, const int64_t ext[3]);
 };
 
 // Sphere-pack porous medium generator (cases.cpp raw voxel format).
