@@ -39,6 +39,9 @@ CONFIGS = {
            "Taylor-Green vortex Re=1600 D3Q27 recursive-regularized 256^3 fp64"),
     "c3": ("cavity", 512, 1000.0, 0.1, "TRT", 19, 32, "weak",
            "lid-driven cavity D3Q19 TRT 512^3 per GPU fp32 (weak scaling)"),
+    "c4": ("porous", 600, 0.0, 0.01, "TRT", 19, 64, "strong",
+           "synthetic Berea-like porous medium: seeded sphere pack (R=8, ~20% porosity) 600^3 "
+           "+ 40/40 fluid buffers, D3Q19 TRT fp64, bounce-back, regularized velocity inlet/outlet"),
     "c5": ("tgv", 1024, 1600.0, 0.2, "BGK", 19, 32, "strong",
            "Taylor-Green vortex D3Q19 BGK 1024^3 fp32 (strong scaling)"),
 }
@@ -111,7 +114,19 @@ def cpu_reference(kind, L, Re, Ma, collision, q, bits, warmup, steps, reps=3):
     if not Reference.available():
         return None
     workers = min(os.cpu_count() or 1, L, 64)
-    case = Case(kind=kind, L=L, Re=Re, Ma=Ma, collision={"BGK": BGK, "TRT": TRT, "RR": RR}[collision])
+    cid = {"BGK": BGK, "TRT": TRT, "RR": RR}[collision]
+    if kind == "porous":
+        # same recipe at a bounded size: seeded sphere pack (R=8, 20 %) + 40/40 buffers
+        import tempfile
+
+        import paper_2506_09242_b200 as dlb
+        vox, _ = dlb.sphere_pack((L, L, L), radius=8.0, porosity=0.20, seed=20250611)
+        path = os.path.join(tempfile.gettempdir(), f"dlb_sphere_{L}.raw")
+        vox.tofile(path)
+        case = Case(kind="porous", L=L, Ma=Ma, collision=cid, tau=1.0, geometry=path,
+                    voxel_dims=(L, L, L), upstream=40, downstream=40)
+    else:
+        case = Case(kind=kind, L=L, Re=Re, Ma=Ma, collision=cid)
     mean, reps_ = Reference().bench(case, bits, workers, warmup, steps, reps)
     return mean, reps_, workers
 
@@ -212,6 +227,7 @@ def main():
     ap.add_argument("--arith", default="exact", choices=["exact", "fast"])
     ap.add_argument("--layout", default="twopop", choices=["twopop", "aa"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dense", action="store_true", help="c4: sweep NoDynamics cells too (reference behaviour)")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
 
@@ -236,11 +252,26 @@ def main():
     if args.L:
         L = args.L
     lt = {"BGK": dlb.LinkType.BGK, "TRT": dlb.LinkType.TRT, "RR": dlb.LinkType.RR}[coll]
-    cfg = dlb.CaseConfig(kind=kind, L=L, Re=Re, Ma=Ma, collision=lt, q=q)
-    setup = dlb.init_tgv(cfg) if kind == "tgv" else dlb.init_cavity(cfg)
+    skip = False
+    extra = {}
+    if kind == "porous":
+        cfg = dlb.CaseConfig(kind="porous", L=L, Ma=Ma, collision=lt, q=q, tau=1.0, upstream=40,
+                             downstream=40)
+        vox, phi = dlb.sphere_pack((L, L, L), radius=8.0, porosity=0.20, seed=20250611)
+        setup = dlb.init_porous(cfg, solid=(vox == 255))
+        kinds = np.bincount(np.asarray(setup.chain_index).reshape(-1), minlength=5)
+        skip = not args.dense
+        extra = {"porosity": phi, "fluid_cells": int(kinds[0] + kinds[3] + kinds[4]),
+                 "bounce_back_cells": int(kinds[1]), "no_dynamics_cells": int(kinds[2]),
+                 "variant": "dense sweep" if args.dense else "masked (NoDynamics skipped)"}
+        del vox
+    else:
+        cfg = dlb.CaseConfig(kind=kind, L=L, Re=Re, Ma=Ma, collision=lt, q=q)
+        setup = dlb.init_tgv(cfg) if kind == "tgv" else dlb.init_cavity(cfg)
     layout = args.layout if world == 1 else "twopop"  # AA runs single-slab lattices
     run = dlb.build_run(setup, precision=bits, arith=args.arith,
-                        dist=(rank, world) if world > 1 else None, devices=[local], layout=layout)
+                        dist=(rank, world) if world > 1 else None, devices=[local], layout=layout,
+                        skip_nodynamics=skip)
     cells_total = run.num_cells()
     bpc, dev_bytes, launches = run.traffic()
 
@@ -265,7 +296,12 @@ def main():
     # roofline of the dominant kernel (the fused collide-stream launch(es) of a step)
     my_cells = run.dims[0] * run.dims[1] * sum(p[1] for k, p in enumerate(run.parts) if k in run.ranks)
     peak, peak_kind = measured_peak_hbm()
-    achieved = bpc * my_cells / (ms / args.steps * 1e-3) / 1e9
+    alg_bytes = bpc * my_cells
+    if skip:  # only fluid + bounce-back cells move populations; every cell reads its u8 slot
+        active = extra["fluid_cells"] + extra["bounce_back_cells"]
+        alg_bytes = (bpc - 1) * active + my_cells
+        extra["mlups_per_fluid_cell"] = mlups * extra["fluid_cells"] / cells_total
+    achieved = alg_bytes / (ms / args.steps * 1e-3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
@@ -285,7 +321,7 @@ def main():
 
     cpu = None
     if world == 1 and not args.no_cpu and q == 19:
-        Ls = min(L, 128)
+        Ls = min(L, 128 if kind != "porous" else 96)
         res = cpu_reference(kind, Ls, Re, Ma, coll, q, bits, 2, 8, reps=3)
         if res:
             mean, reps_, workers = res
@@ -305,7 +341,7 @@ def main():
                    "parallelism": f"z-slab x{world}",
                    "layout": "AA in-place SoA" if layout == "aa" else "two-population SoA",
                    "arith": args.arith, "l2": "inputs larger than L2 (state resident in HBM)",
-                   "device_bytes_per_gpu": dev_bytes},
+                   "device_bytes_per_gpu": dev_bytes, **extra},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "bytes_per_cell": bpc},

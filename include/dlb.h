@@ -87,7 +87,14 @@ typedef struct dlb_lattice_desc {
     int32_t device;          /* CUDA ordinal */
     int64_t z_origin;        /* global z index of the slab's first interior plane */
     int64_t global_nz;       /* global z extent (== dims[2] for a single slab) */
+    int32_t flags;           /* DLB_FLAG_* */
+    int32_t reserved;
 } dlb_lattice_desc;
+
+/* Masked porous variant: cells whose dynamics is NoDynamics are neither loaded
+ * nor stored (their stored state is never consumed by a fluid cell, so every
+ * Collide-kind cell stays bit-identical to the reference). */
+#define DLB_FLAG_SKIP_NODYNAMICS 1
 
 DLB_API dlb_status dlb_lattice_create(const dlb_lattice_desc* desc, const dlb_registry* reg,
                                       dlb_lattice** out);

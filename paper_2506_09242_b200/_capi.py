@@ -48,7 +48,11 @@ class LatticeDesc(C.Structure):
         ("dims", C.c_int64 * 3), ("periodic", C.c_int32 * 3), ("q", C.c_int32),
         ("precision_bits", C.c_int32), ("layout", C.c_int32), ("arith", C.c_int32),
         ("device", C.c_int32), ("z_origin", C.c_int64), ("global_nz", C.c_int64),
+        ("flags", C.c_int32), ("reserved", C.c_int32),
     ]
+
+
+FLAG_SKIP_NODYNAMICS = 1
 
 
 class BlockView(C.Structure):

@@ -28,7 +28,17 @@ __global__ void __launch_bounds__(256, 2) k_pull(const __grid_constant__ StepArg
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int y = blockIdx.y * blockDim.y + threadIdx.y;
     const int z = a.z_begin + int(blockIdx.z) * a.z_step;
-    const bool active = x < g.nx && y < g.ny;
+    bool active = x < g.nx && y < g.ny;
+    int s = a.uniform_slot;
+    if constexpr ((KM & KM_SKIP) != 0) {
+        // masked porous variant: NoDynamics cells (solids without a fluid
+        // neighbour, cases.cpp:239-249) are neither loaded nor stored; their
+        // values are never consumed by a fluid cell.
+        if (active && a.slot != nullptr) {
+            s = a.slot[(static_cast<long long>(z) * g.ny + y) * g.nx + x];
+            active = a.rec[s].kind != KIND_NODYN;
+        }
+    }
     if (active) {
         // Source coordinates of the pull f_i(x) <- f_i(x - c_i).
         const int xm = (x == 0 && g.per_x) ? g.nx - 1 : x - 1;
@@ -48,9 +58,10 @@ __global__ void __launch_bounds__(256, 2) k_pull(const __grid_constant__ StepArg
             f[i] = __ldg(a.fin[i] + (sz * g.plane + sy * g.pitch + sx));
         });
 
-        int s = a.uniform_slot;
-        if (a.slot != nullptr) s = a.slot[(static_cast<long long>(z) * g.ny + y) * g.nx + x];
-        Cell<T, Q>::template apply<KM>(f, a.rec[s]);
+        if constexpr ((KM & KM_SKIP) == 0) {
+            if (a.slot != nullptr) s = a.slot[(static_cast<long long>(z) * g.ny + y) * g.nx + x];
+        }
+        Cell<T, Q>::template apply<KM & ~KM_SKIP>(f, a.rec[s]);
 
         const int center = z * g.plane + y * g.pitch + x;
         sfor<Q>([&](auto I) {
@@ -203,9 +214,13 @@ __global__ void __launch_bounds__(256, 2) k_aa(const __grid_constant__ StepArgs<
         ENTRY(T, 19, KM_RR | KM_BB | KM_MBB),                                             \
         ENTRY(T, 19, KM_BGK | KM_BB | KM_NODYN | KM_REGV | KM_REGP),                      \
         ENTRY(T, 19, KM_TRT | KM_BB | KM_NODYN | KM_REGV | KM_REGP),                      \
-        ENTRY(T, 19, KM_RR | KM_BB | KM_NODYN | KM_REGV | KM_REGP), ENTRY(T, 19, KM_ALL)
+        ENTRY(T, 19, KM_RR | KM_BB | KM_NODYN | KM_REGV | KM_REGP), ENTRY(T, 19, KM_ALL),        \
+        ENTRY(T, 19, KM_BGK | KM_BB | KM_NODYN | KM_REGV | KM_REGP | KM_SKIP),                  \
+        ENTRY(T, 19, KM_TRT | KM_BB | KM_NODYN | KM_REGV | KM_REGP | KM_SKIP),                  \
+        ENTRY(T, 19, KM_RR | KM_BB | KM_NODYN | KM_REGV | KM_REGP | KM_SKIP), ENTRY(T, 19, KM_ALL | KM_SKIP)
 
-#define Q27_SET(T) ENTRY(T, 27, KM_BGK), ENTRY(T, 27, KM_TRT), ENTRY(T, 27, KM_RR), ENTRY(T, 27, KM_ALL)
+#define Q27_SET(T) ENTRY(T, 27, KM_BGK), ENTRY(T, 27, KM_TRT), ENTRY(T, 27, KM_RR), ENTRY(T, 27, KM_ALL), \
+        ENTRY(T, 27, KM_ALL | KM_SKIP)
 
 static const KernelEntry kTable[] = {
     Q19_SET(float), Q19_SET(double), Q27_SET(float), Q27_SET(double), AA_SET(float), AA_SET(double),

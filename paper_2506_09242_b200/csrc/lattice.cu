@@ -157,7 +157,7 @@ const KernelEntry* find_kernel(int arith, int bits, int q, unsigned km, int layo
     for (int k = 0; k < n; ++k) {
         const KernelEntry& e = t[k];
         if (e.precision_bits != bits || e.q != q || e.layout != layout) continue;
-        if ((e.km & km) != km) continue;
+        if ((e.km & km) != km || (e.km & KM_SKIP) != (km & KM_SKIP)) continue;
         if (!best || __builtin_popcount(e.km) < __builtin_popcount(best->km)) best = &e;
     }
     return best;
@@ -379,6 +379,7 @@ void Lattice::set_uniform_slot(int32_t slot) {
 void Lattice::select_kernel() {
     km_needed_ = 0;
     for (int32_t s : present_slots_) km_needed_ |= kind_bits(chains_[std::size_t(s)]);
+    if ((d_.flags & DLB_FLAG_SKIP_NODYNAMICS) && (km_needed_ & KM_NODYN) && !aa()) km_needed_ |= KM_SKIP;
     if (aa()) {
         kernel_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_, LAYOUT_AA);
         kernel_odd_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_, LAYOUT_AA_ODD);

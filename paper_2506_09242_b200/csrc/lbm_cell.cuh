@@ -113,6 +113,7 @@ enum : unsigned {
     KM_NODYN = 1u, KM_BB = 2u, KM_MBB = 4u, KM_BGK = 8u, KM_TRT = 16u, KM_RR = 32u,
     KM_LES = 64u, KM_REGV = 128u, KM_REGP = 256u,
     KM_ALL = 511u,
+    KM_SKIP = 512u,  // variant flag: NoDynamics cells skipped (no loads / stores)
 };
 
 template <typename T, int Q>
