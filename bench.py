@@ -190,13 +190,8 @@ def e2e_block(L, bits, steps, warmup):
         pidx = np.where(tag >= 0, slot, -1).astype(np.int32)
         ds = dlb.DispatchSet.all_of(reg)
 
-        def refresh():  # refresh_envelope_periodic (accelerated_lattice.cpp:202-238)
-            blk[:, 0, :, :] = blk[:, L, :, :]
-            blk[:, L + 1, :, :] = blk[:, 1, :, :]
-            blk[:, :, 0, :] = blk[:, :, L, :]
-            blk[:, :, L + 1, :] = blk[:, :, 1, :]
-            blk[:, :, :, 0] = blk[:, :, :, L]
-            blk[:, :, :, L + 1] = blk[:, :, :, 1]
+        def refresh():  # refresh_envelope_periodic (accelerated_lattice.cpp:202-238), C ABI
+            dlb.refresh_envelope_periodic(blk, (1, 1, 1))
 
         for _ in range(warmup):
             refresh()

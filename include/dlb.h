@@ -170,6 +170,10 @@ typedef struct dlb_block_view {
 DLB_API dlb_status dlb_collide_and_stream(const dlb_registry* reg, dlb_block_view* block,
                                           const int32_t* dispatch_tags, size_t n_dispatch,
                                           int32_t nthreads);
+/* refresh_envelope_periodic<T> (accelerated_lattice.hpp:130-132) on the same
+ * host block: copy interior edge planes into the opposite envelope along the
+ * periodic axes (x, then y over full x rows, then z over full planes). */
+DLB_API dlb_status dlb_refresh_envelope_periodic(dlb_block_view* block, const int32_t* periodic);
 /* Pinned host memory for the block API (page-locked, for full-rate copies). */
 DLB_API dlb_status dlb_host_alloc(size_t bytes, void** out);
 DLB_API void dlb_host_free(void* ptr);

@@ -100,6 +100,7 @@ _SIGS = {
     "dlb_lattice_link_ipc": ([C.c_void_p, C.c_int32, C.c_void_p, C.c_size_t], C.c_int),
     "dlb_lattices_step": ([C.c_void_p, C.c_size_t, C.c_int64], C.c_int),
     "dlb_collide_and_stream": ([C.c_void_p, C.POINTER(BlockView), C.c_void_p, C.c_size_t, C.c_int32], C.c_int),
+    "dlb_refresh_envelope_periodic": ([C.POINTER(BlockView), C.c_void_p], C.c_int),
     "dlb_host_alloc": ([C.c_size_t, C.POINTER(C.c_void_p)], C.c_int),
     "dlb_host_free": ([C.c_void_p], None),
     "dlb_case_sphere_pack": ([C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_uint64,

@@ -323,30 +323,40 @@ DLB_API dlb_status dlb_collide_and_stream(const dlb_registry* reg, dlb_block_vie
         if (nx < 1 || ny < 1 || nz < 1) throw std::invalid_argument("block extents must be >= 1");
         const int64_t ext[3] = {nx + 2, ny + 2, nz + 2};
         // Eager tag scan (accelerated_lattice.cpp:161-181): fail before any
-        // write. Parallel over z; each worker also extracts the slot indices.
+        // write. Parallel over z; the workers also compare param_index with
+        // the slots the cached device lattice holds (re-upload only on change).
         const int ntags = reg->reg.num_tags();
-        std::vector<int32_t> slots(size_t(nx * ny * nz));
+        std::lock_guard<std::mutex> lock(g_block_mu);
+        const std::vector<int64_t> key = {nx, ny, nz, block->q, block->precision_bits};
+        BlockCtx& ctx = g_blocks[key];
+        const bool have_ctx = ctx.lat && ctx.reg == reg && ctx.instances == reg->reg.num_instances() &&
+                              ctx.slots.size() == size_t(nx * ny * nz);
         const int nw = int(std::max<int64_t>(1, std::min<int64_t>(nz, std::thread::hardware_concurrency())));
         std::vector<std::vector<char>> seen(size_t(nw), std::vector<char>(size_t(ntags), 0));
-        std::vector<char> untagged(size_t(nw), 0), unknown(size_t(nw), 0);
-        std::vector<std::thread> th;
-        for (int w = 0; w < nw; ++w) {
-            th.emplace_back([&, w] {
-                for (int64_t z = 1 + nz * w / nw; z < 1 + nz * (w + 1) / nw; ++z)
-                    for (int64_t y = 1; y <= ny; ++y) {
-                        const int64_t row = (z * ext[1] + y) * ext[0];
-                        int64_t k = ((z - 1) * ny + (y - 1)) * nx;
-                        for (int64_t x = 1; x <= nx; ++x, ++k) {
-                            const int32_t t = block->tag[row + x];
-                            if (t >= 0 && t < ntags) seen[size_t(w)][size_t(t)] = 1;
-                            else if (t < 0) untagged[size_t(w)] = 1;
-                            else unknown[size_t(w)] = 1;
-                            slots[size_t(k)] = block->param_index[row + x];
+        std::vector<char> untagged(size_t(nw), 0), unknown(size_t(nw), 0), changed(size_t(nw), 0);
+        {
+            std::vector<std::thread> th;
+            for (int w = 0; w < nw; ++w) {
+                th.emplace_back([&, w] {
+                    for (int64_t z = 1 + nz * w / nw; z < 1 + nz * (w + 1) / nw; ++z)
+                        for (int64_t y = 1; y <= ny; ++y) {
+                            const int64_t row = (z * ext[1] + y) * ext[0];
+                            const int64_t k0 = ((z - 1) * ny + (y - 1)) * nx;
+                            for (int64_t x = 1; x <= nx; ++x) {
+                                const int32_t t = block->tag[row + x];
+                                if (t >= 0 && t < ntags) seen[size_t(w)][size_t(t)] = 1;
+                                else if (t < 0) untagged[size_t(w)] = 1;
+                                else unknown[size_t(w)] = 1;
+                            }
+                            if (have_ctx && !changed[size_t(w)] &&
+                                std::memcmp(ctx.slots.data() + k0, block->param_index + row + 1,
+                                            size_t(nx) * sizeof(int32_t)) != 0)
+                                changed[size_t(w)] = 1;
                         }
-                    }
-            });
+                });
+            }
+            for (auto& t : th) t.join();
         }
-        for (auto& t : th) t.join();
         std::vector<char> allowed(size_t(ntags), 0);
         for (size_t d = 0; d < n_dispatch; ++d)
             if (dispatch_tags[d] >= 0 && dispatch_tags[d] < ntags) allowed[size_t(dispatch_tags[d])] = 1;
@@ -359,10 +369,7 @@ DLB_API dlb_status dlb_collide_and_stream(const dlb_registry* reg, dlb_block_vie
                 if (seen[size_t(w)][size_t(t)] && !allowed[size_t(t)])
                     throw dlb::DispatchError(reg->reg.chain_for(t));
 
-        std::lock_guard<std::mutex> lock(g_block_mu);
-        const std::vector<int64_t> key = {nx, ny, nz, block->q, block->precision_bits};
-        BlockCtx& ctx = g_blocks[key];
-        if (!ctx.lat || ctx.reg != reg || ctx.instances != reg->reg.num_instances()) {
+        if (!have_ctx) {
             dlb_lattice_desc d{};
             d.dims[0] = nx;
             d.dims[1] = ny;
@@ -377,11 +384,17 @@ DLB_API dlb_status dlb_collide_and_stream(const dlb_registry* reg, dlb_block_vie
             ctx.lat->set_periodic_override(false, false, false);
             ctx.reg = reg;
             ctx.instances = reg->reg.num_instances();
-            ctx.slots.clear();
         }
-        if (ctx.slots != slots) {
-            ctx.lat->set_slots(slots.data());
-            ctx.slots.swap(slots);
+        bool any_change = !have_ctx;
+        for (char c : changed) any_change = any_change || c;
+        if (any_change) {
+            ctx.slots.resize(size_t(nx * ny * nz));
+            for (int64_t z = 1; z <= nz; ++z)
+                for (int64_t y = 1; y <= ny; ++y)
+                    std::memcpy(ctx.slots.data() + ((z - 1) * ny + (y - 1)) * nx,
+                                block->param_index + (z * ext[1] + y) * ext[0] + 1,
+                                size_t(nx) * sizeof(int32_t));
+            ctx.lat->set_slots(ctx.slots.data());
         }
         const size_t bytes = size_t(block->q) * size_t(ext[0] * ext[1] * ext[2]) *
                              size_t(block->precision_bits / 8);
@@ -400,6 +413,44 @@ DLB_API dlb_status dlb_collide_and_stream(const dlb_registry* reg, dlb_block_vie
             ctx.lat->download_block_interior(block->f_in, ext, 0);
             ctx.lat->synchronize();
         }
+    });
+}
+
+// refresh_envelope_periodic<T> (accelerated_lattice.cpp:202-238) on a host
+// block: axis-by-axis, later axes spanning the full extent of earlier ones;
+// parallel over directions.
+DLB_API dlb_status dlb_refresh_envelope_periodic(dlb_block_view* block, const int32_t* periodic) {
+    DLB_REQUIRE(block);
+    DLB_REQUIRE(block->f_in);
+    DLB_REQUIRE(periodic);
+    return guarded([&] {
+        const int64_t e[3] = {block->interior[0] + 2, block->interior[1] + 2, block->interior[2] + 2};
+        const int64_t n[3] = {block->interior[0], block->interior[1], block->interior[2]};
+        const int64_t vol = e[0] * e[1] * e[2];
+        const int s = block->precision_bits / 8;
+        char* base = static_cast<char*>(block->f_in);
+        auto work = [&](int i) {
+            char* f = base + std::size_t(i) * vol * s;
+            auto at = [&](int64_t x, int64_t y, int64_t z) { return f + ((z * e[1] + y) * e[0] + x) * s; };
+            if (periodic[0])  // x: interior y, z
+                for (int64_t z = 1; z <= n[2]; ++z)
+                    for (int64_t y = 1; y <= n[1]; ++y) {
+                        std::memcpy(at(0, y, z), at(n[0], y, z), s);
+                        std::memcpy(at(n[0] + 1, y, z), at(1, y, z), s);
+                    }
+            if (periodic[1])  // y: full x rows, interior z
+                for (int64_t z = 1; z <= n[2]; ++z) {
+                    std::memcpy(at(0, 0, z), at(0, n[1], z), e[0] * s);
+                    std::memcpy(at(0, n[1] + 1, z), at(0, 1, z), e[0] * s);
+                }
+            if (periodic[2]) {  // z: full planes
+                std::memcpy(at(0, 0, 0), at(0, 0, n[2]), e[0] * e[1] * s);
+                std::memcpy(at(0, 0, n[2] + 1), at(0, 0, 1), e[0] * e[1] * s);
+            }
+        };
+        std::vector<std::thread> th;
+        for (int i = 0; i < block->q; ++i) th.emplace_back(work, i);
+        for (auto& t : th) t.join();
     });
 }
 

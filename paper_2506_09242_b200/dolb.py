@@ -37,7 +37,7 @@ __all__ = [
     "make_collision_chain", "make_bounce_back", "make_no_dynamics", "make_moving_bounce_back",
     "make_regularized_velocity", "make_regularized_pressure", "chain_string", "serialize_params",
     "DynamicsRegistry", "DispatchSet", "DispatchError", "ExchangeError", "ConfigError", "DlbError",
-    "DeviceRun", "partition", "collide_and_stream", "D3Q19", "D3Q27",
+    "DeviceRun", "partition", "collide_and_stream", "refresh_envelope_periodic", "D3Q19", "D3Q27",
 ]
 
 
@@ -529,6 +529,20 @@ def collide_and_stream(registry: DynamicsRegistry, f_in: np.ndarray, tag: np.nda
     tags = np.asarray(sorted(dispatch.tags), np.int32)
     check(_capi.lib().dlb_collide_and_stream(registry.handle, C.byref(v),
                                              tags.ctypes.data if tags.size else None, tags.size, 1))
+
+
+def refresh_envelope_periodic(f_in: np.ndarray, periodic=(1, 1, 1), q: int = 19):
+    """refresh_envelope_periodic<T> (accelerated_lattice.cpp:202-238) on a host
+    block (q, ez, ey, ex), done by the C++ runtime with one thread per direction."""
+    assert f_in.flags.c_contiguous and f_in.ndim == 4
+    ez, ey, ex = f_in.shape[1:]
+    v = _capi.BlockView()
+    v.precision_bits = 64 if f_in.dtype == np.float64 else 32
+    v.q = q
+    v.interior[0], v.interior[1], v.interior[2] = ex - 2, ey - 2, ez - 2
+    v.f_in = f_in.ctypes.data
+    per = np.asarray(periodic, np.int32)
+    check(_capi.lib().dlb_refresh_envelope_periodic(C.byref(v), per.ctypes.data))
 
 
 def _descriptor(q):

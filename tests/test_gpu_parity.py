@@ -223,12 +223,26 @@ def test_host_block_collide_and_stream_dropin(oracle):
     tag[1:-1, 1:-1, 1:-1] = reg.tag_of_slot(s)
     pidx = np.where(tag >= 0, s, -1).astype(np.int32)
     for _ in range(3):
-        inner = blk[:, 1:-1, 1:-1, 1:-1]
-        blk[:] = np.pad(inner, ((0, 0), (1, 1), (1, 1), (1, 1)), mode="wrap")  # periodic envelope
+        dlb.refresh_envelope_periodic(blk, (1, 1, 1))
         dlb.collide_and_stream(reg, blk, tag, pidx, dlb.DispatchSet.all_of(reg))
     assert np.array_equal(blk[:, 1:-1, 1:-1, 1:-1].reshape(-1), want)
     with pytest.raises(dlb.DispatchError):
         dlb.collide_and_stream(reg, blk, tag, pidx, dlb.DispatchSet())
+    # the same through page-locked host memory (zero-copy PCIe path)
+    import ctypes as C
+    from paper_2506_09242_b200 import _capi
+    p = C.c_void_p()
+    _capi.check(_capi.lib().dlb_host_alloc(blk.nbytes, C.byref(p)))
+    try:
+        pin = np.ctypeslib.as_array((C.c_uint8 * blk.nbytes).from_address(p.value)).view(np.float64).reshape(blk.shape)
+        pin[:] = 0
+        pin[:, 1:-1, 1:-1, 1:-1] = f.reshape(19, n, n, n)
+        for _ in range(3):
+            dlb.refresh_envelope_periodic(pin, (1, 1, 1))
+            dlb.collide_and_stream(reg, pin, tag, pidx, dlb.DispatchSet.all_of(reg))
+        assert np.array_equal(pin[:, 1:-1, 1:-1, 1:-1].reshape(-1), want)
+    finally:
+        _capi.lib().dlb_host_free(p)
 
 
 def test_mass_conservation_long_run():

@@ -179,3 +179,26 @@ def test_no_cpu_fallback_without_gpu():
     with pytest.raises(dlb.DlbError) as e:
         dlb.DeviceRun((8, 8, 8), (1, 1, 1), reg)
     assert e.value.status == 6
+
+
+def test_refresh_envelope_periodic_matches_wrap():
+    """dlb_refresh_envelope_periodic == refresh_envelope_periodic (host-only)."""
+    rng = np.random.default_rng(3)
+    for dt, per in ((np.float64, (1, 1, 1)), (np.float32, (0, 1, 1)), (np.float64, (1, 0, 0))):
+        inner = rng.standard_normal((19, 5, 6, 7)).astype(dt)
+        blk = np.zeros((19, 7, 8, 9), dt)
+        blk[:, 1:-1, 1:-1, 1:-1] = inner
+        dlb.refresh_envelope_periodic(blk, per)
+        want = np.zeros_like(blk)
+        want[:, 1:-1, 1:-1, 1:-1] = inner
+        # axis sweeps x, y, z with later axes spanning earlier ones (accelerated_lattice.cpp:202-238)
+        if per[0]:
+            want[:, 1:-1, 1:-1, 0] = want[:, 1:-1, 1:-1, -2]
+            want[:, 1:-1, 1:-1, -1] = want[:, 1:-1, 1:-1, 1]
+        if per[1]:
+            want[:, 1:-1, 0, :] = want[:, 1:-1, -2, :]
+            want[:, 1:-1, -1, :] = want[:, 1:-1, 1, :]
+        if per[2]:
+            want[:, 0] = want[:, -2]
+            want[:, -1] = want[:, 1]
+        assert np.array_equal(blk, want)

@@ -29,12 +29,7 @@ ds = dlb.DispatchSet.all_of(reg)
 
 
 def refresh():
-    blk[:, 0, :, :] = blk[:, L, :, :]
-    blk[:, L + 1, :, :] = blk[:, 1, :, :]
-    blk[:, :, 0, :] = blk[:, :, L, :]
-    blk[:, :, L + 1, :] = blk[:, :, 1, :]
-    blk[:, :, :, 0] = blk[:, :, :, L]
-    blk[:, :, :, L + 1] = blk[:, :, :, 1]
+    dlb.refresh_envelope_periodic(blk, (1, 1, 1))
 
 
 def tm(fn, n=3):
