@@ -291,11 +291,10 @@ def main():
     # roofline of the dominant kernel (the fused collide-stream launch(es) of a step)
     my_cells = run.dims[0] * run.dims[1] * sum(p[1] for k, p in enumerate(run.parts) if k in run.ranks)
     peak, peak_kind = measured_peak_hbm()
-    alg_bytes = bpc * my_cells
-    if skip:  # only fluid + bounce-back cells move populations; every cell reads its u8 slot
-        active = extra["fluid_cells"] + extra["bounce_back_cells"]
-        alg_bytes = (bpc - 1) * active + my_cells
+    alg_bytes = run.step_bytes()  # dense: bytes/cell x cells; sparse: listed links only
+    if skip:
         extra["mlups_per_fluid_cell"] = mlups * extra["fluid_cells"] / cells_total
+        extra["algorithmic_bytes_per_step"] = alg_bytes
     achieved = alg_bytes / (ms / args.steps * 1e-3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")

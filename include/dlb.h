@@ -91,9 +91,12 @@ typedef struct dlb_lattice_desc {
     int32_t reserved;
 } dlb_lattice_desc;
 
-/* Masked porous variant: cells whose dynamics is NoDynamics are neither loaded
- * nor stored (their stored state is never consumed by a fluid cell, so every
- * Collide-kind cell stays bit-identical to the reference). */
+/* Sparse porous variant: cells whose dynamics is NoDynamics are neither loaded
+ * nor stored and wall cells move only the links that feed fluid cells (their
+ * other values are never consumed by a fluid cell, so every Collide-kind cell
+ * stays bit-identical to the reference). Single-slab lattices
+ * use per-slot cell lists (one launch per dynamics kind); z-slabs use the
+ * masked dense sweep. */
 #define DLB_FLAG_SKIP_NODYNAMICS 1
 
 DLB_API dlb_status dlb_lattice_create(const dlb_lattice_desc* desc, const dlb_registry* reg,
@@ -126,6 +129,10 @@ DLB_API dlb_status dlb_lattice_steps_done(dlb_lattice* lat, int64_t* steps_out);
  * and kernel launches per step (for bench accounting). */
 DLB_API dlb_status dlb_lattice_traffic(dlb_lattice* lat, int64_t* bytes_per_cell,
                                        int64_t* device_bytes, int32_t* launches_per_step);
+/* Algorithmic HBM bytes one step moves (dense: cells * bytes_per_cell; sparse
+ * porous mode: fluid cells 2*q*s + 8 B list entry, wall cells only the links that
+ * feed fluid cells). */
+DLB_API dlb_status dlb_lattice_step_bytes(dlb_lattice* lat, int64_t* bytes_out);
 /* Time nsteps with CUDA events recorded on the lattice stream (milliseconds). */
 DLB_API dlb_status dlb_lattice_time_steps(dlb_lattice* lat, int64_t nsteps, double* ms_out);
 /* Name of the kernel instantiation selected for the present dynamics. */

@@ -256,6 +256,13 @@ DLB_API dlb_status dlb_lattice_traffic(dlb_lattice* lat, int64_t* bytes_per_cell
     return DLB_OK;
 }
 
+DLB_API dlb_status dlb_lattice_step_bytes(dlb_lattice* lat, int64_t* bytes_out) {
+    DLB_REQUIRE(lat);
+    DLB_REQUIRE(bytes_out);
+    *bytes_out = lat->lat->step_bytes();
+    return DLB_OK;
+}
+
 DLB_API dlb_status dlb_lattice_time_steps(dlb_lattice* lat, int64_t nsteps, double* ms_out) {
     DLB_REQUIRE(lat);
     DLB_REQUIRE(ms_out);

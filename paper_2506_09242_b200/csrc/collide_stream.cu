@@ -187,6 +187,62 @@ __global__ void __launch_bounds__(256, 2) k_aa(const __grid_constant__ StepArgs<
     }
 }
 
+// Sparse, kind-sorted list variant for porous media.
+// The host groups the cells that move populations by registry slot (so every
+// launch runs one dynamics kind with a minimal instantiation and no per-cell
+// dispatch), in row-major order. NoDynamics cells are not listed. Bounce-back
+// cells (MASKED) carry the set of links whose source is a fluid cell: only
+// those are loaded and, after the swap, stored — every other link of a wall
+// cell only ever feeds solid cells, so Collide-kind cells stay
+// bit-identical to the dense reference sweep.
+// Entry: x | y << 13 | z << 26 | link mask (links 1..q-1) << 38.
+template <typename T, int Q, unsigned KM, bool MASKED>
+__global__ void __launch_bounds__(256, 2)
+    k_list(const __grid_constant__ StepArgs<T> a, const unsigned long long* __restrict__ list,
+           long long n, int slot) {
+    using L = Lat<Q>;
+    const Geo& g = a.g;
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    unsigned long long next = idx < n ? __ldg(list + idx) : 0ull;
+    for (; idx < n; idx += stride) {
+        const unsigned long long e = next;
+        if (idx + stride < n) next = __ldg(list + idx + stride);  // prefetch the next entry
+        const int x = int(e & 0x1fffull);
+        const int y = int((e >> 13) & 0x1fffull);
+        const int z = int((e >> 26) & 0xfffull);
+        const unsigned mask = unsigned(e >> 38);
+        const int xm = (x == 0 && g.per_x) ? g.nx - 1 : x - 1;
+        const int xp = (x == g.nx - 1 && g.per_x) ? 0 : x + 1;
+        const int ym = (y == 0 && g.per_y) ? g.ny - 1 : y - 1;
+        const int yp = (y == g.ny - 1 && g.per_y) ? 0 : y + 1;
+        const int zm = (z == 0 && g.per_z) ? g.nz - 1 : z - 1;
+        const int zp = (z == g.nz - 1 && g.per_z) ? 0 : z + 1;
+        T f[Q];
+        sfor<Q>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            constexpr int cx = L::c[i][0], cy = L::c[i][1], cz = L::c[i][2];
+            const int sx = cx > 0 ? xm : (cx < 0 ? xp : x);
+            const int sy = cy > 0 ? ym : (cy < 0 ? yp : y);
+            const int sz = cz > 0 ? zm : (cz < 0 ? zp : z);
+            bool use = true;
+            if constexpr (MASKED) use = i != 0 && ((mask >> (i - 1)) & 1u);
+            f[i] = use ? __ldg(a.fin[i] + (sz * g.plane + sy * g.pitch + sx)) : T(0);
+        });
+        Cell<T, Q>::template apply<KM>(f, a.rec[slot]);
+        const int center = z * g.plane + y * g.pitch + x;
+        sfor<Q>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            bool use = true;
+            if constexpr (MASKED) {
+                constexpr int o = opp_of(i);
+                use = o != 0 && ((mask >> (o - 1)) & 1u);
+            }
+            if (use) a.fout[i][center] = f[i];
+        });
+    }
+}
+
 #define DLB_STR2(x) #x
 #define DLB_STR(x) DLB_STR2(x)
 #define ENTRY(T, Q, KM)                                                                  \
@@ -208,6 +264,19 @@ __global__ void __launch_bounds__(256, 2) k_aa(const __grid_constant__ StepArgs<
         AA_PAIR(T, 19, KM_TRT | KM_BB | KM_MBB), AA_PAIR(T, 19, KM_ALL), AA_PAIR(T, 27, KM_RR), \
         AA_PAIR(T, 27, KM_ALL)
 
+#define LIST_ENTRY(T, Q, KM, M)                                                          \
+    KernelEntry {                                                                        \
+        int(sizeof(T) * 8), Q, unsigned(KM), M ? LAYOUT_LIST_MASKED : LAYOUT_LIST,          \
+            reinterpret_cast<const void*>(&k_list<T, Q, unsigned(KM), M>),                \
+            "k_list<" #T ",D3Q" #Q "," #KM "," #M ">[" DLB_STR(DLB_MODE) "]"                  \
+    }
+#define LIST_SET(T, Q)                                                                    \
+    LIST_ENTRY(T, Q, KM_BGK, false), LIST_ENTRY(T, Q, KM_TRT, false), LIST_ENTRY(T, Q, KM_RR, false), \
+        LIST_ENTRY(T, Q, KM_BGK | KM_REGV | KM_REGP, false),                              \
+        LIST_ENTRY(T, Q, KM_TRT | KM_REGV | KM_REGP, false),                              \
+        LIST_ENTRY(T, Q, KM_RR | KM_REGV | KM_REGP, false), LIST_ENTRY(T, Q, KM_ALL, false), \
+        LIST_ENTRY(T, Q, KM_BB, true), LIST_ENTRY(T, Q, KM_MBB, true)
+
 #define Q19_SET(T)                                                                        \
     ENTRY(T, 19, KM_BGK), ENTRY(T, 19, KM_TRT), ENTRY(T, 19, KM_RR),                      \
         ENTRY(T, 19, KM_BGK | KM_BB | KM_MBB), ENTRY(T, 19, KM_TRT | KM_BB | KM_MBB),    \
@@ -224,6 +293,7 @@ __global__ void __launch_bounds__(256, 2) k_aa(const __grid_constant__ StepArgs<
 
 static const KernelEntry kTable[] = {
     Q19_SET(float), Q19_SET(double), Q27_SET(float), Q27_SET(double), AA_SET(float), AA_SET(double),
+    LIST_SET(float, 19), LIST_SET(double, 19), LIST_SET(float, 27), LIST_SET(double, 27),
 };
 
 const KernelEntry* kernel_table(int* n) {

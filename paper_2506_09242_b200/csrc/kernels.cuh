@@ -57,7 +57,8 @@ struct StepArgs {
     DevRecipe<T> rec[kMaxSlots];
 };
 
-enum Layout : int { LAYOUT_TWO_POP = 0, LAYOUT_AA = 1, LAYOUT_AA_ODD = 2 };  // AA: even / odd kernel
+// kernel families: dense two-population, AA even / odd, sparse lists (fluid / masked walls)
+enum Layout : int { LAYOUT_TWO_POP = 0, LAYOUT_AA = 1, LAYOUT_AA_ODD = 2, LAYOUT_LIST = 3, LAYOUT_LIST_MASKED = 4 };
 
 using StepKernelF = void (*)(StepArgs<float>);
 using StepKernelD = void (*)(StepArgs<double>);

@@ -8,6 +8,7 @@
 #include <cstring>
 #include <numeric>
 #include <random>
+#include <thread>
 
 namespace dlb {
 
@@ -294,6 +295,7 @@ Lattice::~Lattice() {
     cudaFree(buf_[0]);
     if (buf_[1] != buf_[0]) cudaFree(buf_[1]);
     cudaFree(d_slot_);
+    cudaFree(d_list_);
     cudaFree(d_flags_);
     cudaFree(d_counter_);
     cudaFree(staging_);
@@ -314,7 +316,13 @@ int64_t Lattice::bytes_per_cell() const {
     return int64_t(2) * d_.q * (d_.precision_bits / 8) + (d_slot_ ? 1 : 0);
 }
 
+int64_t Lattice::step_bytes() const {
+    if (sparse_) return step_bytes_;
+    return bytes_per_cell() * cells();
+}
+
 int Lattice::launches_per_step() const {
+    if (sparse_) return int(lists_.size());
     const bool linked = lower_.linked || upper_.linked;
     if (!linked) return 1;
     return 1 + 1 + (geo_.nz > 2 ? 1 : 0);  // wait + boundary + interior
@@ -352,6 +360,14 @@ void Lattice::set_slots(const int32_t* slots) {
         if (seen[s]) present_slots_.push_back(int32_t(s));
     cudaFree(d_slot_);
     d_slot_ = nullptr;
+    sparse_ = (d_.flags & DLB_FLAG_SKIP_NODYNAMICS) && !split() && !aa() && !(uniform && first >= 0) &&
+              !untagged_ && geo_.nx <= 8192 && geo_.ny <= 8192 && geo_.nz <= 4096;
+    if (sparse_) {
+        uniform_slot_ = 0;
+        slots_set_ = true;
+        build_lists(u8);
+        return;
+    }
     if (uniform && first >= 0) {
         uniform_slot_ = first;
     } else {
@@ -362,6 +378,90 @@ void Lattice::set_slots(const int32_t* slots) {
     }
     slots_set_ = true;
     select_kernel();
+}
+
+// Sparse porous lists (see k_list): cells grouped by slot in row-major order,
+// NoDynamics dropped, wall cells tagged with their fluid-source links.
+void Lattice::build_lists(const std::vector<uint8_t>& u8) {
+    const int nx = geo_.nx, ny = geo_.ny, nz = geo_.nz, q = d_.q;
+    const int nslots = int(chains_.size());
+    std::vector<int> kind(static_cast<std::size_t>(nslots), 0);
+    for (int s = 0; s < nslots; ++s) {
+        const LinkType t = chains_[size_t(s)].links.back().type;
+        kind[size_t(s)] = t == LinkType::NoDynamics ? KIND_NODYN
+                        : t == LinkType::BounceBack ? KIND_BB
+                        : t == LinkType::MovingBounceBack ? KIND_MBB : KIND_COLLIDE;
+    }
+    const int* cx = q == 19 ? kCx19 : kCx27;
+    const int* cy = q == 19 ? kCy19 : kCy27;
+    const int* cz = q == 19 ? kCz19 : kCz27;
+    auto fluid = [&](int x, int y, int z) {
+        if (x < 0 || x >= nx) { if (!geo_.per_x) return false; x = (x + nx) % nx; }
+        if (y < 0 || y >= ny) { if (!geo_.per_y) return false; y = (y + ny) % ny; }
+        if (z < 0 || z >= nz) { if (!geo_.per_z) return false; z = (z + nz) % nz; }
+        return kind[u8[size_t((long long)(z * ny + y) * nx + x)]] == KIND_COLLIDE;
+    };
+    const int nw = std::max(1, std::min<int>(nz, int(std::thread::hardware_concurrency())));
+    std::vector<std::vector<std::vector<unsigned long long>>> part(static_cast<std::size_t>(nw));
+    for (auto& p : part) p.resize(static_cast<std::size_t>(nslots));
+    std::vector<std::vector<int64_t>> bytes(static_cast<std::size_t>(nw), std::vector<int64_t>(1, 0));
+    const int s = d_.precision_bits / 8;
+    std::vector<std::thread> th;
+    for (int w = 0; w < nw; ++w) {
+        th.emplace_back([&, w] {
+            for (int z = nz * w / nw; z < nz * (w + 1) / nw; ++z)
+                for (int y = 0; y < ny; ++y)
+                    for (int x = 0; x < nx; ++x) {
+                        const int sl = u8[size_t((long long)(z * ny + y) * nx + x)];
+                        const int k = kind[size_t(sl)];
+                        if (k == KIND_NODYN) continue;
+                        unsigned long long mask = 0;
+                        if (k == KIND_BB || k == KIND_MBB) {
+                            for (int i = 1; i < q; ++i)
+                                if (fluid(x - cx[i], y - cy[i], z - cz[i])) mask |= 1ull << (i - 1);
+                            if (!mask) continue;  // feeds no fluid cell
+                            bytes[size_t(w)][0] += 2LL * __builtin_popcountll(mask) * s + 8;
+                        } else {
+                            bytes[size_t(w)][0] += 2LL * q * s + 8;
+                        }
+                        part[size_t(w)][size_t(sl)].push_back(
+                            (unsigned long long)x | ((unsigned long long)y << 13) |
+                            ((unsigned long long)z << 26) | (mask << 38));
+                    }
+        });
+    }
+    for (auto& t : th) t.join();
+    std::vector<unsigned long long> all;
+    lists_.clear();
+    step_bytes_ = 0;
+    for (int w = 0; w < nw; ++w) step_bytes_ += bytes[size_t(w)][0];
+    present_slots_.clear();
+    for (int sl = 0; sl < nslots; ++sl) {
+        const long long off = (long long)all.size();
+        for (int w = 0; w < nw; ++w)
+            all.insert(all.end(), part[size_t(w)][size_t(sl)].begin(), part[size_t(w)][size_t(sl)].end());
+        const long long cnt = (long long)all.size() - off;
+        bool present = cnt > 0;
+        if (!present) {  // still present for the dispatch check when any cell has it
+            for (std::size_t c = 0; c < u8.size() && !present; ++c) present = u8[c] == sl;
+        }
+        if (present) present_slots_.push_back(sl);
+        if (cnt == 0) continue;
+        const int k = kind[size_t(sl)];
+        const unsigned km = kind_bits(chains_[size_t(sl)]);
+        const int layout = (k == KIND_BB || k == KIND_MBB) ? LAYOUT_LIST_MASKED : LAYOUT_LIST;
+        const KernelEntry* e = find_kernel(d_.arith, d_.precision_bits, q, km, layout);
+        if (!e) throw std::invalid_argument("no list kernel instantiation covers slot " + std::to_string(sl));
+        lists_.push_back({sl, off, cnt, e});
+    }
+    std::sort(lists_.begin(), lists_.end(),
+              [](const ListLaunch& a, const ListLaunch& b) { return a.count > b.count; });
+    cudaFree(d_list_);
+    d_list_ = nullptr;
+    cuda_check(cudaMalloc(&d_list_, std::max<std::size_t>(1, all.size()) * 8), "cudaMalloc lists");
+    cuda_check(cudaMemcpy(d_list_, all.data(), all.size() * 8, cudaMemcpyHostToDevice), "upload lists");
+    kernel_ = lists_.empty() ? nullptr : lists_.front().kernel;
+    if (!kernel_) kernel_ = find_kernel(d_.arith, d_.precision_bits, q, KM_BB, LAYOUT_LIST_MASKED);
 }
 
 void Lattice::set_uniform_slot(int32_t slot) {
@@ -377,6 +477,7 @@ void Lattice::set_uniform_slot(int32_t slot) {
 }
 
 void Lattice::select_kernel() {
+    if (sparse_) return;
     km_needed_ = 0;
     for (int32_t s : present_slots_) km_needed_ |= kind_bits(chains_[std::size_t(s)]);
     if ((d_.flags & DLB_FLAG_SKIP_NODYNAMICS) && (km_needed_ & KM_NODYN) && !aa()) km_needed_ |= KM_SKIP;
@@ -695,6 +796,18 @@ void Lattice::launch_step(int parity) {
     const void* fn = kernel_->fn;
 
     const bool linked = lower_.linked || upper_.linked;
+    if (sparse_) {
+        for (const ListLaunch& l : lists_) {
+            const unsigned long long* lp = d_list_ + l.offset;
+            long long n = l.count;
+            int slot = l.slot;
+            void* args[] = {&a, &lp, &n, &slot};
+            const long long blocks = std::min<long long>((n + 255) / 256, 148LL * 8);
+            cuda_check(cudaLaunchKernel(l.kernel->fn, dim3(unsigned(blocks)), dim3(256), args, 0, stream_),
+                       "launch list");
+        }
+        return;
+    }
     if (aa()) {
         a.z_begin = 0;
         a.z_step = 1;

@@ -73,6 +73,7 @@ class Lattice {
     cudaStream_t stream() const { return stream_; }
     int64_t steps_done() const { return steps_; }
     int64_t bytes_per_cell() const;
+    int64_t step_bytes() const;
     int64_t device_bytes() const { return device_bytes_; }
     int launches_per_step() const;
     const char* kernel_name() const { return kernel_ ? kernel_->name : "<none>"; }
@@ -126,6 +127,18 @@ class Lattice {
     int64_t device_bytes_ = 0;
     void* staging_ = nullptr;
     std::size_t staging_bytes_ = 0;
+    // sparse porous mode (DLB_FLAG_SKIP_NODYNAMICS on a single slab): per-slot
+    // row-major lists of the cells that move populations, one launch each
+    struct ListLaunch {
+        int slot;
+        long long offset, count;
+        const KernelEntry* kernel;
+    };
+    bool sparse_ = false;
+    std::vector<ListLaunch> lists_;
+    unsigned long long* d_list_ = nullptr;
+    int64_t step_bytes_ = 0;  // algorithmic bytes per step
+    void build_lists(const std::vector<uint8_t>& u8);
     // host-block (zero-copy) path
     void* blk_out_ = nullptr;
     std::size_t blk_out_bytes_ = 0;

@@ -478,6 +478,15 @@ class DeviceRun:
         check(_capi.lib().dlb_lattice_traffic(self.slabs[k].handle, C.byref(b), C.byref(d), C.byref(l)))
         return b.value, d.value, l.value
 
+    def step_bytes(self) -> int:
+        """Algorithmic HBM bytes per step summed over this process's slabs."""
+        tot = 0
+        for s in self.slabs:
+            b = C.c_int64()
+            check(_capi.lib().dlb_lattice_step_bytes(s.handle, C.byref(b)))
+            tot += b.value
+        return tot
+
     def num_cells(self) -> int:
         return self.dims[0] * self.dims[1] * self.dims[2]
 

@@ -319,5 +319,19 @@ def test_skip_nodynamics_fluid_cells_bit_identical(oracle, name):
     want = oracle.run_case(make_case(spec), np.float64, steps).reshape(19, -1)
     fl = fluid_mask(spec)
     assert np.array_equal(got[:, fl], want[:, fl])
-    if "sphere" in name:
-        assert "4|" in run.kernel_name() or "SKIP" in run.kernel_name()
+    assert "k_list" in run.kernel_name()  # single slab -> kind-sorted sparse lists
+    assert run.step_bytes() < 304 * run.num_cells()
+
+
+def test_skip_nodynamics_zslabs_masked_dense(oracle):
+    """With z-slabs the masked dense sweep (KM_SKIP) is used instead of lists."""
+    from golden_cases import make_case
+    spec = CASES["sphere48_trt_f64_c4"]
+    setup, bits, steps = product_setup(spec)
+    run = dlb.build_run(setup, precision=bits, skip_nodynamics=True, slabs=3)
+    run.advance(60)
+    got = run.gather_populations().reshape(19, -1)
+    want = oracle.run_case(make_case(spec), np.float64, 60).reshape(19, -1)
+    fl = fluid_mask(spec)
+    assert np.array_equal(got[:, fl], want[:, fl])
+    assert "SKIP" in run.kernel_name()
