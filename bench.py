@@ -222,7 +222,8 @@ def main():
     ap.add_argument("--arith", default="exact", choices=["exact", "fast"])
     ap.add_argument("--layout", default="twopop", choices=["twopop", "aa"])
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--dense", action="store_true", help="c4: sweep NoDynamics cells too (reference behaviour)")
+    ap.add_argument("--sparse", action="store_true",
+                    help="c4: kind-sorted sparse lists (NoDynamics skipped) instead of the dense sweep")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
 
@@ -255,10 +256,11 @@ def main():
         vox, phi = dlb.sphere_pack((L, L, L), radius=8.0, porosity=0.20, seed=20250611)
         setup = dlb.init_porous(cfg, solid=(vox == 255))
         kinds = np.bincount(np.asarray(setup.chain_index).reshape(-1), minlength=5)
-        skip = not args.dense
+        skip = args.sparse
         extra = {"porosity": phi, "fluid_cells": int(kinds[0] + kinds[3] + kinds[4]),
                  "bounce_back_cells": int(kinds[1]), "no_dynamics_cells": int(kinds[2]),
-                 "variant": "dense sweep" if args.dense else "masked (NoDynamics skipped)"}
+                 "variant": "sparse kind-sorted lists" if args.sparse else
+                 "dense sweep (regularized planes recomputed by list launches)"}
         del vox
     else:
         cfg = dlb.CaseConfig(kind=kind, L=L, Re=Re, Ma=Ma, collision=lt, q=q)

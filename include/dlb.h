@@ -120,6 +120,11 @@ DLB_API dlb_status dlb_lattice_upload_populations(dlb_lattice* lat, const double
 DLB_API dlb_status dlb_lattice_download_populations(dlb_lattice* lat, double* canon);
 /* Same, in the storage precision (float for 32-bit lattices). */
 DLB_API dlb_status dlb_lattice_download_raw(dlb_lattice* lat, void* canon);
+/* Exact, order-independent checksum of the canonical state (q values): for each
+ * direction i, sum over cells of bits(double(f_i) + 0.0) * (global cell index + 1)
+ * modulo 2^64. Independent of layout and decomposition (slab sums add up), so
+ * full-size runs can be compared with the reference without moving the state. */
+DLB_API dlb_status dlb_lattice_checksum(dlb_lattice* lat, uint64_t* per_direction);
 /* Advance nsteps (asynchronous on the lattice stream; includes the halo exchange). */
 DLB_API dlb_status dlb_lattice_step(dlb_lattice* lat, int64_t nsteps);
 DLB_API dlb_status dlb_lattice_synchronize(dlb_lattice* lat);

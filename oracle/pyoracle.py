@@ -401,6 +401,8 @@ class Reference:
             lib.ref_derive_omega_minus.restype = C.c_double
             lib.ref_derive_omega_minus.argtypes = [C.c_double, C.c_double]
             lib.ref_chain_roundtrip.argtypes = [C.c_char_p, C.c_char_p, C.c_size_t]
+            lib.ref_case_checksum.argtypes = [C.POINTER(RefCase), C.c_int, C.c_void_p, C.c_int,
+                                              C.c_int64, C.c_void_p]
             Reference._lib = lib
         self.lib = Reference._lib
 
@@ -430,6 +432,14 @@ class Reference:
         rc = case.ref_struct()
         self._check(self.lib.ref_case_run(C.byref(rc), precision_bits, _ptr(g), workers, nsteps, _ptr(out)))
         return out
+
+    def checksum(self, case: Case, precision_bits: int, nsteps: int, grid=(1, 1, 1), workers=1):
+        out = np.zeros(19, np.uint64)
+        g = np.asarray(grid, np.int32)
+        rc = case.ref_struct()
+        self._check(self.lib.ref_case_checksum(C.byref(rc), precision_bits, _ptr(g), workers, nsteps,
+                                               _ptr(out)))
+        return [int(v) for v in out]
 
     def bench(self, case: Case, precision_bits: int, workers: int, warmup: int, steps: int, reps: int = 3):
         reps_out = np.zeros(reps)
@@ -467,3 +477,14 @@ def canonical_hash(pops: np.ndarray) -> str:
     import hashlib
     a = np.ascontiguousarray(pops, dtype=np.float64) + 0.0
     return hashlib.sha256(a.tobytes()).hexdigest()
+
+
+def canonical_checksum(pops: np.ndarray, q: int = 19) -> list:
+    """Per-direction sum of bits(f + 0.0) * (cell index + 1) mod 2^64 — the
+    dlb_lattice_checksum definition, from a canonical population array."""
+    a = (np.ascontiguousarray(pops, dtype=np.float64) + 0.0).reshape(q, -1)
+    n = a.shape[1]
+    w = np.arange(1, n + 1, dtype=np.uint64)
+    bits = a.view(np.uint64)
+    with np.errstate(over="ignore"):
+        return [int(np.sum(bits[i] * w, dtype=np.uint64)) for i in range(q)]

@@ -111,6 +111,26 @@ void run_case(const RefCase& rc, const int grid[3], int workers, int64_t steps, 
 }
 
 template <typename T>
+void checksum_case(const RefCase& rc, const int grid[3], int workers, int64_t steps, uint64_t* out) {
+    const dolb::CaseSetup setup = make_setup(rc);
+    auto registry = std::make_shared<dolb::DynamicsRegistry>();
+    auto run = dolb::build_run<T>(setup, {grid[0], grid[1], grid[2]}, workers, registry);
+    run.advance(steps);
+    const std::vector<double> pops = run.gather_populations();
+    const std::size_t n = pops.size() / 19;
+    for (int i = 0; i < 19; ++i) {
+        uint64_t acc = 0;
+        for (std::size_t c = 0; c < n; ++c) {
+            const double v = pops[i * n + c] + 0.0;
+            uint64_t bits;
+            std::memcpy(&bits, &v, 8);
+            acc += bits * uint64_t(c + 1);
+        }
+        out[i] = acc;
+    }
+}
+
+template <typename T>
 void bench_case(const RefCase& rc, int workers, int64_t warmup, int64_t steps, int reps,
                 double* rep_mlups, double* mean) {
     const dolb::CaseSetup setup = make_setup(rc);
@@ -180,6 +200,16 @@ __attribute__((visibility("default"))) int ref_case_run(const RefCase* rc, int p
         if (precision_bits == 64) run_case<double>(*rc, grid, workers, steps, out);
         else if (precision_bits == 32) run_case<float>(*rc, grid, workers, steps, out);
         else throw std::invalid_argument("precision must be 32 or 64");
+    });
+}
+
+// dlb_lattice_checksum of the reference's state after `steps` steps.
+__attribute__((visibility("default"))) int ref_case_checksum(const RefCase* rc, int precision_bits,
+                                                             const int* grid, int workers,
+                                                             int64_t steps, uint64_t* out) {
+    return guarded([&] {
+        if (precision_bits == 64) checksum_case<double>(*rc, grid, workers, steps, out);
+        else checksum_case<float>(*rc, grid, workers, steps, out);
     });
 }
 

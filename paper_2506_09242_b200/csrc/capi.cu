@@ -256,6 +256,15 @@ DLB_API dlb_status dlb_lattice_traffic(dlb_lattice* lat, int64_t* bytes_per_cell
     return DLB_OK;
 }
 
+DLB_API dlb_status dlb_lattice_checksum(dlb_lattice* lat, uint64_t* per_direction) {
+    DLB_REQUIRE(lat);
+    DLB_REQUIRE(per_direction);
+    return guarded([&] {
+        lat->lat->synchronize();
+        lat->lat->checksum(reinterpret_cast<unsigned long long*>(per_direction));
+    });
+}
+
 DLB_API dlb_status dlb_lattice_step_bytes(dlb_lattice* lat, int64_t* bytes_out) {
     DLB_REQUIRE(lat);
     DLB_REQUIRE(bytes_out);

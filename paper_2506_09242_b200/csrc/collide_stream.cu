@@ -21,8 +21,20 @@
 namespace dlb {
 namespace DLB_MODE {
 
+// Occupancy target per instantiation (register cap = 65536 / (256 * blocks)):
+// lean dispatch sets (BGK / TRT / walls): fp32 6 blocks (<= 42 regs), D3Q19
+// fp64 3 (<= 85); sets with RR, LES or regularized links, and D3Q27 fp64, get 2
+// (fp32 3) so their larger live state does not spill.
 template <typename T, int Q, unsigned KM>
-__global__ void __launch_bounds__(256, 2) k_pull(const __grid_constant__ StepArgs<T> a) {
+constexpr int min_blocks() {
+    constexpr bool heavy = (KM & (KM_RR | KM_LES | KM_REGV | KM_REGP)) != 0;
+    if (sizeof(T) == 4) return (heavy || Q == 27) ? 3 : 6;
+    if (Q == 27) return 2;
+    return heavy ? 2 : 3;
+}
+
+template <typename T, int Q, unsigned KM>
+__global__ void __launch_bounds__(256, (min_blocks<T, Q, KM>())) k_pull(const __grid_constant__ StepArgs<T> a) {
     using L = Lat<Q>;
     const Geo& g = a.g;
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
@@ -120,7 +132,7 @@ __global__ void __launch_bounds__(256, 2) k_pull(const __grid_constant__ StepArg
 // across a non-periodic face land in the envelope, where they stay part of the
 // canonical state but are never read.
 template <typename T, int Q, unsigned KM, bool ODD>
-__global__ void __launch_bounds__(256, 2) k_aa(const __grid_constant__ StepArgs<T> a) {
+__global__ void __launch_bounds__(256, (min_blocks<T, Q, KM>())) k_aa(const __grid_constant__ StepArgs<T> a) {
     using L = Lat<Q>;
     const Geo& g = a.g;
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
@@ -197,7 +209,7 @@ __global__ void __launch_bounds__(256, 2) k_aa(const __grid_constant__ StepArgs<
 // bit-identical to the dense reference sweep.
 // Entry: x | y << 13 | z << 26 | link mask (links 1..q-1) << 38.
 template <typename T, int Q, unsigned KM, bool MASKED>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, (min_blocks<T, Q, KM>()))
     k_list(const __grid_constant__ StepArgs<T> a, const unsigned long long* __restrict__ list,
            long long n, int slot) {
     using L = Lat<Q>;
@@ -286,7 +298,9 @@ __global__ void __launch_bounds__(256, 2)
         ENTRY(T, 19, KM_RR | KM_BB | KM_NODYN | KM_REGV | KM_REGP), ENTRY(T, 19, KM_ALL),        \
         ENTRY(T, 19, KM_BGK | KM_BB | KM_NODYN | KM_REGV | KM_REGP | KM_SKIP),                  \
         ENTRY(T, 19, KM_TRT | KM_BB | KM_NODYN | KM_REGV | KM_REGP | KM_SKIP),                  \
-        ENTRY(T, 19, KM_RR | KM_BB | KM_NODYN | KM_REGV | KM_REGP | KM_SKIP), ENTRY(T, 19, KM_ALL | KM_SKIP)
+        ENTRY(T, 19, KM_RR | KM_BB | KM_NODYN | KM_REGV | KM_REGP | KM_SKIP), ENTRY(T, 19, KM_ALL | KM_SKIP), \
+        ENTRY(T, 19, KM_BGK | KM_BB | KM_NODYN), ENTRY(T, 19, KM_TRT | KM_BB | KM_NODYN),             \
+        ENTRY(T, 19, KM_RR | KM_BB | KM_NODYN), ENTRY(T, 19, KM_TRT | KM_BB | KM_NODYN | KM_SKIP)
 
 #define Q27_SET(T) ENTRY(T, 27, KM_BGK), ENTRY(T, 27, KM_TRT), ENTRY(T, 27, KM_RR), ENTRY(T, 27, KM_ALL), \
         ENTRY(T, 27, KM_ALL | KM_SKIP)

@@ -146,6 +146,45 @@ __global__ void k_halo_wait(unsigned long long* flags, int have_lower, int have_
     }
 }
 
+// Order-independent exact checksum of the canonical state: per direction
+// S_i = sum over cells of bits(double(f_i) + 0.0) * (global cell index + 1)
+// (mod 2^64). Integer sums commute, so the result does not depend on the
+// reduction order, the slab decomposition or the layout (two-population / AA
+// even / AA odd), and sums of slab checksums equal the monolithic one.
+template <typename T, int Q>
+__global__ void k_checksum(const T* origin0, Geo g, int aa_mode, long long z_origin, long long gnx,
+                           long long gny, unsigned long long* out) {
+    using L = Lat<Q>;
+    unsigned long long acc[Q];
+    for (int i = 0; i < Q; ++i) acc[i] = 0ull;
+    const long long n = static_cast<long long>(g.nx) * g.ny * g.nz;
+    for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
+         c += (long long)gridDim.x * blockDim.x) {
+        const int x = int(c % g.nx);
+        const int y = int((c / g.nx) % g.ny);
+        const int z = int(c / (static_cast<long long>(g.nx) * g.ny));
+        const unsigned long long w = static_cast<unsigned long long>(((z_origin + z) * gny + y) * gnx + x) + 1ull;
+        sfor<Q>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            constexpr int cx = L::c[i][0], cy = L::c[i][1], cz = L::c[i][2];
+            long long at;
+            int dir = i;
+            if (aa_mode == 2) at = shifted(g, x, y, z, cx, cy, cz);          // AA odd layout
+            else {
+                at = static_cast<long long>(z) * g.plane + static_cast<long long>(y) * g.pitch + x;
+                if (aa_mode == 1) dir = opp_of(i);                              // AA even layout
+            }
+            const double v = double(origin0[dir * g.dstride + at]) + 0.0;
+            acc[i] += static_cast<unsigned long long>(__double_as_longlong(v)) * w;
+        });
+    }
+    for (int i = 0; i < Q; ++i) {
+        unsigned long long v = acc[i];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0) atomicAdd(out + i, v);
+    }
+}
+
 int grid_for(long long n) {
     long long b = (n + 255) / 256;
     return int(std::min<long long>(std::max<long long>(b, 1), 148LL * 32));
@@ -296,6 +335,7 @@ Lattice::~Lattice() {
     if (buf_[1] != buf_[0]) cudaFree(buf_[1]);
     cudaFree(d_slot_);
     cudaFree(d_list_);
+    cudaFree(d_fix_);
     cudaFree(d_flags_);
     cudaFree(d_counter_);
     cudaFree(staging_);
@@ -324,7 +364,7 @@ int64_t Lattice::step_bytes() const {
 int Lattice::launches_per_step() const {
     if (sparse_) return int(lists_.size());
     const bool linked = lower_.linked || upper_.linked;
-    if (!linked) return 1;
+    if (!linked) return 1 + ((kernel_main_ && !fixups_.empty()) ? int(fixups_.size()) : 0);
     return 1 + 1 + (geo_.nz > 2 ? 1 : 0);  // wait + boundary + interior
 }
 
@@ -368,6 +408,7 @@ void Lattice::set_slots(const int32_t* slots) {
         build_lists(u8);
         return;
     }
+    build_fixups(u8);
     if (uniform && first >= 0) {
         uniform_slot_ = first;
     } else {
@@ -464,6 +505,44 @@ void Lattice::build_lists(const std::vector<uint8_t>& u8) {
     if (!kernel_) kernel_ = find_kernel(d_.arith, d_.precision_bits, q, KM_BB, LAYOUT_LIST_MASKED);
 }
 
+void Lattice::build_fixups(const std::vector<uint8_t>& u8) {
+    fixups_.clear();
+    cudaFree(d_fix_);
+    d_fix_ = nullptr;
+    if (aa()) return;
+    std::vector<char> reg(chains_.size(), 0);
+    bool any = false;
+    for (std::size_t s = 0; s < chains_.size(); ++s)
+        for (const ChainLink& l : chains_[s].links)
+            if (l.type == LinkType::RegularizedVelocity || l.type == LinkType::RegularizedPressure)
+                reg[s] = 1, any = true;
+    if (!any) return;
+    std::vector<std::vector<unsigned long long>> per(chains_.size());
+    for (int z = 0; z < geo_.nz; ++z)
+        for (int y = 0; y < geo_.ny; ++y)
+            for (int x = 0; x < geo_.nx; ++x) {
+                const int sl = u8[std::size_t((long long)(z * geo_.ny + y) * geo_.nx + x)];
+                if (reg[std::size_t(sl)])
+                    per[std::size_t(sl)].push_back((unsigned long long)x | ((unsigned long long)y << 13) |
+                                                   ((unsigned long long)z << 26));
+            }
+    std::vector<unsigned long long> all;
+    for (std::size_t sl = 0; sl < per.size(); ++sl) {
+        if (per[sl].empty()) continue;
+        const KernelEntry* e =
+            find_kernel(d_.arith, d_.precision_bits, d_.q, kind_bits(chains_[sl]), LAYOUT_LIST);
+        if (!e) return;  // no list instantiation: keep the full dense kernel
+        fixups_.push_back({int(sl), (long long)all.size(), (long long)per[sl].size(), e});
+        all.insert(all.end(), per[sl].begin(), per[sl].end());
+    }
+    if (all.empty() || geo_.nx > 8192 || geo_.ny > 8192 || geo_.nz > 4096) {
+        fixups_.clear();
+        return;
+    }
+    cuda_check(cudaMalloc(&d_fix_, all.size() * 8), "cudaMalloc fixups");
+    cuda_check(cudaMemcpy(d_fix_, all.data(), all.size() * 8, cudaMemcpyHostToDevice), "upload fixups");
+}
+
 void Lattice::set_uniform_slot(int32_t slot) {
     if (slot < 0 || slot >= int32_t(chains_.size()))
         throw std::invalid_argument("slot " + std::to_string(slot) + " is not registered");
@@ -491,6 +570,10 @@ void Lattice::select_kernel() {
     }
     kernel_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_, LAYOUT_TWO_POP);
     if (!kernel_) throw std::invalid_argument("no kernel instantiation covers this dynamics set");
+    kernel_main_ = nullptr;
+    if (!fixups_.empty())
+        kernel_main_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_ & ~(KM_REGV | KM_REGP),
+                                   LAYOUT_TWO_POP);
 }
 
 void Lattice::set_dispatch(const int32_t* tags, std::size_t n) {
@@ -821,7 +904,22 @@ void Lattice::launch_step(int parity) {
         a.z_begin = 0;
         a.z_step = 1;
         void* args[] = {&a};
-        cuda_check(cudaLaunchKernel(fn, dim3(gx, gy, geo_.nz), block, args, 0, stream_), "launch");
+        const bool split_rare = kernel_main_ != nullptr && !fixups_.empty();
+        cuda_check(cudaLaunchKernel(split_rare ? kernel_main_->fn : fn, dim3(gx, gy, geo_.nz), block, args, 0,
+                                    stream_), "launch");
+        if (split_rare) {
+            // the main sweep treated the regularized cells as plain bulk cells;
+            // recompute them (same f_in, later in stream order) with the full chain
+            for (const ListLaunch& l : fixups_) {
+                const unsigned long long* lp = d_fix_ + l.offset;
+                long long n = l.count;
+                int slot = l.slot;
+                void* largs[] = {&a, &lp, &n, &slot};
+                const long long blocks = std::min<long long>((n + 255) / 256, 148LL * 8);
+                cuda_check(cudaLaunchKernel(l.kernel->fn, dim3(unsigned(blocks)), dim3(256), largs, 0, stream_),
+                           "launch fixup");
+            }
+        }
         return;
     }
     // 1. wait until both neighbours completed the boundary planes of the previous step
@@ -900,6 +998,27 @@ void Lattice::exchange() {
                                        plane_bytes, cudaMemcpyDefault, stream_), "halo exchange");
     }
     cuda_check(cudaStreamSynchronize(stream_), "halo exchange");
+}
+
+void Lattice::checksum(unsigned long long* per_dir) {
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    cuda_check(cudaStreamSynchronize(stream_), "sync");
+    unsigned long long* d = static_cast<unsigned long long*>(staging_);
+    cuda_check(cudaMemsetAsync(d, 0, 27 * 8, stream_), "memset");
+    const int mode = !aa() ? 0 : (aa_odd_layout_ ? 2 : 1);
+    const int grid = grid_for(cells());
+    const void* o = origin(cur_);
+    const long long gnx = geo_.nx, gny = geo_.ny;
+    if (d_.precision_bits == 64) {
+        if (d_.q == 19) k_checksum<double, 19><<<grid, 256, 0, stream_>>>((const double*)o, geo_, mode, d_.z_origin, gnx, gny, d);
+        else k_checksum<double, 27><<<grid, 256, 0, stream_>>>((const double*)o, geo_, mode, d_.z_origin, gnx, gny, d);
+    } else {
+        if (d_.q == 19) k_checksum<float, 19><<<grid, 256, 0, stream_>>>((const float*)o, geo_, mode, d_.z_origin, gnx, gny, d);
+        else k_checksum<float, 27><<<grid, 256, 0, stream_>>>((const float*)o, geo_, mode, d_.z_origin, gnx, gny, d);
+    }
+    cuda_check(cudaGetLastError(), "k_checksum");
+    cuda_check(cudaMemcpyAsync(per_dir, d, size_t(d_.q) * 8, cudaMemcpyDeviceToHost, stream_), "d2h");
+    cuda_check(cudaStreamSynchronize(stream_), "checksum");
 }
 
 void Lattice::check_error_flag() {

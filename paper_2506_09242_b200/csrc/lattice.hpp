@@ -63,6 +63,7 @@ class Lattice {
     void enqueue_step();  // one step, no dispatch check (group stepping)
     void check_dispatch() const;
     void synchronize();
+    void checksum(unsigned long long* per_dir);  // q order-independent 64-bit sums
     double time_steps(int64_t nsteps);
 
     void link_lower(Lattice& lower);  // same process
@@ -76,7 +77,10 @@ class Lattice {
     int64_t step_bytes() const;
     int64_t device_bytes() const { return device_bytes_; }
     int launches_per_step() const;
-    const char* kernel_name() const { return kernel_ ? kernel_->name : "<none>"; }
+    const char* kernel_name() const {
+        if (kernel_main_ && !fixups_.empty() && !(lower_.linked || upper_.linked)) return kernel_main_->name;
+        return kernel_ ? kernel_->name : "<none>";
+    }
     int64_t cells() const { return int64_t(d_.dims[0]) * d_.dims[1] * d_.dims[2]; }
     int bits() const { return d_.precision_bits; }
     int q() const { return d_.q; }
@@ -135,6 +139,13 @@ class Lattice {
         const KernelEntry* kernel;
     };
     bool sparse_ = false;
+    // rare-kind split (two-population, unlinked): the dense sweep runs without
+    // the regularized boundary code (fewer registers, higher occupancy) and
+    // list launches recompute the regularized cells afterwards
+    std::vector<ListLaunch> fixups_;
+    unsigned long long* d_fix_ = nullptr;
+    const KernelEntry* kernel_main_ = nullptr;
+    void build_fixups(const std::vector<uint8_t>& u8);
     std::vector<ListLaunch> lists_;
     unsigned long long* d_list_ = nullptr;
     int64_t step_bytes_ = 0;  // algorithmic bytes per step

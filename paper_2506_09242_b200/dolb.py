@@ -478,6 +478,16 @@ class DeviceRun:
         check(_capi.lib().dlb_lattice_traffic(self.slabs[k].handle, C.byref(b), C.byref(d), C.byref(l)))
         return b.value, d.value, l.value
 
+    def checksum(self) -> list:
+        """Per-direction exact checksums of this process's cells (sum of slab
+        checksums mod 2^64; equal to the reference's for identical states)."""
+        tot = np.zeros(self.q, np.uint64)
+        for s in self.slabs:
+            buf = np.zeros(self.q, np.uint64)
+            check(_capi.lib().dlb_lattice_checksum(s.handle, buf.ctypes.data))
+            tot = tot + buf  # uint64 wraps
+        return [int(v) for v in tot]
+
     def step_bytes(self) -> int:
         """Algorithmic HBM bytes per step summed over this process's slabs."""
         tot = 0

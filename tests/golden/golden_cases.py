@@ -56,3 +56,15 @@ def make_case(spec) -> Case:
     if s.get("geometry") == "sphere48":
         s["geometry"] = SPHERE_RAW
     return Case(**s)
+
+
+# Full-size BASELINE configs the reference can run in the build container
+# (62 GB RAM): checksums only (tests/golden/golden_full.json).
+FULL_CASES = {
+    # config 3 per-GPU size: lid-driven cavity D3Q19 TRT 512^3 fp32
+    "cavity512_trt_f32_c3_full": dict(kind="cavity", L=512, Re=1000.0, Ma=0.1, collision=TRT, bits=32,
+                                      steps=6, workers=8),
+    # config 1 (also hashed in golden.json)
+    "cavity64_bgk_f64_c1_full": dict(kind="cavity", L=64, Re=1000.0, Ma=0.1, collision=BGK, bits=64,
+                                     steps=1000, workers=8),
+}

@@ -23,11 +23,32 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
 sys.path.insert(0, HERE)
-from pyoracle import Reference, canonical_hash  # noqa: E402
-from golden_cases import CASES, make_case  # noqa: E402
+from pyoracle import Reference, canonical_checksum, canonical_hash  # noqa: E402
+from golden_cases import CASES, FULL_CASES, make_case  # noqa: E402
+
+
+def full():
+    """Full-size configs: only the order-independent checksum is recorded
+    (dlb_lattice_checksum definition), the state is too large to hash in Python."""
+    ref = Reference()
+    path = os.path.join(HERE, "golden_full.json")
+    out = json.load(open(path)) if os.path.exists(path) else {}
+    for name, spec in FULL_CASES.items():
+        if name in out:
+            continue
+        case = make_case(spec)
+        t = time.time()
+        cs = ref.checksum(case, spec["bits"], spec["steps"], grid=(1, 1, spec.get("workers", 8)),
+                          workers=spec.get("workers", 8))
+        out[name] = {"spec": spec, "checksum": [str(v) for v in cs]}
+        print(f"{name}: {time.time() - t:.1f}s", flush=True)
+        with open(path, "w") as f:
+            json.dump(out, f, indent=1)
 
 
 def main():
+    if "--full" in sys.argv:
+        return full()
     ref = Reference()
     out = {}
     for name, spec in CASES.items():
