@@ -238,6 +238,8 @@ def main():
 
     rank, world = env_int("RANK", 0), env_int("WORLD_SIZE", 1)
     local = env_int("LOCAL_RANK", 0)
+    if os.environ.get("DLB_SAME_DEVICE") == "1":  # protocol test: all ranks share GPU 0
+        local = 0
     if world > 1:
         tdist.init_process_group("gloo")
     torch.cuda.set_device(local)

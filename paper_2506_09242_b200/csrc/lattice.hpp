@@ -150,6 +150,11 @@ class Lattice {
     unsigned long long* d_list_ = nullptr;
     int64_t step_bytes_ = 0;  // algorithmic bytes per step
     void build_lists(const std::vector<uint8_t>& u8);
+    // CUDA graph of two consecutive steps (parity 0 -> 1 -> 0), replayed by
+    // step() / time_steps(); invalidated whenever kernels, slots or links change
+    cudaGraphExec_t graph_ = nullptr;
+    void invalidate_graph();
+    void ensure_graph();
     // host-block (zero-copy) path
     void* blk_out_ = nullptr;
     std::size_t blk_out_bytes_ = 0;

@@ -374,3 +374,18 @@ def test_full_size_config5_layout_and_decomposition_invariance():
         sums.append(run.checksum())
         del run
     assert sums[0] == sums[1] == sums[2]
+
+
+@pytest.mark.parametrize("layout", ["twopop", "aa"])
+def test_graph_replay_any_parity(oracle, layout):
+    """Steps replay as a captured 2-step CUDA graph; odd chunk sizes and
+    restarts at either parity must not change the trajectory."""
+    case = Case(kind="cavity", L=20, Re=200.0, Ma=0.1, collision=TRT)
+    dims, per, rec, slot = case.setup()
+    f = oracle.initial_state(case, np.float64)
+    setup, _, _ = product_setup(dict(kind="cavity", L=20, Re=200.0, Ma=0.1, collision=TRT, bits=64, steps=0))
+    run = dlb.build_run(setup, precision=64, layout=layout)
+    for chunk in (1, 9, 4, 1, 1, 17, 6):
+        run.advance(chunk)
+        oracle.step(19, dims, per, rec, slot, f, chunk)
+        assert np.array_equal(run.gather_populations(), f), chunk
