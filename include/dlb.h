@@ -120,6 +120,12 @@ DLB_API dlb_status dlb_lattice_upload_populations(dlb_lattice* lat, const double
 DLB_API dlb_status dlb_lattice_download_populations(dlb_lattice* lat, double* canon);
 /* Same, in the storage precision (float for 32-bit lattices). */
 DLB_API dlb_status dlb_lattice_download_raw(dlb_lattice* lat, void* canon);
+/* MultiBlockRun::gather_macroscopic (multiblock.cpp:443-484) for this slab:
+ * per cell (x fastest) rho and u in double; Collide cells compute_rho_u of the
+ * populations converted to double, moving walls rho = 1 and their wall velocity,
+ * other cells rho = 1, u = 0. */
+DLB_API dlb_status dlb_lattice_gather_macroscopic(dlb_lattice* lat, double* rho, double* ux,
+                                                  double* uy, double* uz);
 /* Exact, order-independent checksum of the canonical state (q values): for each
  * direction i, sum over cells of bits(double(f_i) + 0.0) * (global cell index + 1)
  * modulo 2^64. Independent of layout and decomposition (slab sums add up), so

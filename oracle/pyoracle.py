@@ -401,6 +401,8 @@ class Reference:
             lib.ref_derive_omega_minus.restype = C.c_double
             lib.ref_derive_omega_minus.argtypes = [C.c_double, C.c_double]
             lib.ref_chain_roundtrip.argtypes = [C.c_char_p, C.c_char_p, C.c_size_t]
+            lib.ref_case_macro.argtypes = [C.POINTER(RefCase), C.c_int, C.c_int64] + [C.c_void_p] * 4
+            lib.ref_case_dump.argtypes = [C.POINTER(RefCase), C.c_int, C.c_int64, C.c_char_p]
             lib.ref_case_checksum.argtypes = [C.POINTER(RefCase), C.c_int, C.c_void_p, C.c_int,
                                               C.c_int64, C.c_void_p]
             Reference._lib = lib
@@ -432,6 +434,18 @@ class Reference:
         rc = case.ref_struct()
         self._check(self.lib.ref_case_run(C.byref(rc), precision_bits, _ptr(g), workers, nsteps, _ptr(out)))
         return out
+
+    def macroscopic(self, case: Case, precision_bits: int, nsteps: int):
+        d = self.dims(case)
+        n = d[0] * d[1] * d[2]
+        arrs = [np.zeros(n) for _ in range(4)]
+        rc = case.ref_struct()
+        self._check(self.lib.ref_case_macro(C.byref(rc), precision_bits, nsteps, *[_ptr(a) for a in arrs]))
+        return tuple(arrs)
+
+    def dump(self, case: Case, precision_bits: int, nsteps: int, path: str):
+        rc = case.ref_struct()
+        self._check(self.lib.ref_case_dump(C.byref(rc), precision_bits, nsteps, path.encode()))
 
     def checksum(self, case: Case, precision_bits: int, nsteps: int, grid=(1, 1, 1), workers=1):
         out = np.zeros(19, np.uint64)

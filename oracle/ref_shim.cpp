@@ -131,6 +131,29 @@ void checksum_case(const RefCase& rc, const int grid[3], int workers, int64_t st
 }
 
 template <typename T>
+void macro_case(const RefCase& rc, int64_t steps, double* rho, double* ux, double* uy, double* uz) {
+    const dolb::CaseSetup setup = make_setup(rc);
+    auto registry = std::make_shared<dolb::DynamicsRegistry>();
+    auto run = dolb::build_run<T>(setup, {1, 1, 2}, 2, registry);
+    run.advance(steps);
+    std::vector<double> r, x, y, z;
+    run.gather_macroscopic(r, x, y, z);
+    std::memcpy(rho, r.data(), r.size() * 8);
+    std::memcpy(ux, x.data(), x.size() * 8);
+    std::memcpy(uy, y.data(), y.size() * 8);
+    std::memcpy(uz, z.data(), z.size() * 8);
+}
+
+template <typename T>
+void dump_case(const RefCase& rc, int64_t steps, const char* path) {
+    const dolb::CaseSetup setup = make_setup(rc);
+    auto registry = std::make_shared<dolb::DynamicsRegistry>();
+    auto run = dolb::build_run<T>(setup, {1, 1, 2}, 2, registry);
+    run.advance(steps);
+    dolb::write_field_dump(path, run.gather_block());
+}
+
+template <typename T>
 void bench_case(const RefCase& rc, int workers, int64_t warmup, int64_t steps, int reps,
                 double* rep_mlups, double* mean) {
     const dolb::CaseSetup setup = make_setup(rc);
@@ -210,6 +233,23 @@ __attribute__((visibility("default"))) int ref_case_checksum(const RefCase* rc, 
     return guarded([&] {
         if (precision_bits == 64) checksum_case<double>(*rc, grid, workers, steps, out);
         else checksum_case<float>(*rc, grid, workers, steps, out);
+    });
+}
+
+__attribute__((visibility("default"))) int ref_case_macro(const RefCase* rc, int precision_bits,
+                                                          int64_t steps, double* rho, double* ux,
+                                                          double* uy, double* uz) {
+    return guarded([&] {
+        if (precision_bits == 64) macro_case<double>(*rc, steps, rho, ux, uy, uz);
+        else macro_case<float>(*rc, steps, rho, ux, uy, uz);
+    });
+}
+
+__attribute__((visibility("default"))) int ref_case_dump(const RefCase* rc, int precision_bits,
+                                                         int64_t steps, const char* path) {
+    return guarded([&] {
+        if (precision_bits == 64) dump_case<double>(*rc, steps, path);
+        else dump_case<float>(*rc, steps, path);
     });
 }
 

@@ -92,6 +92,7 @@ _SIGS = {
     "dlb_lattice_stream": ([C.c_void_p, C.POINTER(C.c_void_p)], C.c_int),
     "dlb_lattice_steps_done": ([C.c_void_p, C.POINTER(C.c_int64)], C.c_int),
     "dlb_lattice_traffic": ([C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int32)], C.c_int),
+    "dlb_lattice_gather_macroscopic": ([C.c_void_p] * 5, C.c_int),
     "dlb_lattice_checksum": ([C.c_void_p, C.c_void_p], C.c_int),
     "dlb_lattice_step_bytes": ([C.c_void_p, C.POINTER(C.c_int64)], C.c_int),
     "dlb_lattice_time_steps": ([C.c_void_p, C.c_int64, C.POINTER(C.c_double)], C.c_int),

@@ -256,6 +256,13 @@ DLB_API dlb_status dlb_lattice_traffic(dlb_lattice* lat, int64_t* bytes_per_cell
     return DLB_OK;
 }
 
+DLB_API dlb_status dlb_lattice_gather_macroscopic(dlb_lattice* lat, double* rho, double* ux,
+                                                  double* uy, double* uz) {
+    DLB_REQUIRE(lat);
+    DLB_REQUIRE(rho && ux && uy && uz);
+    return guarded([&] { lat->lat->gather_macroscopic(rho, ux, uy, uz); });
+}
+
 DLB_API dlb_status dlb_lattice_checksum(dlb_lattice* lat, uint64_t* per_direction) {
     DLB_REQUIRE(lat);
     DLB_REQUIRE(per_direction);

@@ -185,6 +185,56 @@ __global__ void k_checksum(const T* origin0, Geo g, int aa_mode, long long z_ori
     }
 }
 
+// Canonical f_i(x, y, z) of the current state for any layout
+// (aa_mode: 0 two-population, 1 AA even layout, 2 AA odd layout).
+template <typename T, int Q, int i>
+__device__ __forceinline__ T canon_load(const T* origin0, const Geo& g, int x, int y, int z, int aa_mode) {
+    using L = Lat<Q>;
+    constexpr int cx = L::c[i][0], cy = L::c[i][1], cz = L::c[i][2];
+    if (aa_mode == 2) return origin0[i * g.dstride + shifted(g, x, y, z, cx, cy, cz)];
+    const long long at = static_cast<long long>(z) * g.plane + static_cast<long long>(y) * g.pitch + x;
+    return origin0[(aa_mode == 1 ? opp_of(i) : i) * g.dstride + at];
+}
+
+struct MacroSlot {
+    int kind;
+    double uw[3];
+};
+
+// MultiBlockRun::gather_macroscopic (multiblock.cpp:443-484): populations
+// converted to double; Collide cells report compute_rho_u, moving walls their
+// (T-cast) wall velocity with rho = 1, other cells rho = 1, u = 0.
+template <typename T, int Q>
+__global__ void k_macro(const T* origin0, Geo g, int aa_mode, const uint8_t* slot, int uniform_slot,
+                        const MacroSlot* ms, int z0, int nzc, double* rho, double* ux, double* uy,
+                        double* uz) {
+    const long long n = static_cast<long long>(g.nx) * g.ny * nzc;
+    for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
+         c += (long long)gridDim.x * blockDim.x) {
+        const int x = int(c % g.nx);
+        const int y = int((c / g.nx) % g.ny);
+        const int z = z0 + int(c / (static_cast<long long>(g.nx) * g.ny));
+        const int s = slot ? slot[(static_cast<long long>(z) * g.ny + y) * g.nx + x] : uniform_slot;
+        double r = 1.0, u[3] = {0.0, 0.0, 0.0};
+        if (ms[s].kind == KIND_COLLIDE) {
+            double f[Q];
+            sfor<Q>([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                f[i] = double(canon_load<T, Q, i>(origin0, g, x, y, z, aa_mode));
+            });
+            Cell<double, Q>::rho_u(f, r, u);
+        } else if (ms[s].kind == KIND_MBB) {
+            u[0] = ms[s].uw[0];
+            u[1] = ms[s].uw[1];
+            u[2] = ms[s].uw[2];
+        }
+        rho[c] = r;
+        ux[c] = u[0];
+        uy[c] = u[1];
+        uz[c] = u[2];
+    }
+}
+
 int grid_for(long long n) {
     long long b = (n + 255) / 256;
     return int(std::min<long long>(std::max<long long>(b, 1), 148LL * 32));
@@ -1061,6 +1111,51 @@ void Lattice::checksum(unsigned long long* per_dir) {
     cuda_check(cudaGetLastError(), "k_checksum");
     cuda_check(cudaMemcpyAsync(per_dir, d, size_t(d_.q) * 8, cudaMemcpyDeviceToHost, stream_), "d2h");
     cuda_check(cudaStreamSynchronize(stream_), "checksum");
+}
+
+void Lattice::gather_macroscopic(double* rho, double* ux, double* uy, double* uz) {
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    cuda_check(cudaStreamSynchronize(stream_), "sync");
+    if (sparse_) throw std::invalid_argument("gather_macroscopic: not available in the sparse porous mode");
+    std::vector<MacroSlot> ms(std::max<std::size_t>(chains_.size(), 1));
+    for (std::size_t s = 0; s < chains_.size(); ++s) {
+        const LinkType t = chains_[s].links.back().type;
+        ms[s].kind = t == LinkType::MovingBounceBack ? KIND_MBB
+                   : (t == LinkType::BGK || t == LinkType::TRT || t == LinkType::RR) ? KIND_COLLIDE
+                                                                                      : KIND_BB;
+        for (int a = 0; a < 3; ++a) {
+            const double w = chains_[s].params.wall_velocity[a];
+            ms[s].uw[a] = d_.precision_bits == 64 ? w : double(float(w));  // T-cast, as the recipe holds it
+        }
+    }
+    const std::size_t ms_bytes = ms.size() * sizeof(MacroSlot);
+    char* st = static_cast<char*>(staging_);
+    cuda_check(cudaMemcpyAsync(st, ms.data(), ms_bytes, cudaMemcpyHostToDevice, stream_), "h2d");
+    const long long plane_cells = (long long)geo_.nx * geo_.ny;
+    const std::size_t room = staging_bytes_ - 4096;
+    const int zc = int(std::max<long long>(1, (long long)(room / 32) / plane_cells));
+    double* out = reinterpret_cast<double*>(st + 4096);
+    const int mode = !aa() ? 0 : (aa_odd_layout_ ? 2 : 1);
+    for (int z0 = 0; z0 < geo_.nz; z0 += zc) {
+        const int nzc = std::min(zc, geo_.nz - z0);
+        const long long n = plane_cells * nzc;
+        const int grid = grid_for(n);
+        const void* o = origin(cur_);
+        const MacroSlot* dms = reinterpret_cast<const MacroSlot*>(st);
+        if (d_.precision_bits == 64) {
+            if (d_.q == 19) k_macro<double, 19><<<grid, 256, 0, stream_>>>((const double*)o, geo_, mode, d_slot_, uniform_slot_, dms, z0, nzc, out, out + n, out + 2 * n, out + 3 * n);
+            else k_macro<double, 27><<<grid, 256, 0, stream_>>>((const double*)o, geo_, mode, d_slot_, uniform_slot_, dms, z0, nzc, out, out + n, out + 2 * n, out + 3 * n);
+        } else {
+            if (d_.q == 19) k_macro<float, 19><<<grid, 256, 0, stream_>>>((const float*)o, geo_, mode, d_slot_, uniform_slot_, dms, z0, nzc, out, out + n, out + 2 * n, out + 3 * n);
+            else k_macro<float, 27><<<grid, 256, 0, stream_>>>((const float*)o, geo_, mode, d_slot_, uniform_slot_, dms, z0, nzc, out, out + n, out + 2 * n, out + 3 * n);
+        }
+        cuda_check(cudaGetLastError(), "k_macro");
+        const long long off = plane_cells * z0;
+        double* dst[4] = {rho, ux, uy, uz};
+        for (int k = 0; k < 4; ++k)
+            cuda_check(cudaMemcpyAsync(dst[k] + off, out + k * n, n * 8, cudaMemcpyDeviceToHost, stream_), "d2h");
+        cuda_check(cudaStreamSynchronize(stream_), "gather_macroscopic");
+    }
 }
 
 void Lattice::check_error_flag() {

@@ -63,7 +63,8 @@ class Lattice {
     void enqueue_step();  // one step, no dispatch check (group stepping)
     void check_dispatch() const;
     void synchronize();
-    void checksum(unsigned long long* per_dir);  // q order-independent 64-bit sums
+    void checksum(unsigned long long* per_dir);
+    void gather_macroscopic(double* rho, double* ux, double* uy, double* uz);  // q order-independent 64-bit sums
     double time_steps(int64_t nsteps);
 
     void link_lower(Lattice& lower);  // same process

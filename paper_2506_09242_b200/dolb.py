@@ -37,7 +37,7 @@ __all__ = [
     "make_collision_chain", "make_bounce_back", "make_no_dynamics", "make_moving_bounce_back",
     "make_regularized_velocity", "make_regularized_pressure", "chain_string", "serialize_params",
     "DynamicsRegistry", "DispatchSet", "DispatchError", "ExchangeError", "ConfigError", "DlbError",
-    "DeviceRun", "partition", "collide_and_stream", "refresh_envelope_periodic", "D3Q19", "D3Q27",
+    "DeviceRun", "partition", "collide_and_stream", "refresh_envelope_periodic", "read_field_dump", "D3Q19", "D3Q27",
 ]
 
 
@@ -514,6 +514,28 @@ class DeviceRun:
             out[:, (z0 - z_lo) * nxy:(z0 - z_lo + nz) * nxy] = buf.reshape(self.q, -1)
         return out.reshape(-1)
 
+    def gather_macroscopic(self):
+        """rho, ux, uy, uz over this process's cells (multiblock.cpp:443-484)."""
+        nxy = self.dims[0] * self.dims[1]
+        outs = []
+        for k, s in enumerate(self.slabs):
+            _, nz = self._slab_range(k)
+            arrs = [np.zeros(nz * nxy) for _ in range(4)]
+            check(_capi.lib().dlb_lattice_gather_macroscopic(s.handle, *[a.ctypes.data for a in arrs]))
+            outs.append(arrs)
+        return tuple(np.concatenate([o[j] for o in outs]) for j in range(4))
+
+    def write_field_dump(self, path: str):
+        """DOLB1 field dump of the whole (single-process) domain in the storage
+        precision: magic, u8 precision, u32 q, 3 x u64 dims, then the q SoA
+        arrays x fastest (accelerated_lattice.cpp:313-341)."""
+        import struct
+        raw = self.gather_raw()
+        with open(path, "wb") as fh:
+            fh.write(b"DOLB1")
+            fh.write(struct.pack("<BI3Q", self.precision // 8, self.q, *self.dims))
+            fh.write(raw.tobytes())
+
     def gather_raw(self) -> np.ndarray:
         """Like gather_populations but in the storage precision."""
         dt = np.float64 if self.precision == 64 else np.float32
@@ -548,6 +570,24 @@ def collide_and_stream(registry: DynamicsRegistry, f_in: np.ndarray, tag: np.nda
     tags = np.asarray(sorted(dispatch.tags), np.int32)
     check(_capi.lib().dlb_collide_and_stream(registry.handle, C.byref(v),
                                              tags.ctypes.data if tags.size else None, tags.size, 1))
+
+
+def read_field_dump(path: str):
+    """read_field_dump (accelerated_lattice.cpp:343-374): (dims, precision_bytes,
+    q x N doubles)."""
+    import struct
+    with open(path, "rb") as fh:
+        if fh.read(5) != b"DOLB1":
+            raise OSError(f'"{path}" is not a DOLB1 field dump')
+        prec, q, nx, ny, nz = struct.unpack("<BI3Q", fh.read(29))
+        if prec not in (4, 8):
+            raise OSError(f'unsupported field dump header in "{path}"')
+        dt = np.float64 if prec == 8 else np.float32
+        n = q * nx * ny * nz
+        data = np.frombuffer(fh.read(n * prec), dtype=dt)
+        if data.size != n:
+            raise OSError(f'truncated field dump "{path}"')
+    return (nx, ny, nz), prec, data.astype(np.float64)
 
 
 def refresh_envelope_periodic(f_in: np.ndarray, periodic=(1, 1, 1), q: int = 19):
