@@ -427,7 +427,7 @@ DLB_API dlb_status dlb_collide_and_stream(const dlb_registry* reg, dlb_block_vie
                             attr.type == cudaMemoryTypeHost && attr.devicePointer == block->f_in;
         cudaGetLastError();
         if (pinned) {
-            // zero-copy: PCIe pulls + overlapped copy-back (Lattice::step_host_block)
+            // pinned: 3-stage H2D / compute / D2H pipeline (Lattice::step_host_block)
             ctx.lat->step_host_block(block->f_in, ext);
         } else {
             // pageable memory: staged copies through device memory

@@ -393,6 +393,7 @@ Lattice::~Lattice() {
     cudaFree(blk_out_);
     for (cudaEvent_t e : blk_ev_) cudaEventDestroy(e);
     if (copy_stream_) cudaStreamDestroy(copy_stream_);
+    if (h2d_stream_) cudaStreamDestroy(h2d_stream_);
     if (ev0_) cudaEventDestroy(ev0_);
     if (ev1_) cudaEventDestroy(ev1_);
     if (stream_) cudaStreamDestroy(stream_);
@@ -839,6 +840,12 @@ void Lattice::fill_recipes(StepArgs<T>& a) const {
     for (std::size_t s = 0; s < chains_.size(); ++s) a.rec[s] = compile_recipe<T>(chains_[s]);
 }
 
+// Three-stage pipeline over z-chunks of a pinned host block (host layout kept
+// on the device, so every transfer is one contiguous range per direction):
+//   copy engine 1: host planes needed by chunk k -> device input mirror
+//   SMs:           collide-and-stream of chunk k (input mirror -> output mirror)
+//   copy engine 2: finished planes of chunk k - 1 -> back into the host f_in
+// The two PCIe directions run concurrently with the compute.
 template <typename T>
 void Lattice::launch_host_block(void* f_in, const int64_t ext[3]) {
     const long long vol = ext[0] * ext[1] * ext[2];
@@ -851,55 +858,66 @@ void Lattice::launch_host_block(void* f_in, const int64_t ext[3]) {
     hg.dstride = vol;
     hg.per_x = hg.per_y = hg.per_z = 0;  // the caller's envelope is authoritative
     const std::size_t bytes = std::size_t(d_.q) * vol * sizeof(T);
-    if (blk_out_bytes_ < bytes) {
+    if (blk_out_bytes_ < 2 * bytes) {
         cudaFree(blk_out_);
         blk_out_ = nullptr;
-        cuda_check(cudaMalloc(&blk_out_, bytes), "cudaMalloc block mirror");
-        blk_out_bytes_ = bytes;
+        cuda_check(cudaMalloc(&blk_out_, 2 * bytes), "cudaMalloc block mirrors");
+        blk_out_bytes_ = 2 * bytes;
     }
+    T* din = static_cast<T*>(blk_out_);
+    T* dout = din + std::size_t(d_.q) * vol;
     if (!copy_stream_) cuda_check(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking), "stream");
+    if (!h2d_stream_) cuda_check(cudaStreamCreateWithFlags(&h2d_stream_, cudaStreamNonBlocking), "stream");
     StepArgs<T> a{};
     fill_recipes(a);
     a.g = hg;
     const long long org = hg.plane + hg.pitch + 1;
     for (int i = 0; i < d_.q; ++i) {
-        a.fin[i] = static_cast<const T*>(f_in) + i * vol + org;
-        a.fout[i] = static_cast<T*>(blk_out_) + i * vol + org;
+        a.fin[i] = din + i * vol + org;
+        a.fout[i] = dout + i * vol + org;
     }
     const int bx = hg.nx >= 128 ? 128 : (hg.nx > 32 ? 64 : 32);
     const int by = 256 / bx;
     const dim3 block(bx, by, 1);
     const unsigned gx = unsigned((hg.nx + bx - 1) / bx), gy = unsigned((hg.ny + by - 1) / by);
-    // ~8 chunks: the copy-back of chunk k overlaps the PCIe pulls of chunk k + 1
-    const int zc = std::max(1, (hg.nz + 7) / 8);
+    const int zc = std::max(1, (hg.nz + 15) / 16);
     const int nchunks = (hg.nz + zc - 1) / zc;
-    while (int(blk_ev_.size()) < nchunks) {
+    while (int(blk_ev_.size()) < 2 * nchunks) {
         cudaEvent_t e;
         cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
         blk_ev_.push_back(e);
     }
     const std::size_t plane_bytes = std::size_t(hg.plane) * sizeof(T);
-    int written = 0;  // interior planes [0, written) already copied back
-    auto copy_back = [&](int upto) {
-        if (upto <= written) return;
+    auto copy_planes = [&](cudaStream_t st, bool up, int p0, int p1) {  // host plane indices [p0, p1)
+        if (p1 <= p0) return;
         for (int i = 0; i < d_.q; ++i) {
-            const std::size_t off = (std::size_t(i) * vol + std::size_t(written + 1) * hg.plane) * sizeof(T);
-            cuda_check(cudaMemcpyAsync(static_cast<char*>(f_in) + off, static_cast<char*>(blk_out_) + off,
-                                       std::size_t(upto - written) * plane_bytes, cudaMemcpyDeviceToHost,
-                                       copy_stream_), "d2h");
+            const std::size_t off = (std::size_t(i) * vol + std::size_t(p0) * hg.plane) * sizeof(T);
+            char* h = static_cast<char*>(f_in) + off;
+            char* d = reinterpret_cast<char*>(up ? din : dout) + off;
+            cuda_check(cudaMemcpyAsync(up ? d : h, up ? h : d, std::size_t(p1 - p0) * plane_bytes,
+                                       up ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, st),
+                       up ? "h2d" : "d2h");
         }
-        written = upto;
     };
+    int loaded = 0;   // host planes [0, loaded) are on the device
+    int written = 1;  // host planes [1, written) copied back (plane 0 is envelope)
     for (int c = 0; c < nchunks; ++c) {
         const int z0 = c * zc, z1 = std::min(hg.nz, z0 + zc);
+        // chunk [z0, z1) reads host planes [z0, z1 + 2)
+        copy_planes(h2d_stream_, true, loaded, z1 + 2);
+        loaded = z1 + 2;
+        cuda_check(cudaEventRecord(blk_ev_[2 * c], h2d_stream_), "event");
+        cuda_check(cudaStreamWaitEvent(stream_, blk_ev_[2 * c], 0), "wait");
         a.z_begin = z0;
         a.z_step = 1;
         void* args[] = {&a};
         cuda_check(cudaLaunchKernel(kernel_->fn, dim3(gx, gy, z1 - z0), block, args, 0, stream_), "launch");
-        cuda_check(cudaEventRecord(blk_ev_[c], stream_), "event");
-        // plane p of the old state is read by planes p-1..p+1: planes < z1 - 1 are free
-        cuda_check(cudaStreamWaitEvent(copy_stream_, blk_ev_[c], 0), "wait");
-        copy_back(z1 == hg.nz ? hg.nz : z1 - 1);
+        cuda_check(cudaEventRecord(blk_ev_[2 * c + 1], stream_), "event");
+        // the old interior planes z < z1 are no longer read once the host
+        // copy of them is on the device, so finished planes can go back
+        cuda_check(cudaStreamWaitEvent(copy_stream_, blk_ev_[2 * c + 1], 0), "wait");
+        copy_planes(copy_stream_, false, written, z1 + 1);
+        written = z1 + 1;
     }
     cuda_check(cudaStreamSynchronize(copy_stream_), "block copy-back");
     cuda_check(cudaStreamSynchronize(stream_), "block step");

@@ -53,11 +53,9 @@ class Lattice {
     void upload_block(const void* f, const int64_t ext[3]);
     void download_block_interior(void* f, const int64_t ext[3], int which);
     // One step of a caller-owned, page-locked AcceleratedBlock (envelope
-    // included, refreshed by the caller): the kernel pulls f_in straight from
-    // host memory across PCIe (mapped pinned memory), writes the new state to
-    // a device mirror, and finished z-chunks are copied back into f_in on a
-    // second stream as soon as no later plane still reads them, so the PCIe
-    // reads and writes overlap.
+    // included, refreshed by the caller), pipelined over z-chunks: host->device
+    // copies of the next chunk, the step of this chunk and device->host copies
+    // of the previous one run concurrently (both PCIe directions busy).
     void step_host_block(void* f_in, const int64_t ext[3]);
     void step(int64_t nsteps);
     void enqueue_step();  // one step, no dispatch check (group stepping)
@@ -160,6 +158,7 @@ class Lattice {
     void* blk_out_ = nullptr;
     std::size_t blk_out_bytes_ = 0;
     cudaStream_t copy_stream_ = nullptr;
+    cudaStream_t h2d_stream_ = nullptr;
     std::vector<cudaEvent_t> blk_ev_;
     template <typename T>
     void fill_recipes(StepArgs<T>& a) const;
