@@ -202,3 +202,54 @@ def test_refresh_envelope_periodic_matches_wrap():
             want[:, 0] = want[:, -2]
             want[:, -1] = want[:, 1]
         assert np.array_equal(blk, want)
+
+
+def test_capi_null_arguments_and_buffer_protocol():
+    """C-ABI conventions of proj/tests/test_capi.cpp:26-33 and :78-96: null
+    arguments -> INVALID_ARGUMENT with a readable last error; string getters
+    report the required size when called with a NULL buffer and refuse short
+    buffers."""
+    import ctypes as C
+    lib = _capi.lib()
+    assert b"." in lib.dlb_version()
+    assert lib.dlb_registry_register(None, b"COLL_BGK", None, 0, None) == 1
+    assert b"null" in lib.dlb_last_error()
+    assert lib.dlb_lattice_step(None, 1) == 1
+    assert lib.dlb_collide_and_stream(None, None, None, 0, 1) == 1
+    n = C.c_size_t()
+    assert lib.dlb_chain_canonical(b"Boundary_RegularizedPressure_2_M1|COLL_RR", None, 0, C.byref(n)) == 0
+    assert n.value == len("Boundary_RegularizedPressure_2_M1__RR") + 1
+    small = C.create_string_buffer(4)
+    assert lib.dlb_chain_canonical(b"COLL_BGK", small, 4, C.byref(n)) == 2
+    assert b"buffer" in lib.dlb_last_error()
+    full = C.create_string_buffer(n.value)
+    assert lib.dlb_chain_canonical(b"COLL_BGK", full, n.value, C.byref(n)) == 0
+    assert full.value == b"COLL_BGK"
+    # a registry miss is a configuration error that names the chain
+    reg = DynamicsRegistry()
+    t = C.c_int32()
+    assert lib.dlb_registry_tag_for(reg.handle, b"COLL_TRT", C.byref(t)) == 2
+    assert b"COLL_TRT" in lib.dlb_last_error()
+    # parameter records are validated against the chain (chain.cpp:188-230)
+    slot = C.c_int32()
+    two = (C.c_double * 2)(1.2, 0.5)
+    assert lib.dlb_registry_register(reg.handle, b"COLL_BGK", two, 2, C.byref(slot)) == 2
+    assert b"too long" in lib.dlb_last_error()
+    assert lib.dlb_registry_register(reg.handle, b"COLL_TRT", two, 1, C.byref(slot)) == 2
+    assert b"too short" in lib.dlb_last_error()
+
+
+def test_last_error_is_thread_local():
+    import threading
+    lib = _capi.lib()
+    lib.dlb_chain_canonical(b"NOT_A_LINK", None, 0, None)
+    seen = {}
+
+    def worker():
+        lib.dlb_chain_canonical(b"COLL_BGK", None, 0, None)
+        seen["msg"] = lib.dlb_last_error()
+    th = threading.Thread(target=worker)
+    th.start()
+    th.join()
+    assert b"NOT_A_LINK" in lib.dlb_last_error()
+    assert b"NOT_A_LINK" not in seen["msg"]
