@@ -221,6 +221,7 @@ def main():
     ap.add_argument("--L", type=int, default=None, help="override the edge length (profiling only)")
     ap.add_argument("--arith", default="exact", choices=["exact", "fast"])
     ap.add_argument("--layout", default="twopop", choices=["twopop", "aa"])
+    ap.add_argument("--no-tma", action="store_true", help="plain-load dense kernel instead of the TMA-staged one")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sparse", action="store_true",
                     help="c4: kind-sorted sparse lists (NoDynamics skipped) instead of the dense sweep")
@@ -245,6 +246,7 @@ def main():
     torch.cuda.set_device(local)
 
     kind, L, Re, Ma, coll, q, bits, scaling, desc = CONFIGS[args.config]
+    kname = None
     if scaling == "weak":
         L = int(round(L * world ** (1.0 / 3.0)))  # perfmodel.cpp:76-85 weak sizes
     if args.L:
@@ -270,7 +272,7 @@ def main():
     layout = args.layout if world == 1 else "twopop"  # AA runs single-slab lattices
     run = dlb.build_run(setup, precision=bits, arith=args.arith,
                         dist=(rank, world) if world > 1 else None, devices=[local], layout=layout,
-                        skip_nodynamics=skip)
+                        skip_nodynamics=skip, tma=not args.no_tma)
     cells_total = run.num_cells()
     bpc, dev_bytes, launches = run.traffic()
 
@@ -338,7 +340,8 @@ def main():
         "config": {"workload": f"{args.config}: {desc}", "L": L, "cells": cells_total,
                    "parallelism": f"z-slab x{world}",
                    "layout": "AA in-place SoA" if layout == "aa" else "two-population SoA",
-                   "arith": args.arith, "l2": "inputs larger than L2 (state resident in HBM)",
+                   "arith": args.arith, "kernel": run.kernel_name(),
+                   "l2": "inputs larger than L2 (state resident in HBM)",
                    "device_bytes_per_gpu": dev_bytes, **extra},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,

@@ -98,6 +98,10 @@ typedef struct dlb_lattice_desc {
  * use per-slot cell lists (one launch per dynamics kind); z-slabs use the
  * masked dense sweep. */
 #define DLB_FLAG_SKIP_NODYNAMICS 1
+/* Use the plain-load dense kernel instead of the TMA-staged one (the TMA path
+ * is the default for dense single-slab two-population lattices; the
+ * environment variable DLB_NO_TMA has the same effect). */
+#define DLB_FLAG_NO_TMA 2
 
 DLB_API dlb_status dlb_lattice_create(const dlb_lattice_desc* desc, const dlb_registry* reg,
                                       dlb_lattice** out);

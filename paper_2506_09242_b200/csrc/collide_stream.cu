@@ -255,6 +255,140 @@ __global__ void __launch_bounds__(256, (min_blocks<T, Q, KM>()))
     }
 }
 
+// ---------------------------------------------------------------------------
+// TMA-staged pull (dense two-population, single slab). A persistent CTA walks
+// tiles of BX x BY cells of one z-plane; per tile, one elected thread issues q
+// 4-D TMA box loads (cp.async.bulk.tensor) — direction i's box is the tile
+// shifted by -c_i, read straight out of the envelope-inclusive layout — into
+// an S-stage shared-memory ring tracked by mbarriers (expect_tx), so S-1 tiles
+// of neighbour data are in flight while the threads collide the current one.
+// Loads need no wrap logic: on periodic axes the envelope holds the periodic
+// images, which the kernel itself keeps current by pushing every boundary
+// cell's outgoing links into the opposite envelope of the output buffer
+// (k_refresh_envelope primes it once after a fill / upload).
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned phase) {
+    unsigned done = 0;
+    do {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(bar), "r"(phase)
+            : "memory");
+    } while (!done);
+}
+
+template <typename T, int Q, int BX, int BY>
+__device__ __forceinline__ void tma_issue_tile(const CUtensorMap* map, T* dst, unsigned bar, int x0, int y0,
+                                               int z, int xoff) {
+    using L = Lat<Q>;
+    constexpr unsigned bytes = unsigned(Q * BX * BY * sizeof(T));
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    sfor<Q>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        constexpr int cx = L::c[i][0], cy = L::c[i][1], cz = L::c[i][2];
+        const int c0 = x0 - cx + xoff, c1 = y0 - cy + 1, c2 = z - cz + 1, c3 = i;
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst + i * BX * BY)),
+            "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+            : "memory");
+    });
+}
+
+template <typename T, int Q, unsigned KM, int BX, int BY, int S>
+__global__ void __launch_bounds__(BX * BY, (sizeof(T) == 4 ? 2 : 1))
+    k_tma(const __grid_constant__ StepArgs<T> a, const __grid_constant__ CUtensorMap tin, int xoff) {
+    using L = Lat<Q>;
+    const Geo& g = a.g;
+    extern __shared__ __align__(128) unsigned char smem[];
+    T* ring = reinterpret_cast<T*>(smem);
+    unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + size_t(S) * Q * BX * BY * sizeof(T));
+    const int tid = threadIdx.x;
+    const int tx = tid % BX, ty = tid / BX;
+    const int tiles_x = (g.nx + BX - 1) / BX, tiles_y = (g.ny + BY - 1) / BY;
+    const int tiles_per_plane = tiles_x * tiles_y;
+    const long long ntiles = static_cast<long long>(tiles_per_plane) * g.nz;
+    auto tile_xyz = [&](long long t, int& x0, int& y0, int& z) {
+        z = int(t / tiles_per_plane);
+        const int r = int(t % tiles_per_plane);
+        y0 = (r / tiles_x) * BY;
+        x0 = (r % tiles_x) * BX;
+    };
+    if (tid == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(&tin)) : "memory");
+        for (int st = 0; st < S; ++st)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bars + st)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int st = 0; st < S; ++st) {
+            const long long t = blockIdx.x + static_cast<long long>(st) * gridDim.x;
+            if (t >= ntiles) break;
+            int x0, y0, z;
+            tile_xyz(t, x0, y0, z);
+            tma_issue_tile<T, Q, BX, BY>(&tin, ring + size_t(st) * Q * BX * BY, smem_u32(bars + st), x0, y0, z, xoff);
+        }
+    }
+    int k = 0;
+    for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+        const int st = k % S;
+        const unsigned phase = unsigned(k / S) & 1u;
+        int x0, y0, z;
+        tile_xyz(t, x0, y0, z);
+        mbar_wait(smem_u32(bars + st), phase);
+        T f[Q];
+        const T* tile = ring + size_t(st) * Q * BX * BY;
+        sfor<Q>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            f[i] = tile[i * BX * BY + tid];
+        });
+        __syncthreads();  // every thread has its values: the stage can be refilled
+        if (tid == 0) {
+            const long long tn = t + static_cast<long long>(S) * gridDim.x;
+            if (tn < ntiles) {
+                int nx0, ny0, nz0;
+                tile_xyz(tn, nx0, ny0, nz0);
+                tma_issue_tile<T, Q, BX, BY>(&tin, ring + size_t(st) * Q * BX * BY, smem_u32(bars + st), nx0,
+                                             ny0, nz0, xoff);
+            }
+        }
+        const int x = x0 + tx, y = y0 + ty;
+        if (x >= g.nx || y >= g.ny) continue;
+        int s = a.uniform_slot;
+        if (a.slot != nullptr) s = a.slot[(static_cast<long long>(z) * g.ny + y) * g.nx + x];
+        Cell<T, Q>::template apply<KM>(f, a.rec[s]);
+        const int center = z * g.plane + y * g.pitch + x;
+        sfor<Q>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            a.fout[i][center] = f[i];
+        });
+        // periodic images of the outgoing links of boundary cells
+        const bool bx_lo = g.per_x && x == 0, bx_hi = g.per_x && x == g.nx - 1;
+        const bool by_lo = g.per_y && y == 0, by_hi = g.per_y && y == g.ny - 1;
+        const bool bz_lo = g.per_z && z == 0, bz_hi = g.per_z && z == g.nz - 1;
+        if (bx_lo || bx_hi || by_lo || by_hi || bz_lo || bz_hi) {
+            sfor<Q>([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                constexpr int cx = L::c[i][0], cy = L::c[i][1], cz = L::c[i][2];
+                int X = x, Y = y, Z = z;
+                bool moved = false;
+                if (cx > 0 && bx_hi) { X = x - g.nx; moved = true; }
+                if (cx < 0 && bx_lo) { X = x + g.nx; moved = true; }
+                if (cy > 0 && by_hi) { Y = y - g.ny; moved = true; }
+                if (cy < 0 && by_lo) { Y = y + g.ny; moved = true; }
+                if (cz > 0 && bz_hi) { Z = z - g.nz; moved = true; }
+                if (cz < 0 && bz_lo) { Z = z + g.nz; moved = true; }
+                if (moved) a.fout[i][Z * g.plane + Y * g.pitch + X] = f[i];
+            });
+        }
+    }
+}
+
 #define DLB_STR2(x) #x
 #define DLB_STR(x) DLB_STR2(x)
 #define ENTRY(T, Q, KM)                                                                  \
@@ -289,6 +423,22 @@ __global__ void __launch_bounds__(256, (min_blocks<T, Q, KM>()))
         LIST_ENTRY(T, Q, KM_RR | KM_REGV | KM_REGP, false), LIST_ENTRY(T, Q, KM_ALL, false), \
         LIST_ENTRY(T, Q, KM_BB, true), LIST_ENTRY(T, Q, KM_MBB, true)
 
+// TMA tiles: 256 threads; f32 64 x 4 cells (4 stages), f64 32 x 8 (3 stages)
+#define TMA_ENTRY(T, Q, KM, BX, BY, S)                                                   \
+    KernelEntry {                                                                        \
+        int(sizeof(T) * 8), Q, unsigned(KM), LAYOUT_TMA,                                  \
+            reinterpret_cast<const void*>(&k_tma<T, Q, unsigned(KM), BX, BY, S>),          \
+            "k_tma<" #T ",D3Q" #Q "," #KM ">[" DLB_STR(DLB_MODE) "]", BX, BY, S               \
+    }
+#define TMA_SET                                                                           \
+    TMA_ENTRY(float, 19, KM_BGK, 64, 4, 4), TMA_ENTRY(float, 19, KM_TRT, 64, 4, 4),       \
+        TMA_ENTRY(float, 19, KM_BGK | KM_BB | KM_MBB, 64, 4, 4),                          \
+        TMA_ENTRY(float, 19, KM_TRT | KM_BB | KM_MBB, 64, 4, 4),                          \
+        TMA_ENTRY(double, 19, KM_BGK, 32, 8, 3), TMA_ENTRY(double, 19, KM_TRT, 32, 8, 3), \
+        TMA_ENTRY(double, 19, KM_BGK | KM_BB | KM_MBB, 32, 8, 3),                         \
+        TMA_ENTRY(double, 19, KM_TRT | KM_BB | KM_MBB, 32, 8, 3),                         \
+        TMA_ENTRY(double, 27, KM_RR, 32, 8, 2)
+
 #define Q19_SET(T)                                                                        \
     ENTRY(T, 19, KM_BGK), ENTRY(T, 19, KM_TRT), ENTRY(T, 19, KM_RR),                      \
         ENTRY(T, 19, KM_BGK | KM_BB | KM_MBB), ENTRY(T, 19, KM_TRT | KM_BB | KM_MBB),    \
@@ -308,6 +458,7 @@ __global__ void __launch_bounds__(256, (min_blocks<T, Q, KM>()))
 static const KernelEntry kTable[] = {
     Q19_SET(float), Q19_SET(double), Q27_SET(float), Q27_SET(double), AA_SET(float), AA_SET(double),
     LIST_SET(float, 19), LIST_SET(double, 19), LIST_SET(float, 27), LIST_SET(double, 27),
+    TMA_SET,
 };
 
 const KernelEntry* kernel_table(int* n) {

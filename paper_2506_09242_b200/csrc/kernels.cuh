@@ -2,6 +2,7 @@
 // kernel translation units (compiled once per arithmetic mode) and the host.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -58,7 +59,8 @@ struct StepArgs {
 };
 
 // kernel families: dense two-population, AA even / odd, sparse lists (fluid / masked walls)
-enum Layout : int { LAYOUT_TWO_POP = 0, LAYOUT_AA = 1, LAYOUT_AA_ODD = 2, LAYOUT_LIST = 3, LAYOUT_LIST_MASKED = 4 };
+enum Layout : int { LAYOUT_TWO_POP = 0, LAYOUT_AA = 1, LAYOUT_AA_ODD = 2, LAYOUT_LIST = 3, LAYOUT_LIST_MASKED = 4,
+                    LAYOUT_TMA = 5 };
 
 using StepKernelF = void (*)(StepArgs<float>);
 using StepKernelD = void (*)(StepArgs<double>);
@@ -70,6 +72,7 @@ struct KernelEntry {
     int layout;
     const void* fn;  // __global__ function pointer
     const char* name;
+    int tile_x = 0, tile_y = 0, stages = 0;  // TMA kernels: tile shape and ring depth
 };
 
 // Kernel tables of the two arithmetic modes (one translation unit each).

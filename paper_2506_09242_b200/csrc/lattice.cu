@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstring>
 #include <numeric>
+#include <cstdlib>
 #include <random>
 #include <thread>
 
@@ -235,6 +236,28 @@ __global__ void k_macro(const T* origin0, Geo g, int aa_mode, const uint8_t* slo
     }
 }
 
+// Device refresh_envelope_periodic (accelerated_lattice.cpp:202-238): every
+// envelope cell whose out-of-range coordinates all lie on periodic axes gets
+// the value of its periodic image (edges and corners included).
+template <typename T>
+__global__ void k_refresh_envelope(T* origin0, Geo g, int q) {
+    const long long ex = g.nx + 2, ey = g.ny + 2, ez = g.nz + 2;
+    const long long n = ex * ey * ez;
+    for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
+         c += (long long)gridDim.x * blockDim.x) {
+        int x = int(c % ex) - 1, y = int((c / ex) % ey) - 1, z = int(c / (ex * ey)) - 1;
+        const bool env = x < 0 || x >= g.nx || y < 0 || y >= g.ny || z < 0 || z >= g.nz;
+        if (!env) continue;
+        int X = x, Y = y, Z = z;
+        if (X < 0 || X >= g.nx) { if (!g.per_x) continue; X = X < 0 ? X + g.nx : X - g.nx; }
+        if (Y < 0 || Y >= g.ny) { if (!g.per_y) continue; Y = Y < 0 ? Y + g.ny : Y - g.ny; }
+        if (Z < 0 || Z >= g.nz) { if (!g.per_z) continue; Z = Z < 0 ? Z + g.nz : Z - g.nz; }
+        const long long dst = static_cast<long long>(z) * g.plane + static_cast<long long>(y) * g.pitch + x;
+        const long long src = static_cast<long long>(Z) * g.plane + static_cast<long long>(Y) * g.pitch + X;
+        for (int i = 0; i < q; ++i) origin0[i * g.dstride + dst] = origin0[i * g.dstride + src];
+    }
+}
+
 int grid_for(long long n) {
     long long b = (n + 255) / 256;
     return int(std::min<long long>(std::max<long long>(b, 1), 148LL * 32));
@@ -373,6 +396,7 @@ Lattice::Lattice(const dlb_lattice_desc& desc, const DynamicsRegistry& reg) : d_
     cuda_check(cudaMemsetAsync(d_counter_, 0, sizeof(unsigned int), stream_), "memset");
     staging_bytes_ = kStagingBytes;
     cuda_check(cudaMalloc(&staging_, staging_bytes_), "cudaMalloc staging");
+    setup_tma();
     cuda_check(cudaStreamSynchronize(stream_), "init");
 }
 
@@ -422,6 +446,7 @@ int Lattice::launches_per_step() const {
 
 void Lattice::set_periodic_override(bool x, bool y, bool z) {
     invalidate_graph();
+    envelope_valid_ = false;
     geo_.per_x = x;
     geo_.per_y = y;
     geo_.per_z = z;
@@ -597,6 +622,75 @@ void Lattice::build_fixups(const std::vector<uint8_t>& u8) {
     cuda_check(cudaMemcpy(d_fix_, all.data(), all.size() * 8, cudaMemcpyHostToDevice), "upload fixups");
 }
 
+// Tensor map of one population buffer as a 4-D tensor (x, y, z, direction).
+// The base sits 16 B before interior x = 0 so that x = -1 .. nx are in range
+// (needs pitch >= nx + 2 + 16 B / s).
+void Lattice::setup_tma() {
+    tma_ok_ = false;
+    if (aa() || std::getenv("DLB_NO_TMA") || (d_.flags & DLB_FLAG_NO_TMA)) return;
+    const int s = d_.precision_bits / 8;
+    const int e = 16 / s;
+    if (geo_.pitch < geo_.nx + 2 + e) return;
+    using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+        cudaGetLastError();
+        return;
+    }
+    const int bx = s == 4 ? 64 : 32, by = 256 / bx;
+    for (int b = 0; b < 2; ++b) {
+        char* base = static_cast<char*>(buf_[b]) + std::size_t(align_ - e) * s;
+        const cuuint64_t dims[4] = {cuuint64_t(geo_.pitch), cuuint64_t(geo_.ny + 2), cuuint64_t(geo_.nz + 2),
+                                    cuuint64_t(d_.q)};
+        const cuuint64_t strides[3] = {cuuint64_t(geo_.pitch) * s, cuuint64_t(geo_.plane) * s,
+                                       cuuint64_t(geo_.dstride) * s};
+        const cuuint32_t box[4] = {cuuint32_t(bx), cuuint32_t(by), 1u, 1u};
+        const cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
+        const CUresult r = reinterpret_cast<EncodeFn>(fn)(
+            &tmap_[b], s == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, base, dims,
+            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return;
+    }
+    tma_xoff_ = e;
+    tma_ok_ = true;
+}
+
+void Lattice::refresh_envelope(int which) {
+    const long long n = (long long)(geo_.nx + 2) * (geo_.ny + 2) * (geo_.nz + 2);
+    const int grid = grid_for(n);
+    if (d_.precision_bits == 64)
+        k_refresh_envelope<double><<<grid, 256, 0, stream_>>>(static_cast<double*>(origin(which)), geo_, d_.q);
+    else
+        k_refresh_envelope<float><<<grid, 256, 0, stream_>>>(static_cast<float*>(origin(which)), geo_, d_.q);
+    cuda_check(cudaGetLastError(), "k_refresh_envelope");
+}
+
+template <typename T>
+void Lattice::launch_tma(StepArgs<T>& a, int parity) {
+    const KernelEntry* k = kernel_tma_;
+    const std::size_t smem = std::size_t(k->stages) * d_.q * k->tile_x * k->tile_y * sizeof(T) + 64;
+    if (tma_grid_ == 0) {
+        cuda_check(cudaFuncSetAttribute(k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "smem attr");
+        int per_sm = 0;
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k->fn, k->tile_x * k->tile_y, smem),
+                   "occupancy");
+        int sms = 0;
+        cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_), "sm count");
+        tma_grid_ = std::max(1, per_sm) * sms;
+    }
+    if (!envelope_valid_) refresh_envelope(parity);
+    CUtensorMap map = tmap_[parity];
+    int xoff = tma_xoff_;
+    void* args[] = {&a, &map, &xoff};
+    cuda_check(cudaLaunchKernel(k->fn, dim3(unsigned(tma_grid_)), dim3(unsigned(k->tile_x * k->tile_y)), args, smem,
+                                stream_), "launch tma");
+    envelope_valid_ = true;  // the kernel pushed the periodic images into the output buffer
+}
+
 void Lattice::set_uniform_slot(int32_t slot) {
     if (slot < 0 || slot >= int32_t(chains_.size()))
         throw std::invalid_argument("slot " + std::to_string(slot) + " is not registered");
@@ -629,6 +723,10 @@ void Lattice::select_kernel() {
     if (!fixups_.empty())
         kernel_main_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_ & ~(KM_REGV | KM_REGP),
                                    LAYOUT_TWO_POP);
+    kernel_tma_ = nullptr;
+    tma_grid_ = 0;
+    if (tma_ok_ && fixups_.empty() && !(km_needed_ & KM_SKIP))
+        kernel_tma_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_, LAYOUT_TMA);
 }
 
 void Lattice::set_dispatch(const int32_t* tags, std::size_t n) {
@@ -652,6 +750,7 @@ void Lattice::check_dispatch() const {
 }
 
 void Lattice::reset_aa() {
+    envelope_valid_ = false;
     if (!aa()) return;
     const std::size_t bytes = std::size_t(d_.q) * std::size_t(geo_.dstride) * (d_.precision_bits / 8);
     cuda_check(cudaMemsetAsync(buf_[0], 0, bytes, stream_), "memset");
@@ -660,6 +759,7 @@ void Lattice::reset_aa() {
 
 void Lattice::fill_equilibrium(const double* rho, const double* ux, const double* uy,
                                const double* uz) {
+    envelope_valid_ = false;
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
     reset_aa();
     const long long plane_cells = (long long)geo_.nx * geo_.ny;
@@ -693,6 +793,7 @@ void Lattice::fill_tgv(int64_t L, double u_inf) {
         throw std::invalid_argument("TGV fill needs an L^3 domain");
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
     reset_aa();
+    envelope_valid_ = false;
     // cases.cpp:145-156: x = 2 pi / L * (i + 0.5); glibc sin / cos on the host.
     const double scale = 2.0 * 3.14159265358979323846 / double(L);
     std::vector<double> tab(std::size_t(3 * L));
@@ -721,7 +822,10 @@ void Lattice::fill_tgv(int64_t L, double u_inf) {
 // chunked over z planes through the staging buffer.
 void Lattice::copy_canonical(void* host, bool to_device, bool as_double, int elem_bytes) {
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
-    if (to_device) reset_aa();
+    if (to_device) {
+        reset_aa();
+        envelope_valid_ = false;
+    }
     const long long plane_cells = (long long)geo_.nx * geo_.ny;
     const long long n = cells();
     const int zc = int(std::max<long long>(1, (long long)staging_bytes_ / (8 * plane_cells)));
@@ -774,6 +878,7 @@ void Lattice::download_raw(void* canon) {
 // Envelope-inclusive AcceleratedBlock arrays: the whole (nx+2)(ny+2)(nz+2)
 // box of every direction, including the envelope the caller refreshed.
 void Lattice::upload_block(const void* f, const int64_t ext[3]) {
+    envelope_valid_ = false;
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
     const int s = d_.precision_bits / 8;
     const long long vol = ext[0] * ext[1] * ext[2];
@@ -972,6 +1077,11 @@ void Lattice::launch_step(int parity) {
         aa_odd_layout_ = !aa_odd_layout_;
         return;
     }
+    if (!linked && kernel_tma_) {
+        launch_tma<T>(a, parity);
+        return;
+    }
+    envelope_valid_ = false;  // the other kernels wrap in-kernel and leave the envelope stale
     if (!linked) {
         a.z_begin = 0;
         a.z_step = 1;
@@ -1044,6 +1154,10 @@ void Lattice::invalidate_graph() {
 
 void Lattice::ensure_graph() {
     if (graph_) return;
+    if (kernel_tma_ && !envelope_valid_ && !(lower_.linked || upper_.linked)) {
+        refresh_envelope(cur_);  // keep the one-off refresh out of the replayed graph
+        envelope_valid_ = true;
+    }
     const int cur = cur_;
     const bool odd = aa_odd_layout_;
     const int64_t steps = steps_;

@@ -149,6 +149,18 @@ class Lattice {
     unsigned long long* d_list_ = nullptr;
     int64_t step_bytes_ = 0;  // algorithmic bytes per step
     void build_lists(const std::vector<uint8_t>& u8);
+    // TMA-staged dense kernel (single slab): tensor maps of both buffers, and
+    // whether the input buffer's envelope holds the periodic images
+    const KernelEntry* kernel_tma_ = nullptr;
+    CUtensorMap tmap_[2];
+    int tma_xoff_ = 0;
+    bool tma_ok_ = false;
+    bool envelope_valid_ = false;
+    int tma_grid_ = 0;
+    void setup_tma();
+    void refresh_envelope(int which);
+    template <typename T>
+    void launch_tma(StepArgs<T>& a, int parity);
     // CUDA graph of two consecutive steps (parity 0 -> 1 -> 0), replayed by
     // step() / time_steps(); invalidated whenever kernels, slots or links change
     cudaGraphExec_t graph_ = nullptr;

@@ -422,3 +422,44 @@ def test_field_dump_bytes_match_reference(reference, tmp_path, name):
     dims, prec, data = dlb.read_field_dump(str(mine))
     assert dims == setup.dims and prec == bits // 8
     assert np.array_equal(data, run.gather_populations())
+
+
+
+# ---------------------------------------------------------------- TMA vs plain-load kernels
+@pytest.mark.parametrize("name", ["tgv16_bgk_f64", "tgv12_bgk_f32", "cavity32_trt_f32", "cavity64_bgk_f64_c1",
+                                  "tgv128_bgk_f32_c5", "cavity128_trt_f32_c3"])
+def test_tma_and_plain_kernels_bit_identical_to_reference(golden, name):
+    """The TMA-staged kernel (default for dense single-slab lattices) and the
+    plain-load kernel both reproduce the reference bit for bit."""
+    setup, bits, steps = product_setup(CASES[name])
+    names = []
+    for tma in (True, False):
+        run = dlb.build_run(setup, precision=bits, tma=tma)
+        run.advance(steps)
+        assert canonical_hash(run.gather_populations()) == golden[name]["sha256"], run.kernel_name()
+        names.append(run.kernel_name())
+    assert "k_tma" in names[0] and "k_pull" in names[1]
+
+
+def test_tma_d3q27_rr(oracle):
+    spec = dict(q27_case(24, RR, 64), steps=12)
+    got, run = run_product(spec)
+    want = oracle.run_case(Case(kind="tgv", L=24, Re=1600.0, Ma=0.2, collision=RR, q=27), np.float64, 12)
+    assert np.array_equal(got, want)
+    assert "k_tma" in run.kernel_name()
+
+
+def test_tma_envelope_after_upload_and_odd_counts(oracle):
+    """The periodic envelope images are re-primed after an upload and kept
+    current across single steps and graph replays."""
+    case = Case(kind="tgv", L=20, Re=50.0, Ma=0.1, collision=TRT)
+    dims, per, rec, slot = case.setup()
+    f = oracle.initial_state(case, np.float32)
+    setup, _, _ = product_setup(dict(kind="tgv", L=20, Re=50.0, Ma=0.1, collision=TRT, bits=32, steps=0))
+    run = dlb.build_run(setup, precision=32)
+    run.advance(3)
+    run.upload_populations(f.astype(np.float64))
+    for chunk in (1, 6, 1, 9):
+        run.advance(chunk)
+        oracle.step(19, dims, per, rec, slot, f, chunk)
+        assert np.array_equal(run.gather_populations(), f.astype(np.float64)), chunk
