@@ -19,7 +19,6 @@ from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import subprocess
 import sys
@@ -221,7 +220,7 @@ def main():
     ap.add_argument("--L", type=int, default=None, help="override the edge length (profiling only)")
     ap.add_argument("--arith", default="exact", choices=["exact", "fast"])
     ap.add_argument("--layout", default="twopop", choices=["twopop", "aa"])
-    ap.add_argument("--no-tma", action="store_true", help="plain-load dense kernel instead of the TMA-staged one")
+    ap.add_argument("--tma", action="store_true", help="TMA-staged dense kernel instead of the plain-load one")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sparse", action="store_true",
                     help="c4: kind-sorted sparse lists (NoDynamics skipped) instead of the dense sweep")
@@ -246,7 +245,6 @@ def main():
     torch.cuda.set_device(local)
 
     kind, L, Re, Ma, coll, q, bits, scaling, desc = CONFIGS[args.config]
-    kname = None
     if scaling == "weak":
         L = int(round(L * world ** (1.0 / 3.0)))  # perfmodel.cpp:76-85 weak sizes
     if args.L:
@@ -272,7 +270,7 @@ def main():
     layout = args.layout if world == 1 else "twopop"  # AA runs single-slab lattices
     run = dlb.build_run(setup, precision=bits, arith=args.arith,
                         dist=(rank, world) if world > 1 else None, devices=[local], layout=layout,
-                        skip_nodynamics=skip, tma=not args.no_tma)
+                        skip_nodynamics=skip, tma=args.tma)
     cells_total = run.num_cells()
     bpc, dev_bytes, launches = run.traffic()
 

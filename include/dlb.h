@@ -98,10 +98,11 @@ typedef struct dlb_lattice_desc {
  * use per-slot cell lists (one launch per dynamics kind); z-slabs use the
  * masked dense sweep. */
 #define DLB_FLAG_SKIP_NODYNAMICS 1
-/* Use the plain-load dense kernel instead of the TMA-staged one (the TMA path
- * is the default for dense single-slab two-population lattices; the
- * environment variable DLB_NO_TMA has the same effect). */
-#define DLB_FLAG_NO_TMA 2
+/* Use the TMA-staged dense kernel (warp-specialised producer, q 4-D tensor box
+ * loads per tile into an mbarrier ring) for single-slab two-population
+ * lattices. Opt-in: on B200 it reaches 0.58-0.74 of the copy roofline against
+ * 0.94-0.99 for the default plain-load kernel (profiles/r01_summary.md). */
+#define DLB_FLAG_TMA 2
 
 DLB_API dlb_status dlb_lattice_create(const dlb_lattice_desc* desc, const dlb_registry* reg,
                                       dlb_lattice** out);

@@ -53,7 +53,7 @@ class LatticeDesc(C.Structure):
 
 
 FLAG_SKIP_NODYNAMICS = 1
-FLAG_NO_TMA = 2
+FLAG_TMA = 2
 
 
 class BlockView(C.Structure):

@@ -212,7 +212,7 @@ def init_porous(cfg: CaseConfig, solid: np.ndarray | None = None) -> CaseSetup:
 def build_run(setup: CaseSetup, registry: DynamicsRegistry | None = None, precision: int = 64,
               slabs: int = 1, dispatch: DispatchSet | None = None, arith: str = "exact",
               dist=None, devices=None, layout: str = "twopop",
-              skip_nodynamics: bool = False, tma: bool = True) -> DeviceRun:
+              skip_nodynamics: bool = False, tma: bool = False) -> DeviceRun:
     """Register the setup's chains, build the device run, fill tags and state
     (cases.cpp:279-297 + multiblock.cpp:252-287)."""
     registry = registry or DynamicsRegistry()

@@ -281,34 +281,65 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned phase) {
     } while (!done);
 }
 
-template <typename T, int Q, int BX, int BY>
-__device__ __forceinline__ void tma_issue_tile(const CUtensorMap* map, T* dst, unsigned bar, int x0, int y0,
-                                               int z, int xoff) {
-    using L = Lat<Q>;
-    constexpr unsigned bytes = unsigned(Q * BX * BY * sizeof(T));
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-    sfor<Q>([&](auto I) {
-        constexpr int i = decltype(I)::value;
-        constexpr int cx = L::c[i][0], cy = L::c[i][1], cz = L::c[i][2];
-        const int c0 = x0 - cx + xoff, c1 = y0 - cy + 1, c2 = z - cz + 1, c3 = i;
-        asm volatile(
-            "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-            " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst + i * BX * BY)),
-            "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
-            : "memory");
-    });
+// Lattice velocities for the TMA issue loop (kept as a runtime loop: a fully
+// unrolled run of q tensor copies exhausts the uniform register file).
+__constant__ signed char kTmaC[27][3] = {
+    {0, 0, 0},
+    {-1, 0, 0}, {1, 0, 0}, {0, -1, 0}, {0, 1, 0}, {0, 0, -1}, {0, 0, 1},
+    {-1, -1, 0}, {1, 1, 0}, {-1, 1, 0}, {1, -1, 0},
+    {-1, 0, -1}, {1, 0, 1}, {-1, 0, 1}, {1, 0, -1},
+    {0, -1, -1}, {0, 1, 1}, {0, -1, 1}, {0, 1, -1},
+    {-1, -1, -1}, {1, 1, 1}, {-1, -1, 1}, {1, 1, -1},
+    {-1, 1, -1}, {1, -1, 1}, {1, -1, -1}, {-1, 1, 1}};
+
+// TMA tile loads need a 16-B aligned start in the innermost dimension, so each
+// direction's box starts at x0 - E (E = 16 B / sizeof(T)) and is BX + 2E wide;
+// the x shift of the pull is applied when reading shared memory.
+template <typename T>
+__host__ __device__ constexpr int tma_pad() {
+    return int(16 / sizeof(T));
 }
 
+template <typename T, int Q, int BX, int BY>
+__device__ __noinline__ void tma_issue_tile(const CUtensorMap* map, T* dst, unsigned bar, int x0, int y0, int z,
+                                            int xoff) {
+    constexpr int E = tma_pad<T>();
+    constexpr int W = BX + 2 * E;
+    constexpr unsigned bytes = unsigned(Q * W * BY * sizeof(T));
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    const unsigned long long desc = reinterpret_cast<unsigned long long>(map);
+    const unsigned base = smem_u32(dst);
+#pragma unroll 1
+    for (int i = 0; i < Q; ++i) {
+        const int c0 = x0 - E + xoff, c1 = y0 - kTmaC[i][1] + 1, c2 = z - kTmaC[i][2] + 1;
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(base + unsigned(i * W * BY * sizeof(T))),
+            "l"(desc), "r"(c0), "r"(c1), "r"(c2), "r"(i), "r"(bar)
+            : "memory");
+    }
+}
+
+// Warp-specialised: warps 0..NW-1 collide (each thread RPT cells of the
+// tile, rows ty + k * (BY / RPT)), warp NW is the TMA producer. full[st]
+// completes when the q boxes of a tile have landed (expect_tx), empty[st]
+// when all consumer warps have pulled their values out of the stage.
 template <typename T, int Q, unsigned KM, int BX, int BY, int S>
-__global__ void __launch_bounds__(BX * BY, (sizeof(T) == 4 ? 2 : 1))
-    k_tma(const __grid_constant__ StepArgs<T> a, const __grid_constant__ CUtensorMap tin, int xoff) {
+__global__ void __launch_bounds__(BX * BY + 32, 1)
+    k_tma(const __grid_constant__ StepArgs<T> a, const CUtensorMap* __restrict__ tin, int xoff) {
     using L = Lat<Q>;
+    constexpr int NT = BX * BY;             // consumer threads (one cell each)
+    constexpr int NW = NT / 32;             // consumer warps
+    constexpr int RPT = BX * BY / NT;       // cells per consumer thread
+    constexpr int E = tma_pad<T>();
+    constexpr int W = BX + 2 * E;           // padded box width (aligned start, see tma_issue_tile)
+    constexpr int STAGE = Q * W * BY;
     const Geo& g = a.g;
     extern __shared__ __align__(128) unsigned char smem[];
     T* ring = reinterpret_cast<T*>(smem);
-    unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + size_t(S) * Q * BX * BY * sizeof(T));
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + size_t(S) * STAGE * sizeof(T));
+    unsigned long long* empty = full + S;
     const int tid = threadIdx.x;
-    const int tx = tid % BX, ty = tid / BX;
     const int tiles_x = (g.nx + BX - 1) / BX, tiles_y = (g.ny + BY - 1) / BY;
     const int tiles_per_plane = tiles_x * tiles_y;
     const long long ntiles = static_cast<long long>(tiles_per_plane) * g.nz;
@@ -319,72 +350,84 @@ __global__ void __launch_bounds__(BX * BY, (sizeof(T) == 4 ? 2 : 1))
         x0 = (r % tiles_x) * BX;
     };
     if (tid == 0) {
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(&tin)) : "memory");
-        for (int st = 0; st < S; ++st)
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bars + st)) : "memory");
+        for (int st = 0; st < S; ++st) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(full + st)) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(empty + st)), "r"(NW) : "memory");
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (tid == 0) {
-        for (int st = 0; st < S; ++st) {
-            const long long t = blockIdx.x + static_cast<long long>(st) * gridDim.x;
-            if (t >= ntiles) break;
-            int x0, y0, z;
-            tile_xyz(t, x0, y0, z);
-            tma_issue_tile<T, Q, BX, BY>(&tin, ring + size_t(st) * Q * BX * BY, smem_u32(bars + st), x0, y0, z, xoff);
+
+    if (tid >= NT) {  // ---- producer warp
+        if (tid == NT) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(tin)) : "memory");
+            int k = 0;
+            for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+                const int st = k % S;
+                if (k >= S) mbar_wait(smem_u32(empty + st), unsigned((k / S) - 1) & 1u);
+                int x0, y0, z;
+                tile_xyz(t, x0, y0, z);
+                tma_issue_tile<T, Q, BX, BY>(tin, ring + size_t(st) * STAGE, smem_u32(full + st), x0, y0, z, xoff);
+            }
         }
+        return;
     }
+
+    // ---- consumer warps
+    const int tx = tid % BX, ty0 = tid / BX;
+    constexpr int ROWS = NT / BX;  // rows covered by one pass of the consumer threads
     int k = 0;
     for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
         const int st = k % S;
-        const unsigned phase = unsigned(k / S) & 1u;
         int x0, y0, z;
         tile_xyz(t, x0, y0, z);
-        mbar_wait(smem_u32(bars + st), phase);
-        T f[Q];
-        const T* tile = ring + size_t(st) * Q * BX * BY;
-        sfor<Q>([&](auto I) {
-            constexpr int i = decltype(I)::value;
-            f[i] = tile[i * BX * BY + tid];
-        });
-        __syncthreads();  // every thread has its values: the stage can be refilled
-        if (tid == 0) {
-            const long long tn = t + static_cast<long long>(S) * gridDim.x;
-            if (tn < ntiles) {
-                int nx0, ny0, nz0;
-                tile_xyz(tn, nx0, ny0, nz0);
-                tma_issue_tile<T, Q, BX, BY>(&tin, ring + size_t(st) * Q * BX * BY, smem_u32(bars + st), nx0,
-                                             ny0, nz0, xoff);
-            }
-        }
-        const int x = x0 + tx, y = y0 + ty;
-        if (x >= g.nx || y >= g.ny) continue;
-        int s = a.uniform_slot;
-        if (a.slot != nullptr) s = a.slot[(static_cast<long long>(z) * g.ny + y) * g.nx + x];
-        Cell<T, Q>::template apply<KM>(f, a.rec[s]);
-        const int center = z * g.plane + y * g.pitch + x;
-        sfor<Q>([&](auto I) {
-            constexpr int i = decltype(I)::value;
-            a.fout[i][center] = f[i];
-        });
-        // periodic images of the outgoing links of boundary cells
-        const bool bx_lo = g.per_x && x == 0, bx_hi = g.per_x && x == g.nx - 1;
-        const bool by_lo = g.per_y && y == 0, by_hi = g.per_y && y == g.ny - 1;
-        const bool bz_lo = g.per_z && z == 0, bz_hi = g.per_z && z == g.nz - 1;
-        if (bx_lo || bx_hi || by_lo || by_hi || bz_lo || bz_hi) {
+        mbar_wait(smem_u32(full + st), unsigned(k / S) & 1u);
+        const T* tile = ring + size_t(st) * STAGE;
+        T fr[RPT][Q];
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+            const int ty = ty0 + r * ROWS;
             sfor<Q>([&](auto I) {
                 constexpr int i = decltype(I)::value;
-                constexpr int cx = L::c[i][0], cy = L::c[i][1], cz = L::c[i][2];
-                int X = x, Y = y, Z = z;
-                bool moved = false;
-                if (cx > 0 && bx_hi) { X = x - g.nx; moved = true; }
-                if (cx < 0 && bx_lo) { X = x + g.nx; moved = true; }
-                if (cy > 0 && by_hi) { Y = y - g.ny; moved = true; }
-                if (cy < 0 && by_lo) { Y = y + g.ny; moved = true; }
-                if (cz > 0 && bz_hi) { Z = z - g.nz; moved = true; }
-                if (cz < 0 && bz_lo) { Z = z + g.nz; moved = true; }
-                if (moved) a.fout[i][Z * g.plane + Y * g.pitch + X] = f[i];
+                constexpr int cx = L::c[i][0];
+                fr[r][i] = tile[(i * BY + ty) * W + tx + E - cx];
             });
+        }
+        __syncwarp();
+        if ((tid & 31) == 0)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(empty + st)) : "memory");
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+            const int x = x0 + tx, y = y0 + ty0 + r * ROWS;
+            if (x >= g.nx || y >= g.ny) continue;
+            T (&f)[Q] = fr[r];
+            int s = a.uniform_slot;
+            if (a.slot != nullptr) s = a.slot[(static_cast<long long>(z) * g.ny + y) * g.nx + x];
+            Cell<T, Q>::template apply<KM>(f, a.rec[s]);
+            const int center = z * g.plane + y * g.pitch + x;
+            sfor<Q>([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                a.fout[i][center] = f[i];
+            });
+            // periodic images of the outgoing links of boundary cells
+            const bool bx_lo = g.per_x && x == 0, bx_hi = g.per_x && x == g.nx - 1;
+            const bool by_lo = g.per_y && y == 0, by_hi = g.per_y && y == g.ny - 1;
+            const bool bz_lo = g.per_z && z == 0, bz_hi = g.per_z && z == g.nz - 1;
+            if (bx_lo || bx_hi || by_lo || by_hi || bz_lo || bz_hi) {
+                sfor<Q>([&](auto I) {
+                    constexpr int i = decltype(I)::value;
+                    constexpr int cx = L::c[i][0], cy = L::c[i][1], cz = L::c[i][2];
+                    int X = x, Y = y, Z = z;
+                    bool moved = false;
+                    if (cx > 0 && bx_hi) { X = x - g.nx; moved = true; }
+                    if (cx < 0 && bx_lo) { X = x + g.nx; moved = true; }
+                    if (cy > 0 && by_hi) { Y = y - g.ny; moved = true; }
+                    if (cy < 0 && by_lo) { Y = y + g.ny; moved = true; }
+                    if (cz > 0 && bz_hi) { Z = z - g.nz; moved = true; }
+                    if (cz < 0 && bz_lo) { Z = z + g.nz; moved = true; }
+                    if (moved) a.fout[i][Z * g.plane + Y * g.pitch + X] = f[i];
+                });
+            }
         }
     }
 }
@@ -423,7 +466,8 @@ __global__ void __launch_bounds__(BX * BY, (sizeof(T) == 4 ? 2 : 1))
         LIST_ENTRY(T, Q, KM_RR | KM_REGV | KM_REGP, false), LIST_ENTRY(T, Q, KM_ALL, false), \
         LIST_ENTRY(T, Q, KM_BB, true), LIST_ENTRY(T, Q, KM_MBB, true)
 
-// TMA tiles: 256 threads; f32 64 x 4 cells (4 stages), f64 32 x 8 (3 stages)
+// TMA tiles (one consumer thread per cell + 1 producer warp): f32 64 x 8 cells
+// (3 stages), D3Q19 f64 32 x 16 (2 stages), D3Q27 fp64 32 x 8 (2 stages)
 #define TMA_ENTRY(T, Q, KM, BX, BY, S)                                                   \
     KernelEntry {                                                                        \
         int(sizeof(T) * 8), Q, unsigned(KM), LAYOUT_TMA,                                  \
@@ -431,12 +475,12 @@ __global__ void __launch_bounds__(BX * BY, (sizeof(T) == 4 ? 2 : 1))
             "k_tma<" #T ",D3Q" #Q "," #KM ">[" DLB_STR(DLB_MODE) "]", BX, BY, S               \
     }
 #define TMA_SET                                                                           \
-    TMA_ENTRY(float, 19, KM_BGK, 64, 4, 4), TMA_ENTRY(float, 19, KM_TRT, 64, 4, 4),       \
-        TMA_ENTRY(float, 19, KM_BGK | KM_BB | KM_MBB, 64, 4, 4),                          \
-        TMA_ENTRY(float, 19, KM_TRT | KM_BB | KM_MBB, 64, 4, 4),                          \
-        TMA_ENTRY(double, 19, KM_BGK, 32, 8, 3), TMA_ENTRY(double, 19, KM_TRT, 32, 8, 3), \
-        TMA_ENTRY(double, 19, KM_BGK | KM_BB | KM_MBB, 32, 8, 3),                         \
-        TMA_ENTRY(double, 19, KM_TRT | KM_BB | KM_MBB, 32, 8, 3),                         \
+    TMA_ENTRY(float, 19, KM_BGK, 64, 8, 3), TMA_ENTRY(float, 19, KM_TRT, 64, 8, 3),       \
+        TMA_ENTRY(float, 19, KM_BGK | KM_BB | KM_MBB, 64, 8, 3),                          \
+        TMA_ENTRY(float, 19, KM_TRT | KM_BB | KM_MBB, 64, 8, 3),                          \
+        TMA_ENTRY(double, 19, KM_BGK, 32, 16, 2), TMA_ENTRY(double, 19, KM_TRT, 32, 16, 2), \
+        TMA_ENTRY(double, 19, KM_BGK | KM_BB | KM_MBB, 32, 16, 2),                        \
+        TMA_ENTRY(double, 19, KM_TRT | KM_BB | KM_MBB, 32, 16, 2),                        \
         TMA_ENTRY(double, 27, KM_RR, 32, 8, 2)
 
 #define Q19_SET(T)                                                                        \

@@ -62,9 +62,6 @@ struct StepArgs {
 enum Layout : int { LAYOUT_TWO_POP = 0, LAYOUT_AA = 1, LAYOUT_AA_ODD = 2, LAYOUT_LIST = 3, LAYOUT_LIST_MASKED = 4,
                     LAYOUT_TMA = 5 };
 
-using StepKernelF = void (*)(StepArgs<float>);
-using StepKernelD = void (*)(StepArgs<double>);
-
 struct KernelEntry {
     int precision_bits;
     int q;

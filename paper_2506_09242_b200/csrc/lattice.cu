@@ -411,6 +411,7 @@ Lattice::~Lattice() {
     cudaFree(d_slot_);
     cudaFree(d_list_);
     cudaFree(d_fix_);
+    cudaFree(d_tmap_);
     cudaFree(d_flags_);
     cudaFree(d_counter_);
     cudaFree(staging_);
@@ -627,7 +628,7 @@ void Lattice::build_fixups(const std::vector<uint8_t>& u8) {
 // (needs pitch >= nx + 2 + 16 B / s).
 void Lattice::setup_tma() {
     tma_ok_ = false;
-    if (aa() || std::getenv("DLB_NO_TMA") || (d_.flags & DLB_FLAG_NO_TMA)) return;
+    if (aa() || !(d_.flags & DLB_FLAG_TMA)) return;
     const int s = d_.precision_bits / 8;
     const int e = 16 / s;
     if (geo_.pitch < geo_.nx + 2 + e) return;
@@ -640,7 +641,7 @@ void Lattice::setup_tma() {
         cudaGetLastError();
         return;
     }
-    const int bx = s == 4 ? 64 : 32, by = 256 / bx;
+    const int bx = (s == 4 ? 64 : 32) + 2 * e, by = (s == 4 || d_.q == 27) ? 8 : 16;  // padded box (kernel: W x BY)
     for (int b = 0; b < 2; ++b) {
         char* base = static_cast<char*>(buf_[b]) + std::size_t(align_ - e) * s;
         const cuuint64_t dims[4] = {cuuint64_t(geo_.pitch), cuuint64_t(geo_.ny + 2), cuuint64_t(geo_.nz + 2),
@@ -655,6 +656,8 @@ void Lattice::setup_tma() {
             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return;
     }
+    cuda_check(cudaMalloc(&d_tmap_, 2 * sizeof(CUtensorMap)), "cudaMalloc tensor maps");
+    cuda_check(cudaMemcpy(d_tmap_, tmap_, 2 * sizeof(CUtensorMap), cudaMemcpyHostToDevice), "tensor maps");
     tma_xoff_ = e;
     tma_ok_ = true;
 }
@@ -672,22 +675,23 @@ void Lattice::refresh_envelope(int which) {
 template <typename T>
 void Lattice::launch_tma(StepArgs<T>& a, int parity) {
     const KernelEntry* k = kernel_tma_;
-    const std::size_t smem = std::size_t(k->stages) * d_.q * k->tile_x * k->tile_y * sizeof(T) + 64;
+    const int e = int(16 / sizeof(T));
+    const std::size_t smem = std::size_t(k->stages) * d_.q * (k->tile_x + 2 * e) * k->tile_y * sizeof(T) + 128;
     if (tma_grid_ == 0) {
         cuda_check(cudaFuncSetAttribute(k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "smem attr");
         int per_sm = 0;
-        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k->fn, k->tile_x * k->tile_y, smem),
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k->fn, k->tile_x * k->tile_y + 32, smem),
                    "occupancy");
         int sms = 0;
         cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_), "sm count");
         tma_grid_ = std::max(1, per_sm) * sms;
     }
     if (!envelope_valid_) refresh_envelope(parity);
-    CUtensorMap map = tmap_[parity];
+    const CUtensorMap* map = d_tmap_ + parity;
     int xoff = tma_xoff_;
     void* args[] = {&a, &map, &xoff};
-    cuda_check(cudaLaunchKernel(k->fn, dim3(unsigned(tma_grid_)), dim3(unsigned(k->tile_x * k->tile_y)), args, smem,
-                                stream_), "launch tma");
+    cuda_check(cudaLaunchKernel(k->fn, dim3(unsigned(tma_grid_)), dim3(unsigned(k->tile_x * k->tile_y + 32)), args,
+                                smem, stream_), "launch tma");
     envelope_valid_ = true;  // the kernel pushed the periodic images into the output buffer
 }
 

@@ -77,6 +77,7 @@ class Lattice {
     int64_t device_bytes() const { return device_bytes_; }
     int launches_per_step() const;
     const char* kernel_name() const {
+        if (kernel_tma_ && !(lower_.linked || upper_.linked)) return kernel_tma_->name;
         if (kernel_main_ && !fixups_.empty() && !(lower_.linked || upper_.linked)) return kernel_main_->name;
         return kernel_ ? kernel_->name : "<none>";
     }
@@ -86,7 +87,6 @@ class Lattice {
     void set_periodic_override(bool x, bool y, bool z);
 
   private:
-    friend struct LatticeAccess;
     void select_kernel();
     template <typename T>
     void launch_step(int parity);
@@ -153,6 +153,7 @@ class Lattice {
     // whether the input buffer's envelope holds the periodic images
     const KernelEntry* kernel_tma_ = nullptr;
     CUtensorMap tmap_[2];
+    CUtensorMap* d_tmap_ = nullptr;  // the two maps in device global memory
     int tma_xoff_ = 0;
     bool tma_ok_ = false;
     bool envelope_valid_ = false;

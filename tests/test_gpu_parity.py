@@ -13,7 +13,7 @@ import numpy as np
 import pytest
 
 import paper_2506_09242_b200 as dlb
-from golden_cases import CASES, SPHERE_DIMS, SPHERE_RAW
+from golden_cases import CASES, SPHERE_RAW
 from paper_2506_09242_b200.dolb import LinkType
 from pyoracle import BGK, RR, TRT, Case, canonical_hash, descriptor
 
@@ -429,8 +429,8 @@ def test_field_dump_bytes_match_reference(reference, tmp_path, name):
 @pytest.mark.parametrize("name", ["tgv16_bgk_f64", "tgv12_bgk_f32", "cavity32_trt_f32", "cavity64_bgk_f64_c1",
                                   "tgv128_bgk_f32_c5", "cavity128_trt_f32_c3"])
 def test_tma_and_plain_kernels_bit_identical_to_reference(golden, name):
-    """The TMA-staged kernel (default for dense single-slab lattices) and the
-    plain-load kernel both reproduce the reference bit for bit."""
+    """The TMA-staged kernel (opt-in) and the default plain-load kernel both
+    reproduce the reference bit for bit."""
     setup, bits, steps = product_setup(CASES[name])
     names = []
     for tma in (True, False):
@@ -443,7 +443,10 @@ def test_tma_and_plain_kernels_bit_identical_to_reference(golden, name):
 
 def test_tma_d3q27_rr(oracle):
     spec = dict(q27_case(24, RR, 64), steps=12)
-    got, run = run_product(spec)
+    setup, bits, steps = product_setup(spec)
+    run = dlb.build_run(setup, precision=bits, tma=True)
+    run.advance(steps)
+    got = run.gather_populations()
     want = oracle.run_case(Case(kind="tgv", L=24, Re=1600.0, Ma=0.2, collision=RR, q=27), np.float64, 12)
     assert np.array_equal(got, want)
     assert "k_tma" in run.kernel_name()
@@ -456,7 +459,8 @@ def test_tma_envelope_after_upload_and_odd_counts(oracle):
     dims, per, rec, slot = case.setup()
     f = oracle.initial_state(case, np.float32)
     setup, _, _ = product_setup(dict(kind="tgv", L=20, Re=50.0, Ma=0.1, collision=TRT, bits=32, steps=0))
-    run = dlb.build_run(setup, precision=32)
+    run = dlb.build_run(setup, precision=32, tma=True)
+    assert "k_tma" in run.kernel_name()
     run.advance(3)
     run.upload_populations(f.astype(np.float64))
     for chunk in (1, 6, 1, 9):

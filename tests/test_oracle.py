@@ -13,7 +13,7 @@ import numpy as np
 import pytest
 
 from golden_cases import CASES, make_case
-from pyoracle import BB, BGK, COLLIDE, MBB, NODYN, RR, TRT, Case, Recipe, canonical_hash, descriptor
+from pyoracle import BB, BGK, MBB, NODYN, RR, TRT, Case, Recipe, canonical_hash, descriptor
 
 C19, W19, OPP19 = descriptor(19)
 C27, W27, OPP27 = descriptor(27)
