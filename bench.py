@@ -273,6 +273,7 @@ def main():
                         skip_nodynamics=skip, tma=args.tma)
     cells_total = run.num_cells()
     bpc, dev_bytes, launches = run.traffic()
+    kernel = run.kernel_name()
 
     for _ in range(args.warmup):
         run.advance(1)
@@ -306,7 +307,7 @@ def main():
         try:
             with open(tp) as f:
                 tr = json.load(f)
-            key = f"{args.config}:{run.kernel_name()}"
+            key = f"{args.config}:{kernel}"
             if key in tr:
                 traffic = tr[key]["bytes_per_cell"] * my_cells
         except Exception:
@@ -338,7 +339,7 @@ def main():
         "config": {"workload": f"{args.config}: {desc}", "L": L, "cells": cells_total,
                    "parallelism": f"z-slab x{world}",
                    "layout": "AA in-place SoA" if layout == "aa" else "two-population SoA",
-                   "arith": args.arith, "kernel": run.kernel_name(),
+                   "arith": args.arith, "kernel": kernel,
                    "l2": "inputs larger than L2 (state resident in HBM)",
                    "device_bytes_per_gpu": dev_bytes, **extra},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
