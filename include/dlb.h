@@ -19,6 +19,9 @@
  *   dlb_collide_and_stream        collide_and_stream<T>(AcceleratedBlock<T>&, registry,
  *                                 recipes, dispatch, nthreads) on HOST buffers
  *                                 (include/dolb/accelerated_lattice.hpp:124-127)
+ *   dlb_lattice_reduce* /         diag::tree_sum / kinetic_energy / vorticity_fd8 / enstrophy
+ *   dlb_tree_* / _snapshot_*      and Driver::sample / porous_extras on the resident state
+ *                                 (src/diagnostics.cpp:10-131, src/runner.cpp:346-448)
  *   dlb_case_*                    init_tgv / init_cavity / init_porous input generators
  *                                 (include/dolb/cases.hpp:96-98, src/cases.cpp:127-260)
  */
@@ -174,6 +177,81 @@ DLB_API dlb_status dlb_lattice_link_ipc(dlb_lattice* lat, int32_t side, const vo
 /* Advance several slabs of ONE process in lockstep (one step of each in turn),
  * the single-process analogue of MultiBlockRun::advance (multiblock.cpp:376-419). */
 DLB_API dlb_status dlb_lattices_step(dlb_lattice** lats, size_t n, int64_t nsteps);
+
+/* ---- GPU-resident diagnostics (the sampling step after the update) ----------
+ * Replaces the host post-processing of Driver::sample / porous_extras
+ * (runner.cpp:346-423) over gather_macroscopic (multiblock.cpp:443-484):
+ * kinetic energy (diagnostics.cpp:25-31), FD8 vorticity + enstrophy (:33-120),
+ * the cavity convergence sums (runner.cpp:433-444) and the porous plane / sample
+ * means (runner.cpp:346-399), computed from the resident state.
+ *
+ * Every reduction reproduces diag::tree_sum (diagnostics.cpp:10-18) BIT FOR BIT:
+ * the value sequence (x fastest, restricted / compacted as the runner builds
+ * its vectors) is split by the same recursive halving; each slab reduces on the
+ * device the maximal tree nodes that lie inside its segment of the global
+ * sequence, and dlb_tree_combine evaluates the nodes above them on the host.
+ * Leaves (<= 8 values, summed sequentially) cut by a segment boundary are
+ * returned as raw values (len 0). */
+typedef enum dlb_quantity {
+    DLB_Q_KINETIC = 0,        /* 0.5*|u|^2, all cells */
+    DLB_Q_ENSTROPHY = 1,      /* 0.5*|curl_fd8 u|^2, cells with a full stencil */
+    DLB_Q_DU_NUM = 2,         /* |u - u_snapshot|^2, all cells */
+    DLB_Q_DU_DEN = 3,         /* |u|^2, all cells */
+    DLB_Q_PRESSURE_FLUID = 4, /* cs2*rho, fluid cells with x in [x_begin, x_end) */
+    DLB_Q_UX_FLUID = 5,       /* ux, fluid cells with x in [x_begin, x_end) */
+    DLB_Q_UX_ALL = 6,         /* ux, all cells with x in [x_begin, x_end) */
+    DLB_Q_RHO_FLUID = 7,      /* rho, fluid cells with x in [x_begin, x_end) */
+} dlb_quantity;
+
+typedef struct dlb_reduce_args {
+    int32_t quantity;     /* dlb_quantity */
+    int32_t periodic[3];  /* ENSTROPHY: periodicity of the GLOBAL domain (valid-cell box) */
+    int64_t x_begin;      /* masked quantities: x window */
+    int64_t x_end;
+    /* ENSTROPHY on a slab that does not hold the whole z extent: velocity of the
+     * 4 global planes below z_origin / above z_origin + nz, host arrays laid out
+     * [plane][ux|uy|uz][y][x] as dlb_lattice_velocity_planes returns them (NULL
+     * where the stencil never reaches: non-periodic domain ends). */
+    const double* halo_below;
+    const double* halo_above;
+} dlb_reduce_args;
+
+/* One reduced node of the global tree: len >= 1 -> tree_sum of values
+ * [lo, lo + len); len == 0 -> the raw value at index lo. */
+typedef struct dlb_tree_part {
+    int64_t lo;
+    int64_t len;
+    double value;
+} dlb_tree_part;
+
+/* Number of values this slab contributes to the quantity's sequence. */
+DLB_API dlb_status dlb_lattice_reduce_count(dlb_lattice* lat, const dlb_reduce_args* args,
+                                            int64_t* count_out);
+/* Tree parts of this slab's segment [seg_begin, seg_begin + count) of a global
+ * sequence of n_total values. parts may be NULL to query the number (n_out). */
+DLB_API dlb_status dlb_lattice_reduce_parts(dlb_lattice* lat, const dlb_reduce_args* args,
+                                            int64_t n_total, int64_t seg_begin,
+                                            dlb_tree_part* parts, size_t cap, size_t* n_out);
+/* One-slab convenience: count, parts and combine -> tree_sum of the sequence. */
+DLB_API dlb_status dlb_lattice_reduce(dlb_lattice* lat, const dlb_reduce_args* args,
+                                      double* sum_out, int64_t* count_out);
+/* Host: tree_sum of a global sequence of n_total values from the parts of all
+ * slabs (any order). DLB_ERROR_INVALID_ARGUMENT if a needed node is missing. */
+DLB_API dlb_status dlb_tree_combine(int64_t n_total, const dlb_tree_part* parts, size_t n,
+                                    double* sum_out);
+/* Host: the parts segment [seg_begin, seg_end) of an n_total-value sequence
+ * owns (values left 0) -- for callers that reduce their own segments. */
+DLB_API dlb_status dlb_tree_plan(int64_t n_total, int64_t seg_begin, int64_t seg_end,
+                                 dlb_tree_part* parts, size_t cap, size_t* n_out);
+/* Host: diag::tree_sum (diagnostics.cpp:10-18) of a host array. */
+DLB_API dlb_status dlb_tree_sum(const double* values, int64_t n, double* sum_out);
+/* Keep the current velocity field on the device as the DU_NUM reference
+ * (the runner's prev_ux/uy/uz, runner.cpp:445-448). */
+DLB_API dlb_status dlb_lattice_snapshot_velocity(dlb_lattice* lat);
+/* Velocity of local planes [z0, z0 + nz) as [plane][ux|uy|uz][y][x] doubles
+ * (gather_macroscopic semantics): the halo planes a neighbouring slab needs. */
+DLB_API dlb_status dlb_lattice_velocity_planes(dlb_lattice* lat, int32_t z0, int32_t nz,
+                                               double* out);
 
 /* ---- drop-in for collide_and_stream<T> on a host AcceleratedBlock ----------- */
 /* Envelope-inclusive SoA arrays exactly as AcceleratedBlock<T> holds them

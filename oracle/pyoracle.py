@@ -405,6 +405,8 @@ class Reference:
             lib.ref_case_dump.argtypes = [C.POINTER(RefCase), C.c_int, C.c_int64, C.c_char_p]
             lib.ref_case_checksum.argtypes = [C.POINTER(RefCase), C.c_int, C.c_void_p, C.c_int,
                                               C.c_int64, C.c_void_p]
+            lib.ref_case_sample.argtypes = [C.POINTER(RefCase), C.c_int, C.c_int64, C.c_int64, C.c_void_p]
+            lib.ref_tree_sum.argtypes = [C.c_void_p, C.c_int64, C.POINTER(C.c_double)]
             Reference._lib = lib
         self.lib = Reference._lib
 
@@ -442,6 +444,22 @@ class Reference:
         rc = case.ref_struct()
         self._check(self.lib.ref_case_macro(C.byref(rc), precision_bits, nsteps, *[_ptr(a) for a in arrs]))
         return tuple(arrs)
+
+    def sample(self, case: Case, precision_bits: int, steps_a: int, steps_b: int) -> dict:
+        """The runner's sampling step on the reference's own fields
+        (runner.cpp:346-448): kinetic energy and enstrophy after steps_a + steps_b,
+        the cavity convergence sums between the two samples, porous extras."""
+        out = np.zeros(9)
+        rc = case.ref_struct()
+        self._check(self.lib.ref_case_sample(C.byref(rc), precision_bits, steps_a, steps_b, _ptr(out)))
+        keys = ["k", "eps", "nn", "dd", "k_perm", "ubar", "dp", "ux_in", "ux_out"]
+        return dict(zip(keys, (float(v) for v in out)))
+
+    def tree_sum(self, values: np.ndarray) -> float:
+        v = np.ascontiguousarray(values, np.float64)
+        out = C.c_double()
+        self._check(self.lib.ref_tree_sum(_ptr(v), v.size, C.byref(out)))
+        return out.value
 
     def dump(self, case: Case, precision_bits: int, nsteps: int, path: str):
         rc = case.ref_struct()

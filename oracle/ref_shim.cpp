@@ -23,6 +23,7 @@
 #include "dolb/cases.hpp"
 #include "dolb/chain.hpp"
 #include "dolb/descriptor.hpp"
+#include "dolb/diagnostics.hpp"
 #include "dolb/multiblock.hpp"
 #include "dolb/perfmodel.hpp"
 
@@ -54,7 +55,7 @@ dolb::LinkType base_of(int c) {
     throw std::invalid_argument("collision must be 0 (BGK), 1 (TRT) or 2 (RR)");
 }
 
-dolb::CaseSetup make_setup(const RefCase& rc) {
+dolb::CaseConfig make_config(const RefCase& rc) {
     dolb::CaseConfig cfg;
     cfg.kind = rc.kind == 0 ? dolb::CaseKind::Tgv
              : rc.kind == 1 ? dolb::CaseKind::Cavity
@@ -72,9 +73,14 @@ dolb::CaseSetup make_setup(const RefCase& rc) {
     cfg.upstream = rc.upstream;
     cfg.downstream = rc.downstream;
     cfg.plate_layers = rc.plate_layers;
+    cfg.geometry = rc.geometry ? rc.geometry : "";
+    return cfg;
+}
+
+dolb::CaseSetup make_setup(const RefCase& rc) {
+    dolb::CaseConfig cfg = make_config(rc);
     if (rc.kind == 0) return dolb::init_tgv(cfg);
     if (rc.kind == 1) return dolb::init_cavity(cfg);
-    cfg.geometry = rc.geometry ? rc.geometry : "";
     std::shared_ptr<const dolb::VoxelGeometry> geom;
     if (cfg.geometry == "plates") {
         geom = std::make_shared<dolb::VoxelGeometry>(
@@ -151,6 +157,85 @@ void dump_case(const RefCase& rc, int64_t steps, const char* path) {
     auto run = dolb::build_run<T>(setup, {1, 1, 2}, 2, registry);
     run.advance(steps);
     dolb::write_field_dump(path, run.gather_block());
+}
+
+
+// The runner's sampling step (Driver::sample / porous_extras,
+// proj/src/runner.cpp:346-448) on the reference's own gathered fields after
+// steps_a and steps_a + steps_b steps: out = {k, eps, nn, dd, k_perm, ubar, dp,
+// ux_in, ux_out} (nn / dd between the two samples; porous extras zero for
+// other cases).
+template <typename T>
+void sample_case(const RefCase& rc, int64_t steps_a, int64_t steps_b, double* out) {
+    const dolb::CaseConfig cfg = make_config(rc);
+    const dolb::CaseSetup setup = make_setup(rc);
+    auto registry = std::make_shared<dolb::DynamicsRegistry>();
+    auto run = dolb::build_run<T>(setup, {1, 1, 2}, 2, registry);
+    run.advance(steps_a);
+    std::vector<double> r0, x0, y0, z0;
+    run.gather_macroscopic(r0, x0, y0, z0);
+    run.advance(steps_b);
+    std::vector<double> rho, ux, uy, uz;
+    run.gather_macroscopic(rho, ux, uy, uz);
+    dolb::diag::VectorField u;
+    u.dims = setup.dims;
+    u.x = ux;
+    u.y = uy;
+    u.z = uz;
+    out[0] = dolb::diag::kinetic_energy(u);
+    out[1] = dolb::diag::enstrophy(dolb::diag::vorticity_fd8(u, setup.periodic));
+    std::vector<double> num(ux.size()), den(ux.size());
+    for (std::size_t i = 0; i < ux.size(); ++i) {
+        const double dx = ux[i] - x0[i];
+        const double dy = uy[i] - y0[i];
+        const double dz = uz[i] - z0[i];
+        num[i] = dx * dx + dy * dy + dz * dz;
+        den[i] = ux[i] * ux[i] + uy[i] * uy[i] + uz[i] * uz[i];
+    }
+    out[2] = dolb::diag::tree_sum(num);
+    out[3] = dolb::diag::tree_sum(den);
+    for (int k = 4; k < 9; ++k) out[k] = 0.0;
+    if (rc.kind != 2) return;
+    const auto& dims = setup.dims;
+    std::vector<uint8_t> fluid(std::size_t(dims[0] * dims[1] * dims[2]));
+    for (int64_t z = 0; z < dims[2]; ++z)
+        for (int64_t y = 0; y < dims[1]; ++y)
+            for (int64_t x = 0; x < dims[0]; ++x) {
+                const dolb::LinkType t = setup.chain_of(x, y, z)->links.back().type;
+                const bool solid = t == dolb::LinkType::BounceBack || t == dolb::LinkType::NoDynamics ||
+                                   t == dolb::LinkType::MovingBounceBack;
+                fluid[std::size_t((z * dims[1] + y) * dims[0] + x)] = solid ? 0 : 1;
+            }
+    const bool aperture = cfg.geometry == "plates";
+    auto plane_mean = [&](int64_t x, const std::vector<double>& f, double scale) {
+        std::vector<double> vals;
+        for (int64_t z = 0; z < dims[2]; ++z)
+            for (int64_t y = 0; y < dims[1]; ++y) {
+                const int64_t g = (z * dims[1] + y) * dims[0] + x;
+                if (fluid[std::size_t(g)]) vals.push_back(scale == 0.0 ? f[std::size_t(g)] : scale * f[std::size_t(g)]);
+            }
+        return vals.empty() ? 0.0 : dolb::diag::tree_mean(vals);
+    };
+    std::vector<double> vals, density;
+    for (int64_t z = 0; z < dims[2]; ++z)
+        for (int64_t y = 0; y < dims[1]; ++y)
+            for (int64_t x = setup.sample_begin; x < setup.sample_end; ++x) {
+                const int64_t g = (z * dims[1] + y) * dims[0] + x;
+                if (fluid[std::size_t(g)]) density.push_back(rho[std::size_t(g)]);
+                if (aperture && !fluid[std::size_t(g)]) continue;
+                vals.push_back(ux[std::size_t(g)]);
+            }
+    const int64_t x0p = setup.sample_begin, x1p = setup.sample_end - 1;
+    const double ubar = dolb::diag::tree_mean(vals);
+    const double rho_bar = density.empty() ? 1.0 : dolb::diag::tree_mean(density);
+    const double dp = (plane_mean(x0p, rho, dolb::D3Q19::cs2) - plane_mean(x1p, rho, dolb::D3Q19::cs2)) / rho_bar;
+    const double lx = double(x1p - x0p);
+    const double nu = cfg.viscosity();
+    out[4] = std::abs(dp) < 1e-300 ? 0.0 : dolb::diag::permeability(ubar, nu, lx, dp);
+    out[5] = ubar;
+    out[6] = dp;
+    out[7] = plane_mean(1, ux, 0.0);
+    out[8] = plane_mean(dims[0] - 2, ux, 0.0);
 }
 
 template <typename T>
@@ -251,6 +336,19 @@ __attribute__((visibility("default"))) int ref_case_dump(const RefCase* rc, int 
         if (precision_bits == 64) dump_case<double>(*rc, steps, path);
         else dump_case<float>(*rc, steps, path);
     });
+}
+
+__attribute__((visibility("default"))) int ref_case_sample(const RefCase* rc, int precision_bits,
+                                                           int64_t steps_a, int64_t steps_b,
+                                                           double* out) {
+    return guarded([&] {
+        if (precision_bits == 64) sample_case<double>(*rc, steps_a, steps_b, out);
+        else sample_case<float>(*rc, steps_a, steps_b, out);
+    });
+}
+
+__attribute__((visibility("default"))) int ref_tree_sum(const double* v, int64_t n, double* out) {
+    return guarded([&] { *out = dolb::diag::tree_sum(std::span<const double>(v, std::size_t(n))); });
 }
 
 __attribute__((visibility("default"))) int ref_case_bench(const RefCase* rc, int precision_bits,

@@ -64,6 +64,20 @@ class BlockView(C.Structure):
     ]
 
 
+class ReduceArgs(C.Structure):
+    _fields_ = [
+        ("quantity", C.c_int32), ("periodic", C.c_int32 * 3), ("x_begin", C.c_int64),
+        ("x_end", C.c_int64), ("halo_below", C.c_void_p), ("halo_above", C.c_void_p),
+    ]
+
+
+class TreePart(C.Structure):
+    _fields_ = [("lo", C.c_int64), ("len", C.c_int64), ("value", C.c_double)]
+
+
+Q_KINETIC, Q_ENSTROPHY, Q_DU_NUM, Q_DU_DEN = 0, 1, 2, 3
+Q_PRESSURE_FLUID, Q_UX_FLUID, Q_UX_ALL, Q_RHO_FLUID = 4, 5, 6, 7
+
 _lib = None
 
 _SIGS = {
@@ -95,6 +109,15 @@ _SIGS = {
     "dlb_lattice_traffic": ([C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int32)], C.c_int),
     "dlb_lattice_gather_macroscopic": ([C.c_void_p] * 5, C.c_int),
     "dlb_lattice_checksum": ([C.c_void_p, C.c_void_p], C.c_int),
+    "dlb_lattice_reduce_count": ([C.c_void_p, C.POINTER(ReduceArgs), C.POINTER(C.c_int64)], C.c_int),
+    "dlb_lattice_reduce_parts": ([C.c_void_p, C.POINTER(ReduceArgs), C.c_int64, C.c_int64, C.c_void_p,
+                                  C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
+    "dlb_lattice_reduce": ([C.c_void_p, C.POINTER(ReduceArgs), C.POINTER(C.c_double), C.POINTER(C.c_int64)], C.c_int),
+    "dlb_tree_combine": ([C.c_int64, C.c_void_p, C.c_size_t, C.POINTER(C.c_double)], C.c_int),
+    "dlb_tree_plan": ([C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
+    "dlb_tree_sum": ([C.c_void_p, C.c_int64, C.POINTER(C.c_double)], C.c_int),
+    "dlb_lattice_snapshot_velocity": ([C.c_void_p], C.c_int),
+    "dlb_lattice_velocity_planes": ([C.c_void_p, C.c_int32, C.c_int32, C.c_void_p], C.c_int),
     "dlb_lattice_step_bytes": ([C.c_void_p, C.POINTER(C.c_int64)], C.c_int),
     "dlb_lattice_time_steps": ([C.c_void_p, C.c_int64, C.POINTER(C.c_double)], C.c_int),
     "dlb_lattice_kernel_name": ([C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),

@@ -6,6 +6,9 @@ Translation units and their arithmetic flags:
                          reference CPU solver) and DLB_MODE=fast (-fmad=true)
   lattice.cu             -fmad=false (initialisation kernels restate the
                          reference's equilibrium / TGV arithmetic)
+  diag.cu                -fmad=false (diagnostic values and tree sums restate
+                         diagnostics.cpp / runner.cpp double arithmetic)
+  tree.cpp               host tree planning / combination
   capi.cu, chain.cpp     host code
 """
 from __future__ import annotations
@@ -26,14 +29,16 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC",
           "-Xcompiler", "-fvisibility=hidden", "-I", os.path.join(ROOT, "include")]
-HEADERS = ["lbm_cell.cuh", "kernels.cuh", "chain.hpp", "lattice.hpp"]
+HEADERS = ["lbm_cell.cuh", "kernels.cuh", "chain.hpp", "lattice.hpp", "canon.cuh", "tree.hpp"]
 
 UNITS = [
     # (source, object, extra flags)
     ("collide_stream.cu", "collide_stream_exact.o", ["-fmad=false", "-DDLB_MODE=exact"]),
     ("collide_stream.cu", "collide_stream_fast.o", ["-fmad=true", "-DDLB_MODE=fast"]),
     ("lattice.cu", "lattice.o", ["-fmad=false"]),
+    ("diag.cu", "diag.o", ["-fmad=false"]),
     ("capi.cu", "capi.o", ["-fmad=false"]),
+    ("tree.cpp", "tree.o", ["-x", "cu", "-fmad=false"]),
     ("chain.cpp", "chain.o", ["-x", "cu", "-fmad=false"]),
 ]
 

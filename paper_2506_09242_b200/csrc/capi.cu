@@ -12,6 +12,7 @@
 #include "../../include/dlb.h"
 #include "chain.hpp"
 #include "lattice.hpp"
+#include "tree.hpp"
 
 struct dlb_registry {
     dlb::DynamicsRegistry reg;
@@ -261,6 +262,95 @@ DLB_API dlb_status dlb_lattice_gather_macroscopic(dlb_lattice* lat, double* rho,
     DLB_REQUIRE(lat);
     DLB_REQUIRE(rho && ux && uy && uz);
     return guarded([&] { lat->lat->gather_macroscopic(rho, ux, uy, uz); });
+}
+
+DLB_API dlb_status dlb_lattice_reduce_count(dlb_lattice* lat, const dlb_reduce_args* args,
+                                            int64_t* count_out) {
+    DLB_REQUIRE(lat);
+    DLB_REQUIRE(args && count_out);
+    return guarded([&] { *count_out = lat->lat->reduce_count(*args); });
+}
+
+DLB_API dlb_status dlb_lattice_reduce_parts(dlb_lattice* lat, const dlb_reduce_args* args,
+                                            int64_t n_total, int64_t seg_begin,
+                                            dlb_tree_part* parts, size_t cap, size_t* n_out) {
+    DLB_REQUIRE(lat);
+    DLB_REQUIRE(args && n_out);
+    return guarded([&] {
+        std::vector<dlb_tree_part> out;
+        if (parts == nullptr) {  // size query: plan only (no device work)
+            const int64_t cnt = lat->lat->reduce_count(*args);
+            dlb::tree_plan(0, n_total, seg_begin, seg_begin + cnt, out);
+            // device chunks (>= 1 plane each) add at most 2 * depth + 16 parts per boundary
+            int depth = 1;
+            while ((int64_t(1) << depth) < n_total + 1) ++depth;
+            *n_out = out.size() + std::size_t(lat->lat->slab_planes()) * std::size_t(2 * depth + 16);
+            return;
+        }
+        lat->lat->reduce_parts(*args, n_total, seg_begin, out);
+        *n_out = out.size();
+        if (cap < out.size()) throw std::invalid_argument("parts buffer too small");
+        std::memcpy(parts, out.data(), out.size() * sizeof(dlb_tree_part));
+    });
+}
+
+DLB_API dlb_status dlb_lattice_reduce(dlb_lattice* lat, const dlb_reduce_args* args, double* sum_out,
+                                      int64_t* count_out) {
+    DLB_REQUIRE(lat);
+    DLB_REQUIRE(args && sum_out);
+    return guarded([&] {
+        const int64_t cnt = lat->lat->reduce_count(*args);
+        std::vector<dlb_tree_part> out;
+        lat->lat->reduce_parts(*args, cnt, 0, out);
+        *sum_out = dlb::tree_combine(cnt, out.data(), out.size());
+        if (count_out) *count_out = cnt;
+    });
+}
+
+DLB_API dlb_status dlb_tree_combine(int64_t n_total, const dlb_tree_part* parts, size_t n,
+                                    double* sum_out) {
+    DLB_REQUIRE(sum_out);
+    DLB_REQUIRE(parts || n == 0);
+    try {
+        *sum_out = dlb::tree_combine(n_total, parts, n);
+        return DLB_OK;
+    } catch (const std::invalid_argument& e) {
+        return fail(DLB_ERROR_INVALID_ARGUMENT, e.what());
+    } catch (const std::exception& e) {
+        return fail(DLB_ERROR_INTERNAL, e.what());
+    }
+}
+
+DLB_API dlb_status dlb_tree_plan(int64_t n_total, int64_t seg_begin, int64_t seg_end,
+                                 dlb_tree_part* parts, size_t cap, size_t* n_out) {
+    DLB_REQUIRE(n_out);
+    if (n_total < 0 || seg_begin < 0 || seg_end < seg_begin || seg_end > n_total)
+        return fail(DLB_ERROR_INVALID_ARGUMENT, "tree_plan: segment outside [0, n_total]");
+    return guarded([&] {
+        std::vector<dlb_tree_part> out;
+        dlb::tree_plan(0, n_total, seg_begin, seg_end, out);
+        *n_out = out.size();
+        if (parts == nullptr) return;
+        if (cap < out.size()) throw std::invalid_argument("parts buffer too small");
+        std::memcpy(parts, out.data(), out.size() * sizeof(dlb_tree_part));
+    });
+}
+
+DLB_API dlb_status dlb_tree_sum(const double* values, int64_t n, double* sum_out) {
+    DLB_REQUIRE(sum_out);
+    DLB_REQUIRE(values || n == 0);
+    return guarded([&] { *sum_out = dlb::tree_sum_host(values, n); });
+}
+
+DLB_API dlb_status dlb_lattice_snapshot_velocity(dlb_lattice* lat) {
+    DLB_REQUIRE(lat);
+    return guarded([&] { lat->lat->snapshot_velocity(); });
+}
+
+DLB_API dlb_status dlb_lattice_velocity_planes(dlb_lattice* lat, int32_t z0, int32_t nz, double* out) {
+    DLB_REQUIRE(lat);
+    DLB_REQUIRE(out);
+    return guarded([&] { lat->lat->velocity_planes(z0, nz, out); });
 }
 
 DLB_API dlb_status dlb_lattice_checksum(dlb_lattice* lat, uint64_t* per_direction) {

@@ -2,6 +2,7 @@
 // initialisation kernels evaluate equilibrium2<T> and the TGV state with the
 // reference's operation order (multiblock.cpp:278-281, cases.cpp:145-156).
 #include "lattice.hpp"
+#include "canon.cuh"
 
 #include <algorithm>
 #include <cmath>
@@ -37,17 +38,6 @@ constexpr int kCy27[27] = {0, 0, 0, -1, 1, 0, 0, -1, 1, 1, -1, 0, 0, 0, 0, -1, 1
 template <typename T>
 __device__ __forceinline__ long long lin(const Geo& g, int x, int y, int z) {
     return static_cast<long long>(z) * g.plane + static_cast<long long>(y) * g.pitch + x;
-}
-
-// Position of canonical f_i(x, y, z) in the AA array after an odd step /
-// at upload: A[i][x + c_i] (wrapped on periodic axes, envelope otherwise).
-__device__ __forceinline__ long long shifted(const Geo& g, int x, int y, int z, int cx, int cy,
-                                             int cz) {
-    int X = x + cx, Y = y + cy, Z = z + cz;
-    if (g.per_x) X = X < 0 ? X + g.nx : (X >= g.nx ? X - g.nx : X);
-    if (g.per_y) Y = Y < 0 ? Y + g.ny : (Y >= g.ny ? Y - g.ny : Y);
-    if (g.per_z) Z = Z < 0 ? Z + g.nz : (Z >= g.nz ? Z - g.nz : Z);
-    return static_cast<long long>(Z) * g.plane + static_cast<long long>(Y) * g.pitch + X;
 }
 
 template <int Q, int i>
@@ -185,22 +175,6 @@ __global__ void k_checksum(const T* origin0, Geo g, int aa_mode, long long z_ori
         if ((threadIdx.x & 31) == 0) atomicAdd(out + i, v);
     }
 }
-
-// Canonical f_i(x, y, z) of the current state for any layout
-// (aa_mode: 0 two-population, 1 AA even layout, 2 AA odd layout).
-template <typename T, int Q, int i>
-__device__ __forceinline__ T canon_load(const T* origin0, const Geo& g, int x, int y, int z, int aa_mode) {
-    using L = Lat<Q>;
-    constexpr int cx = L::c[i][0], cy = L::c[i][1], cz = L::c[i][2];
-    if (aa_mode == 2) return origin0[i * g.dstride + shifted(g, x, y, z, cx, cy, cz)];
-    const long long at = static_cast<long long>(z) * g.plane + static_cast<long long>(y) * g.pitch + x;
-    return origin0[(aa_mode == 1 ? opp_of(i) : i) * g.dstride + at];
-}
-
-struct MacroSlot {
-    int kind;
-    double uw[3];
-};
 
 // MultiBlockRun::gather_macroscopic (multiblock.cpp:443-484): populations
 // converted to double; Collide cells report compute_rho_u, moving walls their
@@ -416,6 +390,8 @@ Lattice::~Lattice() {
     cudaFree(d_counter_);
     cudaFree(staging_);
     cudaFree(blk_out_);
+    cudaFree(d_uprev_);
+    cudaFree(diag_buf_);
     for (cudaEvent_t e : blk_ev_) cudaEventDestroy(e);
     if (copy_stream_) cudaStreamDestroy(copy_stream_);
     if (h2d_stream_) cudaStreamDestroy(h2d_stream_);

@@ -81,10 +81,19 @@ class Lattice {
         if (kernel_main_ && !fixups_.empty() && !(lower_.linked || upper_.linked)) return kernel_main_->name;
         return kernel_ ? kernel_->name : "<none>";
     }
+    int slab_planes() const { return d_.dims[2]; }
     int64_t cells() const { return int64_t(d_.dims[0]) * d_.dims[1] * d_.dims[2]; }
     int bits() const { return d_.precision_bits; }
     int q() const { return d_.q; }
     void set_periodic_override(bool x, bool y, bool z);
+
+    // GPU-resident diagnostics (diag.cu): split deterministic tree reductions
+    // of per-cell quantities of the current state (include/dlb.h).
+    int64_t reduce_count(const dlb_reduce_args& a) const;
+    void reduce_parts(const dlb_reduce_args& a, int64_t n_total, int64_t seg_begin,
+                      std::vector<dlb_tree_part>& out);
+    void snapshot_velocity();
+    void velocity_planes(int z0, int nz, double* out);
 
   private:
     void select_kernel();
@@ -177,6 +186,17 @@ class Lattice {
     void fill_recipes(StepArgs<T>& a) const;
     template <typename T>
     void launch_host_block(void* f_in, const int64_t ext[3]);
+    // diagnostics state (diag.cu)
+    double* d_uprev_ = nullptr;  // velocity snapshot [ux | uy | uz] x cells
+    void* diag_buf_ = nullptr;
+    std::size_t diag_bytes_ = 0;
+    void* diag_scratch(std::size_t min_bytes);
+    template <typename T>
+    void diag_impl(const dlb_reduce_args& a, int64_t n_total, int64_t seg_begin,
+                   std::vector<dlb_tree_part>& out);
+    template <typename T>
+    void velocity_planes_impl(int z0, int nz, double* dev_out);
+    void* diag_slots();  // per-slot kind / fluid flag / wall velocity on the device
 };
 
 // Sphere-pack porous medium generator (cases.cpp raw voxel format).

@@ -536,6 +536,142 @@ class DeviceRun:
             fh.write(struct.pack("<BI3Q", self.precision // 8, self.q, *self.dims))
             fh.write(raw.tobytes())
 
+    # -- GPU-resident diagnostics (runner.cpp:346-448, diagnostics.cpp:10-131) --
+    def _all_gather(self, obj):
+        if self.dist is None or self.dist[1] == 1:
+            return [obj]
+        import torch.distributed as dist
+        out = [None] * self.dist[1]
+        dist.all_gather_object(out, obj)
+        return out
+
+    def _args(self, quantity, x_range=None, halos=(None, None)):
+        a = _capi.ReduceArgs()
+        a.quantity = quantity
+        for ax in range(3):
+            a.periodic[ax] = self.periodic[ax]
+        a.x_begin, a.x_end = x_range if x_range is not None else (0, self.dims[0])
+        a.halo_below = halos[0].ctypes.data if halos[0] is not None else None
+        a.halo_above = halos[1].ctypes.data if halos[1] is not None else None
+        return a
+
+    def velocity_planes(self, z0: int, nz: int, k: int = 0) -> np.ndarray:
+        """(nz, 3, ny, nx) velocity of local planes [z0, z0 + nz) of slab k."""
+        out = np.zeros((nz, 3, self.dims[1], self.dims[0]))
+        check(_capi.lib().dlb_lattice_velocity_planes(self.slabs[k].handle, z0, nz, out.ctypes.data))
+        return out
+
+    def _enstrophy_halos(self):
+        """Per local slab: the 4 global velocity planes below and above it
+        (the FD8 stencil's reach), gathered from the slabs that own them."""
+        nz_g = self.dims[2]
+        if len(self.parts) == 1:
+            return [(None, None)]
+        # every slab publishes its (up to) 4 bottom and 4 top planes
+        mine = {}
+        for k in range(len(self.slabs)):
+            z0, nz = self._slab_range(k)
+            want = sorted(set(list(range(min(4, nz))) + list(range(max(0, nz - 4), nz))))
+            planes = self.velocity_planes(want[0], want[-1] - want[0] + 1, k) if want else None
+            for j in want:
+                mine[z0 + j] = planes[j - want[0]]
+        have = {}
+        for d in self._all_gather(mine):
+            have.update(d)
+        zero = np.zeros((3, self.dims[1], self.dims[0]))
+        out = []
+        for k in range(len(self.slabs)):
+            z0, nz = self._slab_range(k)
+
+            def block(zs):
+                rows = []
+                for zg in zs:
+                    if not self.periodic[2] and not 0 <= zg < nz_g:
+                        rows.append(zero)
+                        continue
+                    rows.append(have[zg % nz_g])
+                return np.ascontiguousarray(np.stack(rows))
+            out.append((block(range(z0 - 4, z0)), block(range(z0 + nz, z0 + nz + 4))))
+        return out
+
+    def tree_reduce(self, quantity: int, x_range=None):
+        """(tree_sum, count) of a quantity's value sequence over the whole
+        (possibly decomposed) domain, bit-identical to diag::tree_sum over the
+        vector the reference's runner builds."""
+        halos = self._enstrophy_halos() if quantity == _capi.Q_ENSTROPHY else [(None, None)] * len(self.slabs)
+        args = [self._args(quantity, x_range, halos[k]) for k in range(len(self.slabs))]
+        counts = []
+        for k, s in enumerate(self.slabs):
+            c = C.c_int64()
+            check(_capi.lib().dlb_lattice_reduce_count(s.handle, C.byref(args[k]), C.byref(c)))
+            counts.append((self.ranks[k], c.value))
+        allc = sorted(c for part in self._all_gather(counts) for c in part)
+        n_total = sum(c for _, c in allc)
+        begin = {}
+        acc = 0
+        for r, c in allc:
+            begin[r] = acc
+            acc += c
+        parts = []
+        for k, s in enumerate(self.slabs):
+            n = C.c_size_t()
+            check(_capi.lib().dlb_lattice_reduce_parts(s.handle, C.byref(args[k]), n_total, begin[self.ranks[k]],
+                                                       None, 0, C.byref(n)))
+            buf = (_capi.TreePart * max(n.value, 1))()
+            check(_capi.lib().dlb_lattice_reduce_parts(s.handle, C.byref(args[k]), n_total, begin[self.ranks[k]],
+                                                       buf, n.value, C.byref(n)))
+            parts.extend((p.lo, p.len, p.value) for p in buf[:n.value])
+        allp = [p for part in self._all_gather(parts) for p in part]
+        arr = (_capi.TreePart * max(len(allp), 1))(*[_capi.TreePart(*p) for p in allp])
+        out = C.c_double()
+        check(_capi.lib().dlb_tree_combine(n_total, arr, len(allp), C.byref(out)))
+        return out.value, n_total
+
+    def _tree_mean(self, quantity, x_range=None, empty=None):
+        s, n = self.tree_reduce(quantity, x_range)
+        if n == 0:
+            if empty is None:
+                raise ValueError("mean of an empty set")  # diagnostics.cpp:21
+            return empty
+        return s / float(n)
+
+    def kinetic_energy(self) -> float:
+        """diag::kinetic_energy of the gathered velocity (diagnostics.cpp:25-31)."""
+        return self._tree_mean(_capi.Q_KINETIC)
+
+    def enstrophy(self) -> float:
+        """diag::enstrophy(diag::vorticity_fd8(u, periodic)) (diagnostics.cpp:65-120)."""
+        return self._tree_mean(_capi.Q_ENSTROPHY)
+
+    def snapshot_velocity(self):
+        """Keep the current velocity on the device (the runner's prev_u, runner.cpp:445-448)."""
+        for s in self.slabs:
+            check(_capi.lib().dlb_lattice_snapshot_velocity(s.handle))
+
+    def convergence_sums(self):
+        """(tree_sum |u - u_prev|^2, tree_sum |u|^2) against the last snapshot (runner.cpp:433-444)."""
+        return self.tree_reduce(_capi.Q_DU_NUM)[0], self.tree_reduce(_capi.Q_DU_DEN)[0]
+
+    def porous_extras(self, sample_begin: int, sample_end: int, nu: float, aperture_mean: bool = False):
+        """Driver::porous_extras (runner.cpp:346-399): [k_perm, ubar, dp, ux_in, ux_out]."""
+        x0, x1 = sample_begin, sample_end - 1
+
+        def plane_mean_p(x):
+            return self._tree_mean(_capi.Q_PRESSURE_FLUID, (x, x + 1), empty=0.0)
+
+        def plane_mean_ux(x):
+            return self._tree_mean(_capi.Q_UX_FLUID, (x, x + 1), empty=0.0)
+        win = (sample_begin, sample_end)
+        ubar = self._tree_mean(_capi.Q_UX_FLUID if aperture_mean else _capi.Q_UX_ALL, win)
+        rho_bar = self._tree_mean(_capi.Q_RHO_FLUID, win, empty=1.0)
+        dp = (plane_mean_p(x0) - plane_mean_p(x1)) / rho_bar
+        lx = float(x1 - x0)
+        if abs(dp) < 1e-300:
+            k_perm = 0.0
+        else:
+            k_perm = ubar * nu * lx / dp  # diag::permeability (diagnostics.cpp:122-127)
+        return [k_perm, ubar, dp, plane_mean_ux(1), plane_mean_ux(self.dims[0] - 2)]
+
     def gather_raw(self) -> np.ndarray:
         """Like gather_populations but in the storage precision."""
         dt = np.float64 if self.precision == 64 else np.float32

@@ -68,3 +68,19 @@ FULL_CASES = {
     "cavity64_bgk_f64_c1_full": dict(kind="cavity", L=64, Re=1000.0, Ma=0.1, collision=BGK, bits=64,
                                      steps=1000, workers=8),
 }
+
+# Sampling-step goldens (runner.cpp:346-448 on the reference's own fields):
+# case name -> (steps before the velocity snapshot, steps after it).
+DIAG_CASES = {
+    "tgv16_bgk_f64": (5, 5),
+    "tgv12_bgk_f32": (3, 2),
+    "tgv32_rr_f64": (25, 25),
+    "tgv24_smag_trt_f32": (20, 20),
+    "tgv128_bgk_f32_c5": (50, 50),
+    "cavity64_bgk_f64_c1": (500, 500),
+    "cavity32_trt_f32": (100, 100),
+    "cavity24_rr_f64": (50, 50),
+    "plates16_trt_vel_f64": (100, 100),
+    "plates16_trt_pres_f32": (100, 100),
+    "sphere48_trt_f64_c4": (100, 100),
+}

@@ -3,7 +3,9 @@
 Run in the build container (needs oracle/_ref/libdolb_refshim.so, built from
 /root/reference/proj by `make -C oracle ref`):
 
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py          # golden.json
+    python tests/golden/make_golden.py --full   # golden_full.json (full-size checksums)
+    python tests/golden/make_golden.py --diag   # golden_diag.json (sampling step)
 
 Each entry records the reference's gather_populations() after `steps` steps
 (MultiBlockRun<T>, 8 workers x z-blocks — decomposition does not change the
@@ -24,7 +26,7 @@ ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
 sys.path.insert(0, HERE)
 from pyoracle import Reference, canonical_checksum, canonical_hash  # noqa: E402
-from golden_cases import CASES, FULL_CASES, make_case  # noqa: E402
+from golden_cases import CASES, DIAG_CASES, FULL_CASES, make_case  # noqa: E402
 
 
 def full():
@@ -46,9 +48,27 @@ def full():
             json.dump(out, f, indent=1)
 
 
+def diag():
+    """Sampling-step values (kinetic energy, enstrophy, cavity convergence sums,
+    porous permeability extras) of the reference's runner arithmetic on its own
+    gathered fields, stored as exact float hex strings."""
+    ref = Reference()
+    out = {}
+    for name, (a, b) in DIAG_CASES.items():
+        spec = CASES[name]
+        t = time.time()
+        vals = ref.sample(make_case(spec), spec["bits"], a, b)
+        out[name] = {"steps": [a, b], "values": {k: float(v).hex() for k, v in vals.items()}}
+        print(f"{name}: {time.time() - t:.1f}s k={vals['k']:.6g} eps={vals['eps']:.6g}", flush=True)
+    with open(os.path.join(HERE, "golden_diag.json"), "w") as f:
+        json.dump(out, f, indent=1)
+
+
 def main():
     if "--full" in sys.argv:
         return full()
+    if "--diag" in sys.argv:
+        return diag()
     ref = Reference()
     out = {}
     for name, spec in CASES.items():
