@@ -965,31 +965,32 @@ void Lattice::launch_host_block(void* f_in, const int64_t ext[3]) {
     const int by = 256 / bx;
     const dim3 block(bx, by, 1);
     const unsigned gx = unsigned((hg.nx + bx - 1) / bx), gy = unsigned((hg.ny + by - 1) / by);
-    const int zc = std::max(1, (hg.nz + 15) / 16);
+    // 32 z-chunks (2-D copies keep the per-chunk cost low; shorter fill / drain), >= 1 plane each
+    static const int kChunks = [] {
+        const char* e = std::getenv("DLB_BLOCK_CHUNKS");
+        return e ? std::max(1, std::atoi(e)) : 32;
+    }();
+    const int zc = std::max(1, (hg.nz + kChunks - 1) / kChunks);
     const int nchunks = (hg.nz + zc - 1) / zc;
     while (int(blk_ev_.size()) < 2 * nchunks) {
         cudaEvent_t e;
         cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
         blk_ev_.push_back(e);
     }
-    const std::size_t plane_bytes = std::size_t(hg.plane) * sizeof(T);
-    auto copy_planes = [&](cudaStream_t st, bool up, int p0, int p1) {  // host plane indices [p0, p1)
-        if (p1 <= p0) return;
-        for (int i = 0; i < d_.q; ++i) {
-            const std::size_t off = (std::size_t(i) * vol + std::size_t(p0) * hg.plane) * sizeof(T);
-            char* h = static_cast<char*>(f_in) + off;
-            char* d = reinterpret_cast<char*>(up ? din : dout) + off;
-            cuda_check(cudaMemcpyAsync(up ? d : h, up ? h : d, std::size_t(p1 - p0) * plane_bytes,
-                                       up ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, st),
-                       up ? "h2d" : "d2h");
-        }
-    };
-    int loaded = 0;   // host planes [0, loaded) are on the device
-    int written = 1;  // host planes [1, written) copied back (plane 0 is envelope)
+    blk_.f_in = f_in;
+    blk_.vol = vol;
+    blk_.plane = hg.plane;
+    blk_.nz = hg.nz;
+    blk_.zc = zc;
+    blk_.nchunks = nchunks;
+    blk_.elem = int(sizeof(T));
+    blk_.dout = dout;
+    blk_.pending = true;
+    int loaded = 0;  // host planes [0, loaded) are on the device
     for (int c = 0; c < nchunks; ++c) {
         const int z0 = c * zc, z1 = std::min(hg.nz, z0 + zc);
         // chunk [z0, z1) reads host planes [z0, z1 + 2)
-        copy_planes(h2d_stream_, true, loaded, z1 + 2);
+        block_copy(h2d_stream_, din, true, loaded, z1 + 2);
         loaded = z1 + 2;
         cuda_check(cudaEventRecord(blk_ev_[2 * c], h2d_stream_), "event");
         cuda_check(cudaStreamWaitEvent(stream_, blk_ev_[2 * c], 0), "wait");
@@ -998,22 +999,71 @@ void Lattice::launch_host_block(void* f_in, const int64_t ext[3]) {
         void* args[] = {&a};
         cuda_check(cudaLaunchKernel(kernel_->fn, dim3(gx, gy, z1 - z0), block, args, 0, stream_), "launch");
         cuda_check(cudaEventRecord(blk_ev_[2 * c + 1], stream_), "event");
-        // the old interior planes z < z1 are no longer read once the host
-        // copy of them is on the device, so finished planes can go back
+    }
+}
+
+// One direction-strided copy of host planes [p0, p1) between the caller's block
+// and a device mirror (the same envelope-inclusive layout).
+void Lattice::block_copy(cudaStream_t st, void* dev, bool up, int p0, int p1) {
+    if (p1 <= p0) return;
+    const std::size_t plane_bytes = std::size_t(blk_.plane) * blk_.elem;
+    {
+        // all q direction arrays in one 2-D copy (rows = directions, pitch = one array)
+        const std::size_t off = std::size_t(p0) * blk_.plane * blk_.elem;
+        const std::size_t pitch = std::size_t(blk_.vol) * blk_.elem;
+        char* h = static_cast<char*>(blk_.f_in) + off;
+        char* d = static_cast<char*>(dev) + off;
+        const cudaError_t e = cudaMemcpy2DAsync(up ? d : h, pitch, up ? h : d, pitch, std::size_t(p1 - p0) * plane_bytes,
+                                                d_.q, up ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) return;
+        cudaGetLastError();  // pitch beyond the 2-D copy limit: one copy per direction
+    }
+    for (int i = 0; i < d_.q; ++i) {
+        const std::size_t off = (std::size_t(i) * blk_.vol + std::size_t(p0) * blk_.plane) * blk_.elem;
+        char* h = static_cast<char*>(blk_.f_in) + off;
+        char* d = static_cast<char*>(dev) + off;
+        cuda_check(cudaMemcpyAsync(up ? d : h, up ? h : d, std::size_t(p1 - p0) * plane_bytes,
+                                   up ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, st),
+                   up ? "h2d" : "d2h");
+    }
+}
+
+void Lattice::begin_host_block(void* f_in, const int64_t ext[3]) {
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    if (aa()) throw std::invalid_argument("host-block stepping uses the two-population layout");
+    if (blk_.pending) abort_host_block();
+    if (d_.precision_bits == 64) launch_host_block<double>(f_in, ext);
+    else launch_host_block<float>(f_in, ext);
+}
+
+// Copy-back: finished planes go back as soon as their chunk is computed (the
+// old interior planes z < z1 are no longer read once the host copy of them is
+// on the device), on a second copy engine, overlapping the remaining H2D.
+void Lattice::finish_host_block() {
+    if (!blk_.pending) throw std::logic_error("finish_host_block without begin_host_block");
+    int written = 1;  // host planes [1, written) copied back (plane 0 is envelope)
+    for (int c = 0; c < blk_.nchunks; ++c) {
+        const int z1 = std::min(blk_.nz, (c + 1) * blk_.zc);
         cuda_check(cudaStreamWaitEvent(copy_stream_, blk_ev_[2 * c + 1], 0), "wait");
-        copy_planes(copy_stream_, false, written, z1 + 1);
+        block_copy(copy_stream_, blk_.dout, false, written, z1 + 1);
         written = z1 + 1;
     }
+    blk_.pending = false;
     cuda_check(cudaStreamSynchronize(copy_stream_), "block copy-back");
     cuda_check(cudaStreamSynchronize(stream_), "block step");
+    ++steps_;
+}
+
+// Drop a begun step: nothing was written to the caller's block.
+void Lattice::abort_host_block() {
+    blk_.pending = false;
+    cuda_check(cudaStreamSynchronize(h2d_stream_), "block abort");
+    cuda_check(cudaStreamSynchronize(stream_), "block abort");
 }
 
 void Lattice::step_host_block(void* f_in, const int64_t ext[3]) {
-    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
-    if (aa()) throw std::invalid_argument("host-block stepping uses the two-population layout");
-    if (d_.precision_bits == 64) launch_host_block<double>(f_in, ext);
-    else launch_host_block<float>(f_in, ext);
-    ++steps_;
+    begin_host_block(f_in, ext);
+    finish_host_block();
 }
 
 template <typename T>

@@ -57,6 +57,13 @@ class Lattice {
     // copies of the next chunk, the step of this chunk and device->host copies
     // of the previous one run concurrently (both PCIe directions busy).
     void step_host_block(void* f_in, const int64_t ext[3]);
+    // The same in two halves: begin enqueues every H2D chunk and its compute
+    // (device-side writes only), finish enqueues the copy-back into the
+    // caller's block; abort drops a begun step. Lets the caller's eager
+    // dispatch scan overlap the transfers while still failing before any write.
+    void begin_host_block(void* f_in, const int64_t ext[3]);
+    void finish_host_block();
+    void abort_host_block();
     void step(int64_t nsteps);
     void enqueue_step();  // one step, no dispatch check (group stepping)
     void check_dispatch() const;
@@ -182,6 +189,14 @@ class Lattice {
     cudaStream_t copy_stream_ = nullptr;
     cudaStream_t h2d_stream_ = nullptr;
     std::vector<cudaEvent_t> blk_ev_;
+    struct BlockPlan {
+        void* f_in = nullptr;
+        void* dout = nullptr;
+        long long vol = 0;
+        int plane = 0, nz = 0, zc = 1, nchunks = 0, elem = 4;
+        bool pending = false;
+    } blk_;
+    void block_copy(cudaStream_t st, void* dev, bool up, int p0, int p1);
     template <typename T>
     void fill_recipes(StepArgs<T>& a) const;
     template <typename T>

@@ -245,6 +245,53 @@ def test_host_block_collide_and_stream_dropin(oracle):
         _capi.lib().dlb_host_free(p)
 
 
+def test_host_block_speculative_pipeline(oracle):
+    """Pinned block, cached device lattice: the copies + step start while the
+    eager tag scan runs. A dispatch error must still leave the block untouched,
+    and a param_index change must recompute with the new slots."""
+    import ctypes as C
+    from paper_2506_09242_b200 import _capi
+    n = 16
+    case = Case(kind="cavity", L=n, Re=100.0, Ma=0.1, collision=TRT)
+    dims, per, rec, slot = case.setup()
+    f = oracle.initial_state(case, np.float64)
+    bulk_only = np.zeros_like(slot)
+    want = oracle.step(19, dims, per, rec, slot, f.copy(), 2)
+    want = oracle.step(19, dims, per, rec, bulk_only, want, 1)   # param_index changed
+    want = oracle.step(19, dims, per, rec, slot, want, 1)        # and back
+    reg = dlb.DynamicsRegistry()
+    setup = dlb.init_cavity(dlb.CaseConfig(kind="cavity", L=n, Re=100.0, Ma=0.1, collision=LinkType.TRT))
+    slots = np.asarray([reg.register_chain(ch) for ch in setup.chains], np.int32)
+
+    def tags_of(idx):
+        tag = np.full((n + 2,) * 3, -1, np.int32)
+        pidx = np.full((n + 2,) * 3, -1, np.int32)
+        pidx[1:-1, 1:-1, 1:-1] = slots[idx]
+        tag[1:-1, 1:-1, 1:-1] = np.vectorize(reg.tag_of_slot)(slots[idx])
+        return tag, pidx
+    real, bulk = tags_of(setup.chain_index), tags_of(np.zeros_like(setup.chain_index))
+    p = C.c_void_p()
+    nbytes = 19 * (n + 2) ** 3 * 8
+    _capi.check(_capi.lib().dlb_host_alloc(nbytes, C.byref(p)))
+    try:
+        pin = np.ctypeslib.as_array((C.c_uint8 * nbytes).from_address(p.value)).view(np.float64)
+        pin = pin.reshape(19, n + 2, n + 2, n + 2)
+        pin[:] = 0
+        pin[:, 1:-1, 1:-1, 1:-1] = f.reshape(19, n, n, n)
+        alld = dlb.DispatchSet.all_of(reg)
+        for _ in range(2):
+            dlb.collide_and_stream(reg, pin, *real, alld)
+        before = pin.copy()
+        with pytest.raises(dlb.DispatchError):  # speculative start, then the verdict
+            dlb.collide_and_stream(reg, pin, *real, dlb.DispatchSet.from_strings(reg, [setup.chains[0].chain_string()]))
+        assert np.array_equal(pin, before)
+        dlb.collide_and_stream(reg, pin, *bulk, alld)
+        dlb.collide_and_stream(reg, pin, *real, alld)
+        assert np.array_equal(pin[:, 1:-1, 1:-1, 1:-1].reshape(-1), want)
+    finally:
+        _capi.lib().dlb_host_free(p)
+
+
 def test_mass_conservation_long_run():
     """Periodic TGV: total mass drift <= 1e-12 relative over 1000 steps (acceptance.cpp:133-175)."""
     setup, _, _ = product_setup(dict(kind="tgv", L=32, Re=100.0, Ma=0.1, collision=BGK, bits=64, steps=0))
