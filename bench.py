@@ -222,8 +222,10 @@ def main():
     ap.add_argument("--layout", default="twopop", choices=["twopop", "aa"])
     ap.add_argument("--tma", action="store_true", help="TMA-staged dense kernel instead of the plain-load one")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--sparse", action="store_true",
-                    help="c4: kind-sorted sparse lists (NoDynamics skipped) instead of the dense sweep")
+    ap.add_argument("--porous", default="masked", choices=["dense", "masked", "lists"],
+                    help="c4 kernel variant: dense sweep of every cell (reference behaviour), masked "
+                         "sweep (NoDynamics segments skipped), or kind-sorted sparse lists")
+    ap.add_argument("--sparse", action="store_true", help="alias of --porous lists")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
 
@@ -258,11 +260,15 @@ def main():
         vox, phi = dlb.sphere_pack((L, L, L), radius=8.0, porosity=0.20, seed=20250611)
         setup = dlb.init_porous(cfg, solid=(vox == 255))
         kinds = np.bincount(np.asarray(setup.chain_index).reshape(-1), minlength=5)
-        skip = args.sparse
+        variant = "lists" if args.sparse else args.porous
+        skip = variant != "dense"
         extra = {"porosity": phi, "fluid_cells": int(kinds[0] + kinds[3] + kinds[4]),
                  "bounce_back_cells": int(kinds[1]), "no_dynamics_cells": int(kinds[2]),
-                 "variant": "sparse kind-sorted lists" if args.sparse else
-                 "dense sweep (regularized planes recomputed by list launches)"}
+                 "variant": {"lists": "sparse kind-sorted lists (NoDynamics not listed)",
+                             "masked": "masked sweep: all-NoDynamics 32-B segments neither loaded nor "
+                                       "stored (regularized planes recomputed by list launches)",
+                             "dense": "dense sweep of every cell (regularized planes recomputed by "
+                                      "list launches)"}[variant]}
         del vox
     else:
         cfg = dlb.CaseConfig(kind=kind, L=L, Re=Re, Ma=Ma, collision=lt, q=q)
@@ -270,7 +276,8 @@ def main():
     layout = args.layout if world == 1 else "twopop"  # AA runs single-slab lattices
     run = dlb.build_run(setup, precision=bits, arith=args.arith,
                         dist=(rank, world) if world > 1 else None, devices=[local], layout=layout,
-                        skip_nodynamics=skip, tma=args.tma)
+                        skip_nodynamics=skip, tma=args.tma,
+                        sparse_lists=kind == "porous" and variant == "lists")
     cells_total = run.num_cells()
     bpc, dev_bytes, launches = run.traffic()
     kernel = run.kernel_name()

@@ -94,18 +94,24 @@ typedef struct dlb_lattice_desc {
     int32_t reserved;
 } dlb_lattice_desc;
 
-/* Sparse porous variant: cells whose dynamics is NoDynamics are neither loaded
- * nor stored and wall cells move only the links that feed fluid cells (their
- * other values are never consumed by a fluid cell, so every Collide-kind cell
- * stays bit-identical to the reference). Single-slab lattices
- * use per-slot cell lists (one launch per dynamics kind); z-slabs use the
- * masked dense sweep. */
+/* Masked porous variant: NoDynamics cells are neither loaded nor stored, at the
+ * granularity of x-aligned groups of one 32-B segment per direction array (a
+ * group moves nothing only when all its cells are NoDynamics; the NoDynamics
+ * cells of a mixed group run their dense update). The skipped values are never
+ * consumed by a fluid cell, so every Collide-kind cell stays bit-identical to
+ * the reference. Works on single slabs and z-slabs. */
 #define DLB_FLAG_SKIP_NODYNAMICS 1
 /* Use the TMA-staged dense kernel (warp-specialised producer, q 4-D tensor box
  * loads per tile into an mbarrier ring) for single-slab two-population
  * lattices. Opt-in: on B200 it reaches 0.58-0.74 of the copy roofline against
  * 0.94-0.99 for the default plain-load kernel (profiles/r01_summary.md). */
 #define DLB_FLAG_TMA 2
+/* Sparse porous variant (single slab): per-slot, row-major cell lists, one
+ * launch per dynamics kind; NoDynamics cells are not listed and wall cells
+ * move only the links that feed fluid cells. Implies the masked sweep where
+ * lists do not apply (z-slabs, AA). Slower than the masked sweep on B200
+ * (profiles/r01_summary.md): kept for comparison. */
+#define DLB_FLAG_SPARSE_LISTS 4
 
 DLB_API dlb_status dlb_lattice_create(const dlb_lattice_desc* desc, const dlb_registry* reg,
                                       dlb_lattice** out);

@@ -54,6 +54,7 @@ class LatticeDesc(C.Structure):
 
 FLAG_SKIP_NODYNAMICS = 1
 FLAG_TMA = 2
+FLAG_SPARSE_LISTS = 4
 
 
 class BlockView(C.Structure):

@@ -212,14 +212,14 @@ def init_porous(cfg: CaseConfig, solid: np.ndarray | None = None) -> CaseSetup:
 def build_run(setup: CaseSetup, registry: DynamicsRegistry | None = None, precision: int = 64,
               slabs: int = 1, dispatch: DispatchSet | None = None, arith: str = "exact",
               dist=None, devices=None, layout: str = "twopop",
-              skip_nodynamics: bool = False, tma: bool = False) -> DeviceRun:
+              skip_nodynamics: bool = False, tma: bool = False, sparse_lists: bool = False) -> DeviceRun:
     """Register the setup's chains, build the device run, fill tags and state
     (cases.cpp:279-297 + multiblock.cpp:252-287)."""
     registry = registry or DynamicsRegistry()
     slot_of = [registry.register_chain(ch) for ch in setup.chains]
     run = DeviceRun(setup.dims, setup.periodic, registry, dispatch, q=setup.q, precision=precision,
                     slabs=slabs, arith=arith, dist=dist, devices=devices, layout=layout,
-                    skip_nodynamics=skip_nodynamics, tma=tma)
+                    skip_nodynamics=skip_nodynamics, tma=tma, sparse_lists=sparse_lists)
     if np.isscalar(setup.chain_index):
         slots = slot_of[int(setup.chain_index)]
     else:

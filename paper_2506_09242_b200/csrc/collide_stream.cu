@@ -33,6 +33,60 @@ constexpr int min_blocks() {
     return heavy ? 2 : 3;
 }
 
+// One cell of the two-population pull step: gather f_i(x) <- f_i(x - c_i)
+// from the input buffer (periodic axes wrap in-kernel, non-periodic faces
+// read the zero envelope / ghost planes), apply the slot's dynamics, store to
+// the output buffer, and push the z-crossing links into the neighbours' ghost
+// planes when the slab is linked. READ_SLOT: look the slot up here (after the
+// loads, so the slot read overlaps them); otherwise `s` is already known.
+template <typename T, int Q, unsigned KM, bool READ_SLOT>
+__device__ __forceinline__ void cell_update(const StepArgs<T>& a, int x, int y, int z, int s) {
+    using L = Lat<Q>;
+    const Geo& g = a.g;
+    const int xm = (x == 0 && g.per_x) ? g.nx - 1 : x - 1;
+    const int xp = (x == g.nx - 1 && g.per_x) ? 0 : x + 1;
+    const int ym = (y == 0 && g.per_y) ? g.ny - 1 : y - 1;
+    const int yp = (y == g.ny - 1 && g.per_y) ? 0 : y + 1;
+    const int zm = (z == 0 && g.per_z) ? g.nz - 1 : z - 1;
+    const int zp = (z == g.nz - 1 && g.per_z) ? 0 : z + 1;
+
+    T f[Q];
+    sfor<Q>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        constexpr int cx = L::c[i][0], cy = L::c[i][1], cz = L::c[i][2];
+        const int sx = cx > 0 ? xm : (cx < 0 ? xp : x);
+        const int sy = cy > 0 ? ym : (cy < 0 ? yp : y);
+        const int sz = cz > 0 ? zm : (cz < 0 ? zp : z);
+        f[i] = __ldg(a.fin[i] + (sz * g.plane + sy * g.pitch + sx));
+    });
+
+    if constexpr (READ_SLOT) {
+        if (a.slot != nullptr) s = a.slot[(static_cast<long long>(z) * g.ny + y) * g.nx + x];
+    }
+    Cell<T, Q>::template apply<KM>(f, a.rec[s]);
+
+    const int center = z * g.plane + y * g.pitch + x;
+    sfor<Q>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        a.fout[i][center] = f[i];
+    });
+
+    if (a.push_up != nullptr && z == g.nz - 1) {
+        const int ghost = -g.plane + y * g.pitch + x;
+        sfor<Q>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            if constexpr (L::c[i][2] > 0) a.push_up[i * a.up_dstride + ghost] = f[i];
+        });
+    }
+    if (a.push_down != nullptr && z == 0) {
+        const int ghost = a.down_ghost_z * g.plane + y * g.pitch + x;
+        sfor<Q>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            if constexpr (L::c[i][2] < 0) a.push_down[i * a.down_dstride + ghost] = f[i];
+        });
+    }
+}
+
 template <typename T, int Q, unsigned KM>
 __global__ void __launch_bounds__(256, (min_blocks<T, Q, KM>())) k_pull(const __grid_constant__ StepArgs<T> a) {
     using L = Lat<Q>;
@@ -45,57 +99,26 @@ __global__ void __launch_bounds__(256, (min_blocks<T, Q, KM>())) k_pull(const __
     if constexpr ((KM & KM_SKIP) != 0) {
         // masked porous variant: NoDynamics cells (solids without a fluid
         // neighbour, cases.cpp:239-249) are neither loaded nor stored; their
-        // values are never consumed by a fluid cell.
+        // values are never consumed by a fluid cell. The skip
+        // works on x-aligned groups of a.skip_group cells (one memory segment
+        // of every direction array): a group moves nothing only when all its
+        // cells are NoDynamics, otherwise its NoDynamics cells run their dense
+        // (reference) update, so every store covers whole segments and no
+        // partial-segment writes reach HBM. blockDim.x is a multiple of 32
+        // and rows start 128-B aligned, so warp lanes are x-consecutive and
+        // groups are segment-aligned.
+        bool need = false;
         if (active && a.slot != nullptr) {
             s = a.slot[(static_cast<long long>(z) * g.ny + y) * g.nx + x];
-            active = a.rec[s].kind != KIND_NODYN;
+            need = a.rec[s].kind != KIND_NODYN;
         }
+        const unsigned ball = __ballot_sync(0xffffffffu, need);
+        const int G = a.skip_group;
+        const unsigned lane = threadIdx.x & 31u;
+        const unsigned gmask = G >= 32 ? 0xffffffffu : ((1u << G) - 1u);
+        active = active && ((ball >> (lane & ~unsigned(G - 1))) & gmask) != 0u;
     }
-    if (active) {
-        // Source coordinates of the pull f_i(x) <- f_i(x - c_i).
-        const int xm = (x == 0 && g.per_x) ? g.nx - 1 : x - 1;
-        const int xp = (x == g.nx - 1 && g.per_x) ? 0 : x + 1;
-        const int ym = (y == 0 && g.per_y) ? g.ny - 1 : y - 1;
-        const int yp = (y == g.ny - 1 && g.per_y) ? 0 : y + 1;
-        const int zm = (z == 0 && g.per_z) ? g.nz - 1 : z - 1;
-        const int zp = (z == g.nz - 1 && g.per_z) ? 0 : z + 1;
-
-        T f[Q];
-        sfor<Q>([&](auto I) {
-            constexpr int i = decltype(I)::value;
-            constexpr int cx = L::c[i][0], cy = L::c[i][1], cz = L::c[i][2];
-            const int sx = cx > 0 ? xm : (cx < 0 ? xp : x);
-            const int sy = cy > 0 ? ym : (cy < 0 ? yp : y);
-            const int sz = cz > 0 ? zm : (cz < 0 ? zp : z);
-            f[i] = __ldg(a.fin[i] + (sz * g.plane + sy * g.pitch + sx));
-        });
-
-        if constexpr ((KM & KM_SKIP) == 0) {
-            if (a.slot != nullptr) s = a.slot[(static_cast<long long>(z) * g.ny + y) * g.nx + x];
-        }
-        Cell<T, Q>::template apply<KM & ~KM_SKIP>(f, a.rec[s]);
-
-        const int center = z * g.plane + y * g.pitch + x;
-        sfor<Q>([&](auto I) {
-            constexpr int i = decltype(I)::value;
-            a.fout[i][center] = f[i];
-        });
-
-        if (a.push_up != nullptr && z == g.nz - 1) {
-            const int ghost = -g.plane + y * g.pitch + x;
-            sfor<Q>([&](auto I) {
-                constexpr int i = decltype(I)::value;
-                if constexpr (L::c[i][2] > 0) a.push_up[i * a.up_dstride + ghost] = f[i];
-            });
-        }
-        if (a.push_down != nullptr && z == 0) {
-            const int ghost = a.down_ghost_z * g.plane + y * g.pitch + x;
-            sfor<Q>([&](auto I) {
-                constexpr int i = decltype(I)::value;
-                if constexpr (L::c[i][2] < 0) a.push_down[i * a.down_dstride + ghost] = f[i];
-            });
-        }
-    }
+    if (active) cell_update<T, Q, KM & ~KM_SKIP, (KM & KM_SKIP) == 0>(a, x, y, z, s);
 
     if (a.counter != nullptr) {
         // Publish this block's peer stores at system scope, then take a ticket.
@@ -116,6 +139,33 @@ __global__ void __launch_bounds__(256, (min_blocks<T, Q, KM>())) k_pull(const __
             }
         }
     }
+}
+
+
+// Compacted masked sweep for porous media (single slab): the host lists the
+// x-aligned segments of a.skip_group cells that hold at least one
+// non-NoDynamics cell (the same rule as the KM_SKIP ballot), as linear
+// segment indices (z * ny + y) * ceil(nx / G) + x / G in row-major order.
+// Consecutive threads take consecutive cells of consecutive listed segments,
+// so every warp is fully populated (the masked dense sweep keeps idle lanes in
+// the warps that straddle solids, which caps its bytes in flight) while every
+// store still covers whole segments. NoDynamics cells of a listed segment run
+// their dense update; unlisted segments are never touched.
+template <typename T, int Q, unsigned KM>
+__global__ void __launch_bounds__(256, (min_blocks<T, Q, KM>()))
+    k_seg(const __grid_constant__ StepArgs<T> a, const unsigned* __restrict__ segs, long long nseg, int gshift) {
+    const Geo& g = a.g;
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const long long si = t >> gshift;
+    if (si >= nseg) return;
+    const unsigned e = __ldg(segs + si);
+    const unsigned nsx = unsigned((g.nx + (1 << gshift) - 1) >> gshift);
+    const unsigned row = e / nsx;
+    const int x = int((e - row * nsx) << gshift) + int(t & ((1 << gshift) - 1));
+    if (x >= g.nx) return;
+    const int z = int(row / unsigned(g.ny));
+    const int y = int(row - unsigned(z) * unsigned(g.ny));
+    cell_update<T, Q, KM, true>(a, x, y, z, a.uniform_slot);
 }
 
 
@@ -453,6 +503,20 @@ __global__ void __launch_bounds__(BX * BY + 32, 1)
         AA_PAIR(T, 19, KM_TRT | KM_BB | KM_MBB), AA_PAIR(T, 19, KM_ALL), AA_PAIR(T, 27, KM_RR), \
         AA_PAIR(T, 27, KM_ALL)
 
+#define SEG_ENTRY(T, Q, KM)                                                              \
+    KernelEntry {                                                                        \
+        int(sizeof(T) * 8), Q, unsigned(KM), LAYOUT_SEG,                                  \
+            reinterpret_cast<const void*>(&k_seg<T, Q, unsigned(KM)>),                    \
+            "k_seg<" #T ",D3Q" #Q "," #KM ">[" DLB_STR(DLB_MODE) "]"                        \
+    }
+#define SEG_SET(T)                                                                        \
+    SEG_ENTRY(T, 19, KM_BGK | KM_BB | KM_NODYN), SEG_ENTRY(T, 19, KM_TRT | KM_BB | KM_NODYN), \
+        SEG_ENTRY(T, 19, KM_RR | KM_BB | KM_NODYN),                                       \
+        SEG_ENTRY(T, 19, KM_BGK | KM_BB | KM_NODYN | KM_REGV | KM_REGP),                  \
+        SEG_ENTRY(T, 19, KM_TRT | KM_BB | KM_NODYN | KM_REGV | KM_REGP),                  \
+        SEG_ENTRY(T, 19, KM_RR | KM_BB | KM_NODYN | KM_REGV | KM_REGP), SEG_ENTRY(T, 19, KM_ALL), \
+        SEG_ENTRY(T, 27, KM_ALL)
+
 #define LIST_ENTRY(T, Q, KM, M)                                                          \
     KernelEntry {                                                                        \
         int(sizeof(T) * 8), Q, unsigned(KM), M ? LAYOUT_LIST_MASKED : LAYOUT_LIST,          \
@@ -502,7 +566,7 @@ __global__ void __launch_bounds__(BX * BY + 32, 1)
 static const KernelEntry kTable[] = {
     Q19_SET(float), Q19_SET(double), Q27_SET(float), Q27_SET(double), AA_SET(float), AA_SET(double),
     LIST_SET(float, 19), LIST_SET(double, 19), LIST_SET(float, 27), LIST_SET(double, 27),
-    TMA_SET,
+    TMA_SET, SEG_SET(float), SEG_SET(double),
 };
 
 const KernelEntry* kernel_table(int* n) {

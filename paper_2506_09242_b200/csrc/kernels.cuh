@@ -39,6 +39,10 @@ struct StepArgs {
     const uint8_t* slot;    // nx*ny*nz registry slots (x fastest) or nullptr if uniform
     int uniform_slot;
     int z_begin, z_step;    // plane z = z_begin + blockIdx.z * z_step
+    // masked porous sweep (KM_SKIP): x-aligned groups of skip_group cells (a
+    // power of two <= 32, one 32-B or 64-B memory segment) are skipped only
+    // when every cell of the group is NoDynamics
+    int skip_group;
     Geo g;
     // z-slab halo push over peer memory (nullptr when absent): after the
     // collision, cells of the top plane store their c_z = +1 populations into
@@ -60,7 +64,7 @@ struct StepArgs {
 
 // kernel families: dense two-population, AA even / odd, sparse lists (fluid / masked walls)
 enum Layout : int { LAYOUT_TWO_POP = 0, LAYOUT_AA = 1, LAYOUT_AA_ODD = 2, LAYOUT_LIST = 3, LAYOUT_LIST_MASKED = 4,
-                    LAYOUT_TMA = 5 };
+                    LAYOUT_TMA = 5, LAYOUT_SEG = 6 };
 
 struct KernelEntry {
     int precision_bits;

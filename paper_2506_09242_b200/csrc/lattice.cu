@@ -339,6 +339,16 @@ Lattice::Lattice(const dlb_lattice_desc& desc, const DynamicsRegistry& reg) : d_
 
     const int s = d_.precision_bits / 8;
     align_ = 128 / s;
+    {
+        // masked porous sweep: skip granularity in bytes of one direction
+        // array (default one 32-B sector; DLB_SKIP_GROUP_BYTES overrides, 4..128)
+        const char* e = std::getenv("DLB_SKIP_GROUP_BYTES");
+        int gb = e ? std::atoi(e) : 32;
+        gb = std::min(128, std::max(int(s), gb));
+        int g = 1;
+        while (g * 2 <= std::min(32, gb / int(s))) g *= 2;
+        skip_group_ = g;
+    }
     const long long nx = d_.dims[0], ny = d_.dims[1], nz = d_.dims[2];
     const long long pitch = (nx + 2 + align_ - 1) / align_ * align_;
     const long long plane = pitch * (ny + 2);
@@ -384,6 +394,7 @@ Lattice::~Lattice() {
     if (buf_[1] != buf_[0]) cudaFree(buf_[1]);
     cudaFree(d_slot_);
     cudaFree(d_list_);
+    cudaFree(d_seg_);
     cudaFree(d_fix_);
     cudaFree(d_tmap_);
     cudaFree(d_flags_);
@@ -411,6 +422,10 @@ int64_t Lattice::bytes_per_cell() const {
 
 int64_t Lattice::step_bytes() const {
     if (sparse_) return step_bytes_;
+    if (kernel_seg_ && !(lower_.linked || upper_.linked))  // listed cells + their slot bytes + 4 B per segment
+        return (int64_t(2) * d_.q * (d_.precision_bits / 8) + 1) * masked_cells_ + 4 * nseg_;
+    if ((km_needed_ & KM_SKIP) && masked_cells_ >= 0)
+        return int64_t(2) * d_.q * (d_.precision_bits / 8) * masked_cells_ + (d_slot_ ? cells() : 0);
     return bytes_per_cell() * cells();
 }
 
@@ -456,7 +471,44 @@ void Lattice::set_slots(const int32_t* slots) {
         if (seen[s]) present_slots_.push_back(int32_t(s));
     cudaFree(d_slot_);
     d_slot_ = nullptr;
-    sparse_ = (d_.flags & DLB_FLAG_SKIP_NODYNAMICS) && !split() && !aa() && !(uniform && first >= 0) &&
+    masked_cells_ = -1;
+    if ((d_.flags & (DLB_FLAG_SKIP_NODYNAMICS | DLB_FLAG_SPARSE_LISTS)) && !aa()) {
+        // cells the masked sweep moves: x-aligned groups of skip_group_ cells
+        // that hold at least one non-NoDynamics cell (k_pull KM_SKIP rule)
+        std::vector<uint8_t> nodyn(chains_.size(), 0);
+        for (std::size_t k = 0; k < chains_.size(); ++k) nodyn[k] = kind_bits(chains_[k]) == KM_NODYN;
+        const int G = skip_group_;
+        const long long nsx = (geo_.nx + G - 1) / G;
+        // compacted segment list for the single-slab masked sweep (k_seg)
+        const char* ce = std::getenv("DLB_MASKED_COMPACT");
+        const bool compact = !(ce && ce[0] == '0');
+        const bool want_segs = compact && !split() && !(d_.flags & DLB_FLAG_SPARSE_LISTS) &&
+                               (n / G) < (1LL << 32) - 1;
+        std::vector<uint32_t> segs;
+        long long moved = 0;
+        for (long long r = 0; r < n / geo_.nx; ++r) {
+            const uint8_t* row = u8.data() + r * geo_.nx;
+            for (int x0 = 0; x0 < geo_.nx; x0 += G) {
+                const int x1 = std::min(geo_.nx, x0 + G);
+                bool any = untagged_;
+                for (int x = x0; x < x1 && !any; ++x) any = !nodyn[row[x]];
+                if (!any) continue;
+                moved += x1 - x0;
+                if (want_segs) segs.push_back(uint32_t(r * nsx + x0 / G));
+            }
+        }
+        masked_cells_ = moved;
+        cudaFree(d_seg_);
+        d_seg_ = nullptr;
+        nseg_ = 0;
+        if (want_segs && !segs.empty() && !untagged_) {
+            cuda_check(cudaMalloc(&d_seg_, segs.size() * sizeof(uint32_t)), "cudaMalloc segments");
+            cuda_check(cudaMemcpy(d_seg_, segs.data(), segs.size() * sizeof(uint32_t), cudaMemcpyHostToDevice),
+                       "upload segments");
+            nseg_ = (long long)segs.size();
+        }
+    }
+    sparse_ = (d_.flags & DLB_FLAG_SPARSE_LISTS) && !split() && !aa() && !(uniform && first >= 0) &&
               !untagged_ && geo_.nx <= 8192 && geo_.ny <= 8192 && geo_.nz <= 4096;
     if (sparse_) {
         uniform_slot_ = 0;
@@ -676,6 +728,10 @@ void Lattice::set_uniform_slot(int32_t slot) {
         throw std::invalid_argument("slot " + std::to_string(slot) + " is not registered");
     cudaFree(d_slot_);
     d_slot_ = nullptr;
+    cudaFree(d_seg_);
+    d_seg_ = nullptr;
+    nseg_ = 0;
+    masked_cells_ = -1;
     uniform_slot_ = slot;
     untagged_ = false;
     present_slots_ = {slot};
@@ -688,7 +744,8 @@ void Lattice::select_kernel() {
     if (sparse_) return;
     km_needed_ = 0;
     for (int32_t s : present_slots_) km_needed_ |= kind_bits(chains_[std::size_t(s)]);
-    if ((d_.flags & DLB_FLAG_SKIP_NODYNAMICS) && (km_needed_ & KM_NODYN) && !aa()) km_needed_ |= KM_SKIP;
+    if ((d_.flags & (DLB_FLAG_SKIP_NODYNAMICS | DLB_FLAG_SPARSE_LISTS)) && (km_needed_ & KM_NODYN) && !aa())
+        km_needed_ |= KM_SKIP;
     if (aa()) {
         kernel_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_, LAYOUT_AA);
         kernel_odd_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_, LAYOUT_AA_ODD);
@@ -703,6 +760,12 @@ void Lattice::select_kernel() {
     if (!fixups_.empty())
         kernel_main_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_ & ~(KM_REGV | KM_REGP),
                                    LAYOUT_TWO_POP);
+    kernel_seg_ = nullptr;
+    if (d_seg_ && (km_needed_ & KM_SKIP)) {
+        unsigned km = km_needed_ & ~KM_SKIP;
+        if (kernel_main_) km &= ~(KM_REGV | KM_REGP);
+        kernel_seg_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km, LAYOUT_SEG);
+    }
     kernel_tma_ = nullptr;
     tma_grid_ = 0;
     if (tma_ok_ && fixups_.empty() && !(km_needed_ & KM_SKIP))
@@ -922,6 +985,7 @@ template <typename T>
 void Lattice::fill_recipes(StepArgs<T>& a) const {
     a.slot = d_slot_;
     a.uniform_slot = uniform_slot_;
+    a.skip_group = skip_group_;
     for (std::size_t s = 0; s < chains_.size(); ++s) a.rec[s] = compile_recipe<T>(chains_[s]);
 }
 
@@ -1075,6 +1139,7 @@ void Lattice::launch_step(int parity) {
     }
     a.slot = d_slot_;
     a.uniform_slot = uniform_slot_;
+    a.skip_group = skip_group_;
     a.g = geo_;
     for (std::size_t s = 0; s < chains_.size(); ++s) a.rec[s] = compile_recipe<T>(chains_[s]);
 
@@ -1117,8 +1182,20 @@ void Lattice::launch_step(int parity) {
         a.z_step = 1;
         void* args[] = {&a};
         const bool split_rare = kernel_main_ != nullptr && !fixups_.empty();
-        cuda_check(cudaLaunchKernel(split_rare ? kernel_main_->fn : fn, dim3(gx, gy, geo_.nz), block, args, 0,
-                                    stream_), "launch");
+        if (kernel_seg_) {
+            // compacted masked sweep: one thread per cell of the listed segments
+            const unsigned* sp = d_seg_;
+            long long ns = nseg_;
+            int gshift = 0;
+            while ((1 << gshift) < skip_group_) ++gshift;
+            void* sargs[] = {&a, &sp, &ns, &gshift};
+            const long long threads = ns << gshift;
+            cuda_check(cudaLaunchKernel(kernel_seg_->fn, dim3(unsigned((threads + 255) / 256)), dim3(256), sargs, 0,
+                                        stream_), "launch segments");
+        } else {
+            cuda_check(cudaLaunchKernel(split_rare ? kernel_main_->fn : fn, dim3(gx, gy, geo_.nz), block, args, 0,
+                                        stream_), "launch");
+        }
         if (split_rare) {
             // the main sweep treated the regularized cells as plain bulk cells;
             // recompute them (same f_in, later in stream order) with the full chain

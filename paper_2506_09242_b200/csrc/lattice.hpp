@@ -85,6 +85,7 @@ class Lattice {
     int launches_per_step() const;
     const char* kernel_name() const {
         if (kernel_tma_ && !(lower_.linked || upper_.linked)) return kernel_tma_->name;
+        if (kernel_seg_ && !(lower_.linked || upper_.linked)) return kernel_seg_->name;
         if (kernel_main_ && !fixups_.empty() && !(lower_.linked || upper_.linked)) return kernel_main_->name;
         return kernel_ ? kernel_->name : "<none>";
     }
@@ -119,6 +120,12 @@ class Lattice {
     cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
     Geo geo_{};
     int align_ = 32;            // elements per 128 B
+    int skip_group_ = 8;        // masked porous sweep: cells per skip group (power of two <= 32)
+    int64_t masked_cells_ = -1; // masked porous sweep: cells in non-skipped groups (-1: not masked)
+    // compacted masked sweep (single slab): listed segment indices and kernel
+    unsigned* d_seg_ = nullptr;
+    long long nseg_ = 0;
+    const KernelEntry* kernel_seg_ = nullptr;
     long long base_off_ = 0;    // elements from array start to the interior origin
     void* buf_[2] = {nullptr, nullptr};
     int cur_ = 0;               // buffer holding the current state (f_in)

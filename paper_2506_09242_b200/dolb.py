@@ -322,7 +322,8 @@ class DeviceRun:
 
     def __init__(self, dims, periodic, registry: DynamicsRegistry, dispatch: DispatchSet | None = None,
                  q: int = 19, precision: int = 64, slabs: int = 1, devices=None, arith: str = "exact",
-                 dist=None, layout: str = "twopop", skip_nodynamics: bool = False, tma: bool = False):
+                 dist=None, layout: str = "twopop", skip_nodynamics: bool = False, tma: bool = False,
+                 sparse_lists: bool = False):
         self.dims = tuple(int(v) for v in dims)
         self.periodic = tuple(int(bool(p)) for p in periodic)
         self.registry = registry
@@ -345,7 +346,8 @@ class DeviceRun:
             d.arith = ARITH_FAST if arith == "fast" else ARITH_EXACT
             d.device = devices[k]
             d.z_origin, d.global_nz = parts[r][0], self.dims[2]
-            d.flags = (_capi.FLAG_SKIP_NODYNAMICS if skip_nodynamics else 0) | (_capi.FLAG_TMA if tma else 0)
+            d.flags = ((_capi.FLAG_SKIP_NODYNAMICS if skip_nodynamics else 0) | (_capi.FLAG_TMA if tma else 0)
+                       | (_capi.FLAG_SPARSE_LISTS if sparse_lists else 0))
             self.slabs.append(_Lattice(d, registry))
         self.ranks = mine
         if dist is None and world > 1:

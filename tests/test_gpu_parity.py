@@ -354,10 +354,29 @@ def test_aa_upload_mid_run(oracle):
 
 # ---------------------------------------------------------------- masked porous variant
 @pytest.mark.parametrize("name", ["sphere48_trt_f64_c4", "plates16_trt_vel_f64", "plates16_rr_vel_f64"])
-def test_skip_nodynamics_fluid_cells_bit_identical(oracle, name):
+def test_sparse_lists_fluid_cells_bit_identical(oracle, name):
     """Skipping NoDynamics cells (no loads / stores) leaves every Collide-kind
     cell bit-identical to the reference trajectory."""
     from golden_cases import make_case
+    spec = CASES[name]
+    setup, bits, steps = product_setup(spec)
+    run = dlb.build_run(setup, precision=bits, sparse_lists=True)
+    run.advance(steps)
+    got = run.gather_populations().reshape(19, -1)
+    want = oracle.run_case(make_case(spec), np.float64, steps).reshape(19, -1)
+    fl = fluid_mask(spec)
+    assert np.array_equal(got[:, fl], want[:, fl])
+    assert "k_list" in run.kernel_name()  # single slab -> kind-sorted sparse lists
+    assert run.step_bytes() < 304 * run.num_cells()
+
+
+@pytest.mark.parametrize("group_bytes", [8, 32, 64, 256])
+@pytest.mark.parametrize("name", ["sphere48_trt_f64_c4", "plates16_trt_vel_f64", "plates16_rr_vel_f64"])
+def test_masked_sweep_fluid_cells_bit_identical(oracle, name, group_bytes, monkeypatch):
+    """Masked sweep: all-NoDynamics segments (1 .. 32 cells) are skipped, mixed
+    segments run the dense update; Collide-kind cells stay bit-identical."""
+    from golden_cases import make_case
+    monkeypatch.setenv("DLB_SKIP_GROUP_BYTES", str(group_bytes))
     spec = CASES[name]
     setup, bits, steps = product_setup(spec)
     run = dlb.build_run(setup, precision=bits, skip_nodynamics=True)
@@ -366,8 +385,27 @@ def test_skip_nodynamics_fluid_cells_bit_identical(oracle, name):
     want = oracle.run_case(make_case(spec), np.float64, steps).reshape(19, -1)
     fl = fluid_mask(spec)
     assert np.array_equal(got[:, fl], want[:, fl])
-    assert "k_list" in run.kernel_name()  # single slab -> kind-sorted sparse lists
-    assert run.step_bytes() < 304 * run.num_cells()
+    nod = np.asarray(setup.chain_index).reshape(-1) == 2
+    if nod.any():
+        assert "k_seg" in run.kernel_name()  # single slab -> compacted segment sweep
+        assert run.step_bytes() < 304 * run.num_cells()
+    # moved cells >= non-NoDynamics cells: the byte count covers every Collide / wall cell
+    assert run.step_bytes() >= 304 * int((~nod).sum())
+
+
+def test_masked_dense_sweep_fluid_cells_bit_identical(oracle, monkeypatch):
+    """The uncompacted masked sweep (warp ballot over x-aligned segments)."""
+    from golden_cases import make_case
+    monkeypatch.setenv("DLB_MASKED_COMPACT", "0")
+    spec = CASES["sphere48_trt_f64_c4"]
+    setup, bits, steps = product_setup(spec)
+    run = dlb.build_run(setup, precision=bits, skip_nodynamics=True)
+    run.advance(steps)
+    got = run.gather_populations().reshape(19, -1)
+    want = oracle.run_case(make_case(spec), np.float64, steps).reshape(19, -1)
+    fl = fluid_mask(spec)
+    assert np.array_equal(got[:, fl], want[:, fl])
+    assert "SKIP" in run.kernel_name()
 
 
 def test_skip_nodynamics_zslabs_masked_dense(oracle):
