@@ -9,7 +9,12 @@ Translation units and their arithmetic flags:
   diag.cu                -fmad=false (diagnostic values and tree sums restate
                          diagnostics.cpp / runner.cpp double arithmetic)
   tree.cpp               host tree planning / combination
-  capi.cu, chain.cpp     host code
+  capi.cu, chain.cpp     host code (dlb.h boundary, chain / registry model)
+  cases.cpp, device_run.cpp, runner.cpp, dolb_capi.cpp
+                         host code: benchmark cases, multi-slab DeviceRun, the
+                         runner and the reference's dolb.h C interface
+The library is also linked as _lib/libdolb.so (symlink) for callers of the
+reference's dolb.h (CLI, capi tests: -ldolb).
 """
 from __future__ import annotations
 
@@ -29,7 +34,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC",
           "-Xcompiler", "-fvisibility=hidden", "-I", os.path.join(ROOT, "include")]
-HEADERS = ["lbm_cell.cuh", "kernels.cuh", "chain.hpp", "lattice.hpp", "canon.cuh", "tree.hpp"]
+HEADERS = ["lbm_cell.cuh", "kernels.cuh", "chain.hpp", "lattice.hpp", "canon.cuh", "tree.hpp", "cases.hpp",
+           "device_run.hpp", "runner.hpp"]
 
 UNITS = [
     # (source, object, extra flags)
@@ -40,11 +46,17 @@ UNITS = [
     ("capi.cu", "capi.o", ["-fmad=false"]),
     ("tree.cpp", "tree.o", ["-x", "cu", "-fmad=false"]),
     ("chain.cpp", "chain.o", ["-x", "cu", "-fmad=false"]),
+    ("cases.cpp", "cases.o", ["-x", "cu", "-fmad=false"]),
+    ("device_run.cpp", "device_run.o", ["-x", "cu", "-fmad=false"]),
+    ("runner.cpp", "runner.o", ["-x", "cu", "-fmad=false"]),
+    ("dolb_capi.cpp", "dolb_capi.o", ["-x", "cu", "-fmad=false"]),
 ]
+DOLB = os.path.join(LIBDIR, "libdolb.so")
 
 
 def _deps_mtime() -> float:
-    files = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "dlb.h")]
+    files = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", h)
+                                                        for h in ("dlb.h", "dolb.h")]
     return max(os.path.getmtime(f) for f in files)
 
 
@@ -80,6 +92,10 @@ def build(verbose: bool = False, force: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    if not os.path.islink(DOLB):
+        if os.path.exists(DOLB):
+            os.remove(DOLB)
+        os.symlink(os.path.basename(LIB), DOLB)
     return "\n".join(logs)
 
 

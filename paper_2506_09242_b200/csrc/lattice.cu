@@ -831,6 +831,41 @@ void Lattice::fill_equilibrium(const double* rho, const double* ux, const double
     }
 }
 
+// Uniform equilibrium state (rho, u) in every cell: the chunked equilibrium
+// fill with constant staging arrays (same k_fill_eq arithmetic).
+void Lattice::fill_uniform(double rho, double ux, double uy, double uz) {
+    const long long plane_cells = (long long)geo_.nx * geo_.ny;
+    const int zc = int(std::max<long long>(1, std::min<long long>(geo_.nz, (long long)(staging_bytes_ / 32) / plane_cells)));
+    const long long n = plane_cells * zc;
+    if (n * 32 > (long long)staging_bytes_) throw std::invalid_argument("plane too large");
+    std::vector<double> h(std::size_t(4 * n));
+    std::fill(h.begin(), h.begin() + n, rho);
+    std::fill(h.begin() + n, h.begin() + 2 * n, ux);
+    std::fill(h.begin() + 2 * n, h.begin() + 3 * n, uy);
+    std::fill(h.begin() + 3 * n, h.end(), uz);
+    // k_fill_eq indexes the staging arrays chunk-locally: one upload serves every chunk
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    envelope_valid_ = false;
+    reset_aa();
+    double* st = static_cast<double*>(staging_);
+    cuda_check(cudaMemcpyAsync(st, h.data(), h.size() * 8, cudaMemcpyHostToDevice, stream_), "h2d");
+    for (int z0 = 0; z0 < geo_.nz; z0 += zc) {
+        const int nzc = std::min(zc, geo_.nz - z0);
+        const long long m = plane_cells * nzc;
+        const int grid = grid_for(m);
+        void* o = origin(cur_);
+        if (d_.precision_bits == 64) {
+            if (d_.q == 19) k_fill_eq<double, 19><<<grid, 256, 0, stream_>>>((double*)o, geo_, st, st + n, st + 2 * n, st + 3 * n, z0, nzc, aa());
+            else k_fill_eq<double, 27><<<grid, 256, 0, stream_>>>((double*)o, geo_, st, st + n, st + 2 * n, st + 3 * n, z0, nzc, aa());
+        } else {
+            if (d_.q == 19) k_fill_eq<float, 19><<<grid, 256, 0, stream_>>>((float*)o, geo_, st, st + n, st + 2 * n, st + 3 * n, z0, nzc, aa());
+            else k_fill_eq<float, 27><<<grid, 256, 0, stream_>>>((float*)o, geo_, st, st + n, st + 2 * n, st + 3 * n, z0, nzc, aa());
+        }
+        cuda_check(cudaGetLastError(), "k_fill_eq");
+    }
+    cuda_check(cudaStreamSynchronize(stream_), "fill_uniform");
+}
+
 void Lattice::fill_tgv(int64_t L, double u_inf) {
     if (d_.dims[0] != L || d_.dims[1] != L || d_.global_nz != L)
         throw std::invalid_argument("TGV fill needs an L^3 domain");

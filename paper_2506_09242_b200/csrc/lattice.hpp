@@ -45,6 +45,7 @@ class Lattice {
     void set_uniform_slot(int32_t slot);
     void set_dispatch(const int32_t* tags, std::size_t n);
     void fill_equilibrium(const double* rho, const double* ux, const double* uy, const double* uz);
+    void fill_uniform(double rho, double ux, double uy, double uz);
     void fill_tgv(int64_t L, double u_inf);
     void upload(const double* canon);
     void download(double* canon);
