@@ -389,8 +389,8 @@ def test_masked_sweep_fluid_cells_bit_identical(oracle, name, group_bytes, monke
     if nod.any():
         assert "k_seg" in run.kernel_name()  # single slab -> compacted segment sweep
         assert run.step_bytes() < 304 * run.num_cells()
-    # moved cells >= non-NoDynamics cells: the byte count covers every Collide / wall cell
-    assert run.step_bytes() >= 304 * int((~nod).sum())
+    # stores cover at least every Collide / wall cell (wall cells load only fluid-facing links)
+    assert run.step_bytes() >= 152 * int((~nod).sum())  # every listed cell stores its q links
 
 
 def test_masked_dense_sweep_fluid_cells_bit_identical(oracle, monkeypatch):
