@@ -35,6 +35,15 @@ RUNNER_CASES = {
                             "case.H": "4", "case.upstream": "4", "case.downstream": "4",
                             "run.tmax": "steady", "run.steady_tol": "1e-4", "run.max_steps": "3000",
                             "run.output_every": "50"},
+    # config 1 through the public API: lid-driven cavity 64^3 D3Q19 BGK fp64, 1000 steps
+    "c1_cavity64_bgk_f64": {"case.kind": "cavity", "case.L": "64", "case.Re": "1000", "case.Ma": "0.1",
+                            "run.tmax": "1000", "run.output_every": "250", "run.blocks": "1,1,8",
+                            "run.workers": "8", "run.dump_every": "1000"},
+    # config 3 shape at reduced size: cavity TRT fp32
+    "c3_cavity96_trt_f32": {"case.kind": "cavity", "case.L": "96", "case.Re": "1000", "case.Ma": "0.1",
+                            "case.collision": "trt", "case.precision": "f32", "run.tmax": "200",
+                            "run.output_every": "100", "run.blocks": "1,1,8", "run.workers": "8",
+                            "run.avg_from": "0"},
     "sphere48_trt_f64": {"case.kind": "porous", "case.geometry": "@SPHERE", "case.voxel_dims": "48,48,48",
                          "case.upstream": "8", "case.downstream": "8", "run.tmax": "200",
                          "run.output_every": "50", "run.dump_every": "200"},
