@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <numeric>
 #include <cstdlib>
@@ -1085,6 +1086,12 @@ void Lattice::launch_host_block(void* f_in, const int64_t ext[3]) {
     blk_.elem = int(sizeof(T));
     blk_.dout = dout;
     blk_.pending = true;
+    static const bool trace = std::getenv("DLB_TRACE_BLOCK") != nullptr;
+    if (trace) {  // timeline events (DLB_TRACE_BLOCK): begin, end of H2D, end of compute
+        for (auto& e : blk_tr_)
+            if (!e) cuda_check(cudaEventCreate(&e), "event");
+        cuda_check(cudaEventRecord(blk_tr_[0], h2d_stream_), "event");
+    }
     int loaded = 0;  // host planes [0, loaded) are on the device
     for (int c = 0; c < nchunks; ++c) {
         const int z0 = c * zc, z1 = std::min(hg.nz, z0 + zc);
@@ -1098,6 +1105,10 @@ void Lattice::launch_host_block(void* f_in, const int64_t ext[3]) {
         void* args[] = {&a};
         cuda_check(cudaLaunchKernel(kernel_->fn, dim3(gx, gy, z1 - z0), block, args, 0, stream_), "launch");
         cuda_check(cudaEventRecord(blk_ev_[2 * c + 1], stream_), "event");
+    }
+    if (trace) {
+        cuda_check(cudaEventRecord(blk_tr_[1], h2d_stream_), "event");
+        cuda_check(cudaEventRecord(blk_tr_[2], stream_), "event");
     }
 }
 
@@ -1144,12 +1155,20 @@ void Lattice::finish_host_block() {
     for (int c = 0; c < blk_.nchunks; ++c) {
         const int z1 = std::min(blk_.nz, (c + 1) * blk_.zc);
         cuda_check(cudaStreamWaitEvent(copy_stream_, blk_ev_[2 * c + 1], 0), "wait");
+        if (c == 0 && blk_tr_[3]) cuda_check(cudaEventRecord(blk_tr_[3], copy_stream_), "event");
         block_copy(copy_stream_, blk_.dout, false, written, z1 + 1);
         written = z1 + 1;
     }
+    if (blk_tr_[4]) cuda_check(cudaEventRecord(blk_tr_[4], copy_stream_), "event");
     blk_.pending = false;
     cuda_check(cudaStreamSynchronize(copy_stream_), "block copy-back");
     cuda_check(cudaStreamSynchronize(stream_), "block step");
+    if (blk_tr_[4]) {
+        float t[5] = {0, 0, 0, 0, 0};
+        for (int k = 1; k < 5; ++k) cudaEventElapsedTime(&t[k], blk_tr_[0], blk_tr_[k]);
+        std::fprintf(stderr, "[dlb block] H2D done %.1f ms, compute done %.1f ms, D2H start %.1f ms, D2H done %.1f ms\n",
+                     t[1], t[2], t[3], t[4]);
+    }
     ++steps_;
 }
 

@@ -197,6 +197,7 @@ class Lattice {
     cudaStream_t copy_stream_ = nullptr;
     cudaStream_t h2d_stream_ = nullptr;
     std::vector<cudaEvent_t> blk_ev_;
+    cudaEvent_t blk_tr_[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // DLB_TRACE_BLOCK timeline
     struct BlockPlan {
         void* f_in = nullptr;
         void* dout = nullptr;
