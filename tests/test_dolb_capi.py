@@ -34,13 +34,15 @@ def api():
 
 
 # ------------------------------------------------------------------ CPU: C surface
-def test_library_exports_dolb_h():
+def test_library_exports_every_dolb_h_symbol():
     import ctypes as C
-    lib = C.CDLL(DOLB_LIB)
-    for sym in ("dolb_version", "dolb_last_error", "dolb_config_new", "dolb_config_free", "dolb_config_load",
-                "dolb_config_set", "dolb_config_get", "dolb_run", "dolb_show_models", "dolb_bytes_per_cell",
-                "dolb_peak_glups", "dolb_memory_fraction"):
-        assert hasattr(lib, sym), sym
+    import re
+    header = open(os.path.join(os.path.dirname(HERE), "include", "dolb.h")).read()
+    declared = set(re.findall(r"DOLB_API\s+[\w\s\*]+?\b(dolb_\w+)\s*\(", header))
+    assert len(declared) == 12, declared
+    lib = C.CDLL(DOLB_LIB)  # the libdolb.so name the reference's callers link against
+    missing = [s for s in declared if not hasattr(lib, s)]
+    assert not missing, missing
 
 
 def test_version_and_null_arguments(api):
