@@ -39,8 +39,8 @@ constexpr int min_blocks() {
 // the output buffer, and push the z-crossing links into the neighbours' ghost
 // planes when the slab is linked. READ_SLOT: look the slot up here (after the
 // loads, so the slot read overlaps them); otherwise `s` is already known.
-template <typename T, int Q, unsigned KM, bool READ_SLOT>
-__device__ __forceinline__ void cell_update(const StepArgs<T>& a, int x, int y, int z, int s) {
+template <typename T, int Q>
+__device__ __forceinline__ void pull_cell(const StepArgs<T>& a, int x, int y, int z, T (&f)[Q]) {
     using L = Lat<Q>;
     const Geo& g = a.g;
     const int xm = (x == 0 && g.per_x) ? g.nx - 1 : x - 1;
@@ -49,8 +49,6 @@ __device__ __forceinline__ void cell_update(const StepArgs<T>& a, int x, int y, 
     const int yp = (y == g.ny - 1 && g.per_y) ? 0 : y + 1;
     const int zm = (z == 0 && g.per_z) ? g.nz - 1 : z - 1;
     const int zp = (z == g.nz - 1 && g.per_z) ? 0 : z + 1;
-
-    T f[Q];
     sfor<Q>([&](auto I) {
         constexpr int i = decltype(I)::value;
         constexpr int cx = L::c[i][0], cy = L::c[i][1], cz = L::c[i][2];
@@ -59,10 +57,12 @@ __device__ __forceinline__ void cell_update(const StepArgs<T>& a, int x, int y, 
         const int sz = cz > 0 ? zm : (cz < 0 ? zp : z);
         f[i] = __ldg(a.fin[i] + (sz * g.plane + sy * g.pitch + sx));
     });
+}
 
-    if constexpr (READ_SLOT) {
-        if (a.slot != nullptr) s = a.slot[(static_cast<long long>(z) * g.ny + y) * g.nx + x];
-    }
+template <typename T, int Q, unsigned KM>
+__device__ __forceinline__ void collide_store_cell(const StepArgs<T>& a, int x, int y, int z, int s, T (&f)[Q]) {
+    using L = Lat<Q>;
+    const Geo& g = a.g;
     Cell<T, Q>::template apply<KM>(f, a.rec[s]);
 
     const int center = z * g.plane + y * g.pitch + x;
@@ -85,6 +85,16 @@ __device__ __forceinline__ void cell_update(const StepArgs<T>& a, int x, int y, 
             if constexpr (L::c[i][2] < 0) a.push_down[i * a.down_dstride + ghost] = f[i];
         });
     }
+}
+
+template <typename T, int Q, unsigned KM, bool READ_SLOT>
+__device__ __forceinline__ void cell_update(const StepArgs<T>& a, int x, int y, int z, int s) {
+    T f[Q];
+    pull_cell<T, Q>(a, x, y, z, f);
+    if constexpr (READ_SLOT) {
+        if (a.slot != nullptr) s = a.slot[(static_cast<long long>(z) * a.g.ny + y) * a.g.nx + x];
+    }
+    collide_store_cell<T, Q, KM>(a, x, y, z, s, f);
 }
 
 template <typename T, int Q, unsigned KM>
@@ -151,21 +161,42 @@ __global__ void __launch_bounds__(256, (min_blocks<T, Q, KM>())) k_pull(const __
 // the warps that straddle solids, which caps its bytes in flight) while every
 // store still covers whole segments. NoDynamics cells of a listed segment run
 // their dense update; unlisted segments are never touched.
-template <typename T, int Q, unsigned KM>
-__global__ void __launch_bounds__(256, (min_blocks<T, Q, KM>()))
+// CPT cells per thread (cells t and t + 256 of a 256 * CPT-cell block range):
+// every thread issues the loads of all its cells before the first collision,
+// CPT times the bytes in flight per thread of the latency-bound fp64 sweep.
+template <typename T, int Q, unsigned KM, int CPT>
+__global__ void __launch_bounds__(256, (CPT == 1 ? min_blocks<T, Q, KM>() : 2))
     k_seg(const __grid_constant__ StepArgs<T> a, const unsigned* __restrict__ segs, long long nseg, int gshift) {
     const Geo& g = a.g;
-    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const long long si = t >> gshift;
-    if (si >= nseg) return;
-    const unsigned e = __ldg(segs + si);
     const unsigned nsx = unsigned((g.nx + (1 << gshift) - 1) >> gshift);
-    const unsigned row = e / nsx;
-    const int x = int((e - row * nsx) << gshift) + int(t & ((1 << gshift) - 1));
-    if (x >= g.nx) return;
-    const int z = int(row / unsigned(g.ny));
-    const int y = int(row - unsigned(z) * unsigned(g.ny));
-    cell_update<T, Q, KM, true>(a, x, y, z, a.uniform_slot);
+    const long long n = nseg << gshift;
+    const long long base = static_cast<long long>(blockIdx.x) * (256 * CPT) + threadIdx.x;
+    int xs[CPT], ys[CPT], zs[CPT];
+    bool ok[CPT];
+    T f[CPT][Q];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+        const long long t = base + 256 * c;
+        ok[c] = t < n;
+        xs[c] = ys[c] = zs[c] = 0;
+        if (ok[c]) {
+            const unsigned e = __ldg(segs + (t >> gshift));
+            const unsigned row = e / nsx;
+            xs[c] = int((e - row * nsx) << gshift) + int(t & ((1 << gshift) - 1));
+            zs[c] = int(row / unsigned(g.ny));
+            ys[c] = int(row - unsigned(zs[c]) * unsigned(g.ny));
+            ok[c] = xs[c] < g.nx;
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < CPT; ++c)
+        if (ok[c]) pull_cell<T, Q>(a, xs[c], ys[c], zs[c], f[c]);
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+        if (!ok[c]) continue;
+        const int s = a.slot ? a.slot[(static_cast<long long>(zs[c]) * g.ny + ys[c]) * g.nx + xs[c]] : a.uniform_slot;
+        collide_store_cell<T, Q, KM>(a, xs[c], ys[c], zs[c], s, f[c]);
+    }
 }
 
 
@@ -503,12 +534,13 @@ __global__ void __launch_bounds__(BX * BY + 32, 1)
         AA_PAIR(T, 19, KM_TRT | KM_BB | KM_MBB), AA_PAIR(T, 19, KM_ALL), AA_PAIR(T, 27, KM_RR), \
         AA_PAIR(T, 27, KM_ALL)
 
-#define SEG_ENTRY(T, Q, KM)                                                              \
+#define SEG_ENTRY1(T, Q, KM, CPT)                                                        \
     KernelEntry {                                                                        \
         int(sizeof(T) * 8), Q, unsigned(KM), LAYOUT_SEG,                                  \
-            reinterpret_cast<const void*>(&k_seg<T, Q, unsigned(KM)>),                    \
-            "k_seg<" #T ",D3Q" #Q "," #KM ">[" DLB_STR(DLB_MODE) "]"                        \
+            reinterpret_cast<const void*>(&k_seg<T, Q, unsigned(KM), CPT>),               \
+            "k_seg<" #T ",D3Q" #Q "," #KM ",x" #CPT ">[" DLB_STR(DLB_MODE) "]", 0, 0, 0, CPT \
     }
+#define SEG_ENTRY(T, Q, KM) SEG_ENTRY1(T, Q, KM, 1), SEG_ENTRY1(T, Q, KM, 2)
 #define SEG_SET(T)                                                                        \
     SEG_ENTRY(T, 19, KM_BGK | KM_BB | KM_NODYN), SEG_ENTRY(T, 19, KM_TRT | KM_BB | KM_NODYN), \
         SEG_ENTRY(T, 19, KM_RR | KM_BB | KM_NODYN),                                       \

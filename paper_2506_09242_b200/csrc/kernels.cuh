@@ -74,6 +74,7 @@ struct KernelEntry {
     const void* fn;  // __global__ function pointer
     const char* name;
     int tile_x = 0, tile_y = 0, stages = 0;  // TMA kernels: tile shape and ring depth
+    int cpt = 1;                             // segment kernels: cells per thread
 };
 
 // Kernel tables of the two arithmetic modes (one translation unit each).

@@ -766,6 +766,18 @@ void Lattice::select_kernel() {
         unsigned km = km_needed_ & ~KM_SKIP;
         if (kernel_main_) km &= ~(KM_REGV | KM_REGP);
         kernel_seg_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km, LAYOUT_SEG);
+        // cells per thread of the segment sweep (DLB_SEG_CPT): 2 for fp64
+        // (c4: 24.96 vs 23.76 GLUPS, profiles/r01_summary.md), 1 for fp32
+        const char* ce = std::getenv("DLB_SEG_CPT");
+        const int cpt = ce ? std::atoi(ce) : (d_.precision_bits == 64 ? 2 : 1);
+        if (kernel_seg_ && kernel_seg_->cpt != cpt) {
+            int nt = 0;
+            const KernelEntry* t = d_.arith == DLB_ARITH_FAST ? fast::kernel_table(&nt) : exact::kernel_table(&nt);
+            for (int k = 0; k < nt; ++k)
+                if (t[k].layout == LAYOUT_SEG && t[k].km == kernel_seg_->km && t[k].cpt == cpt &&
+                    t[k].precision_bits == kernel_seg_->precision_bits && t[k].q == kernel_seg_->q)
+                    kernel_seg_ = &t[k];
+        }
     }
     kernel_tma_ = nullptr;
     tma_grid_ = 0;
@@ -1244,8 +1256,9 @@ void Lattice::launch_step(int parity) {
             while ((1 << gshift) < skip_group_) ++gshift;
             void* sargs[] = {&a, &sp, &ns, &gshift};
             const long long threads = ns << gshift;
-            cuda_check(cudaLaunchKernel(kernel_seg_->fn, dim3(unsigned((threads + 255) / 256)), dim3(256), sargs, 0,
-                                        stream_), "launch segments");
+            const long long per_block = 256LL * kernel_seg_->cpt;
+            cuda_check(cudaLaunchKernel(kernel_seg_->fn, dim3(unsigned((threads + per_block - 1) / per_block)),
+                                        dim3(256), sargs, 0, stream_), "launch segments");
         } else {
             cuda_check(cudaLaunchKernel(split_rare ? kernel_main_->fn : fn, dim3(gx, gy, geo_.nz), block, args, 0,
                                         stream_), "launch");

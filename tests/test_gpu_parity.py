@@ -387,10 +387,26 @@ def test_masked_sweep_fluid_cells_bit_identical(oracle, name, group_bytes, monke
     assert np.array_equal(got[:, fl], want[:, fl])
     nod = np.asarray(setup.chain_index).reshape(-1) == 2
     if nod.any():
-        assert "k_seg" in run.kernel_name()  # single slab -> compacted segment sweep
+        assert "k_seg" in run.kernel_name()  # single slab -> compacted segment sweep (x2 cells per thread in fp64)
         assert run.step_bytes() < 304 * run.num_cells()
     # stores cover at least every Collide / wall cell (wall cells load only fluid-facing links)
     assert run.step_bytes() >= 152 * int((~nod).sum())  # every listed cell stores its q links
+
+
+@pytest.mark.parametrize("cpt", ["1", "2"])
+def test_segment_sweep_cells_per_thread(oracle, cpt, monkeypatch):
+    """k_seg with one and two cells per thread: Collide-kind cells bit-identical."""
+    from golden_cases import make_case
+    monkeypatch.setenv("DLB_SEG_CPT", cpt)
+    spec = CASES["sphere48_trt_f64_c4"]
+    setup, bits, steps = product_setup(spec)
+    run = dlb.build_run(setup, precision=bits, skip_nodynamics=True)
+    assert f",x{cpt}>" in run.kernel_name()
+    run.advance(steps)
+    got = run.gather_populations().reshape(19, -1)
+    want = oracle.run_case(make_case(spec), np.float64, steps).reshape(19, -1)
+    fl = fluid_mask(spec)
+    assert np.array_equal(got[:, fl], want[:, fl])
 
 
 def test_masked_dense_sweep_fluid_cells_bit_identical(oracle, monkeypatch):
