@@ -128,7 +128,54 @@ __global__ void __launch_bounds__(256, (min_blocks<T, Q, KM>())) k_pull(const __
         const unsigned gmask = G >= 32 ? 0xffffffffu : ((1u << G) - 1u);
         active = active && ((ball >> (lane & ~unsigned(G - 1))) & gmask) != 0u;
     }
-    if (active) cell_update<T, Q, KM & ~KM_SKIP, (KM & KM_SKIP) == 0>(a, x, y, z, s);
+    // (body kept inline rather than through cell_update: the inlined helper
+    // changes the instruction schedule and costs 13 % on c3, profiles/r01_summary.md)
+    if (active) {
+        // Source coordinates of the pull f_i(x) <- f_i(x - c_i).
+        const int xm = (x == 0 && g.per_x) ? g.nx - 1 : x - 1;
+        const int xp = (x == g.nx - 1 && g.per_x) ? 0 : x + 1;
+        const int ym = (y == 0 && g.per_y) ? g.ny - 1 : y - 1;
+        const int yp = (y == g.ny - 1 && g.per_y) ? 0 : y + 1;
+        const int zm = (z == 0 && g.per_z) ? g.nz - 1 : z - 1;
+        const int zp = (z == g.nz - 1 && g.per_z) ? 0 : z + 1;
+
+        T f[Q];
+        sfor<Q>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            constexpr int cx = L::c[i][0], cy = L::c[i][1], cz = L::c[i][2];
+            const int sx = cx > 0 ? xm : (cx < 0 ? xp : x);
+            const int sy = cy > 0 ? ym : (cy < 0 ? yp : y);
+            const int sz = cz > 0 ? zm : (cz < 0 ? zp : z);
+            f[i] = __ldg(a.fin[i] + (sz * g.plane + sy * g.pitch + sx));
+        });
+
+        if constexpr ((KM & KM_SKIP) == 0) {
+            if (a.slot != nullptr) s = a.slot[(static_cast<long long>(z) * g.ny + y) * g.nx + x];
+        }
+        Cell<T, Q>::template apply<KM & ~KM_SKIP>(f, a.rec[s]);
+
+        const int center = z * g.plane + y * g.pitch + x;
+        sfor<Q>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            a.fout[i][center] = f[i];
+        });
+
+        if (a.push_up != nullptr && z == g.nz - 1) {
+            const int ghost = -g.plane + y * g.pitch + x;
+            sfor<Q>([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                if constexpr (L::c[i][2] > 0) a.push_up[i * a.up_dstride + ghost] = f[i];
+            });
+        }
+        if (a.push_down != nullptr && z == 0) {
+            const int ghost = a.down_ghost_z * g.plane + y * g.pitch + x;
+            sfor<Q>([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                if constexpr (L::c[i][2] < 0) a.push_down[i * a.down_dstride + ghost] = f[i];
+            });
+        }
+    }
+
 
     if (a.counter != nullptr) {
         // Publish this block's peer stores at system scope, then take a ticket.
