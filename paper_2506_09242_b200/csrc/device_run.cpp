@@ -26,8 +26,11 @@ std::vector<std::pair<int64_t, int64_t>> balanced_partition(int64_t n, int k) {
 }
 
 DeviceRun::DeviceRun(std::array<int64_t, 3> dims, std::array<bool, 3> periodic, const DynamicsRegistry& reg, int q,
-                     int precision_bits, int slabs, const std::vector<int>& devices, int arith, int flags)
+                     int precision_bits, int slabs, const std::vector<int>& devices, int arith, int flags,
+                     int layout)
     : dims_(dims), periodic_(periodic), q_(q), bits_(precision_bits) {
+    if (layout == DLB_LAYOUT_AA && slabs != 1)
+        throw std::invalid_argument("the AA layout runs single-slab lattices (run.blocks 1,1,1)");
     parts_ = balanced_partition(dims[2], slabs);
     for (int k = 0; k < slabs; ++k) {
         dlb_lattice_desc d{};
@@ -37,7 +40,7 @@ DeviceRun::DeviceRun(std::array<int64_t, 3> dims, std::array<bool, 3> periodic, 
         for (int a = 0; a < 3; ++a) d.periodic[a] = periodic[std::size_t(a)];
         d.q = q;
         d.precision_bits = precision_bits;
-        d.layout = DLB_LAYOUT_TWO_POP;
+        d.layout = layout;
         d.arith = arith;
         d.device = devices.empty() ? 0 : devices[std::size_t(k) % devices.size()];
         d.z_origin = parts_[std::size_t(k)].first;

@@ -28,7 +28,7 @@ class DeviceRun {
   public:
     DeviceRun(std::array<int64_t, 3> dims, std::array<bool, 3> periodic, const DynamicsRegistry& reg, int q,
               int precision_bits, int slabs, const std::vector<int>& devices, int arith = DLB_ARITH_EXACT,
-              int flags = 0);
+              int flags = 0, int layout = DLB_LAYOUT_TWO_POP);
     DeviceRun(const DeviceRun&) = delete;
     DeviceRun& operator=(const DeviceRun&) = delete;
 

@@ -515,6 +515,9 @@ void Lattice::set_slots(const int32_t* slots) {
         uniform_slot_ = 0;
         slots_set_ = true;
         build_lists(u8);
+        // the list kernels carry their slot; the per-cell array serves the diagnostics
+        cuda_check(cudaMalloc(&d_slot_, std::size_t(n)), "cudaMalloc slots");
+        cuda_check(cudaMemcpy(d_slot_, u8.data(), std::size_t(n), cudaMemcpyHostToDevice), "upload slots");
         return;
     }
     build_fixups(u8);
@@ -1422,7 +1425,6 @@ void Lattice::checksum(unsigned long long* per_dir) {
 void Lattice::gather_macroscopic(double* rho, double* ux, double* uy, double* uz) {
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
     cuda_check(cudaStreamSynchronize(stream_), "sync");
-    if (sparse_) throw std::invalid_argument("gather_macroscopic: not available in the sparse porous mode");
     std::vector<MacroSlot> ms(std::max<std::size_t>(chains_.size(), 1));
     for (std::size_t s = 0; s < chains_.size(); ++s) {
         const LinkType t = chains_[s].links.back().type;

@@ -273,6 +273,15 @@ RunPlan resolve(const Config& config) {
             }
         }
     }
+    plan.layout_name = config.get_or("run.layout", "twopop");
+    if (plan.layout_name == "twopop") plan.layout = DLB_LAYOUT_TWO_POP;
+    else if (plan.layout_name == "aa") plan.layout = DLB_LAYOUT_AA;
+    else throw std::invalid_argument("unknown layout \"" + plan.layout_name + "\"; valid layouts: twopop, aa");
+    plan.porous_name = config.get_or("run.porous", "dense");
+    if (plan.porous_name == "dense") plan.flags = 0;
+    else if (plan.porous_name == "masked") plan.flags = DLB_FLAG_SKIP_NODYNAMICS;
+    else if (plan.porous_name == "lists") plan.flags = DLB_FLAG_SPARSE_LISTS;
+    else throw std::invalid_argument("unknown porous sweep \"" + plan.porous_name + "\"; valid sweeps: dense, masked, lists");
     {
         const std::string a = config.get_or("run.arith", "exact");
         if (a == "exact") plan.arith = DLB_ARITH_EXACT;
@@ -552,6 +561,8 @@ void Driver::write_manifest() const {
         m.set("run.devices", d);
     }
     if (plan_.arith == DLB_ARITH_FAST) m.set("run.arith", "fast");
+    if (plan_.layout == DLB_LAYOUT_AA) m.set("run.layout", "aa");
+    if (plan_.flags) m.set("run.porous", plan_.porous_name);
     std::string models;
     for (int t = 0; t < reg_.num_tags(); ++t) {
         if (!dispatch_.count(t)) continue;
@@ -645,7 +656,8 @@ RunArtifacts execute(const Config& config) {
         }
         for (int d = 0; d < n; ++d) devices.push_back(d);
     }
-    DeviceRun run(setup.dims, setup.periodic, reg, 19, cc.precision_bits, slabs, devices, plan.arith, 0);
+    DeviceRun run(setup.dims, setup.periodic, reg, 19, cc.precision_bits, slabs, devices, plan.arith, plan.flags,
+                  plan.layout);
     std::vector<int32_t> slots;
     if (!setup.chain_index.empty()) {
         slots.resize(setup.chain_index.size());

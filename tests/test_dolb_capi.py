@@ -270,3 +270,40 @@ def test_fast_arith_and_device_keys(api, tmp_path):
         text = fh.read()
     assert "arith = fast" in text and "devices = 0" in text
     shutil.rmtree(out)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,extra,dumps", [
+    ("sphere48_trt_f64", {"run.porous": "masked"}, False),   # NoDynamics segments skipped
+    ("sphere48_trt_f64", {"run.porous": "lists"}, False),
+    ("tgv16_bgk_f64", {"run.layout": "aa"}, True),             # in-place AA streaming
+    ("cavity16_trt_f32", {"run.layout": "aa"}, False),
+])
+def test_device_variants_keep_the_reference_series(api, name, extra, dumps, tmp_path):
+    """Device-runtime variants behind run.porous / run.layout: series.csv (and,
+    where every cell is updated, the DOLB1 dumps) stay byte-identical to the
+    reference's dolb_run -- the masked / sparse porous sweeps only leave
+    never-consumed solid-cell values stale, which the diagnostics never read."""
+    with open(os.path.join(GOLD, "index.json")) as fh:
+        want = json.load(fh)[name]
+    out = str(tmp_path / "v")
+    steps, _ = api.run(dict(resolve_paths(RUNNER_CASES[name], out), **extra))
+    assert steps == want["steps"]
+    with open(os.path.join(GOLD, name, "series.csv")) as a, open(os.path.join(out, "series.csv")) as b:
+        assert b.read() == a.read()
+    if dumps:
+        for dump, sha in want["dumps"].items():
+            assert _sha(os.path.join(out, dump)) == sha, dump
+    with open(os.path.join(out, "manifest")) as fh:
+        text = fh.read()
+    for k, v in extra.items():
+        assert f"{k.split('.')[1]} = {v}" in text
+
+
+def test_variant_keys_validated(api, tmp_path):
+    for key, bad, msg in (("run.layout", "soa", 'unknown layout "soa"'),
+                          ("run.porous", "holes", 'unknown porous sweep "holes"'),
+                          ("run.arith", "approx", 'unknown arithmetic mode "approx"')):
+        with pytest.raises(DolbError) as e:
+            api.run({key: bad, "run.out": str(tmp_path)})
+        assert e.value.status == CONFIG and msg in e.value.message
