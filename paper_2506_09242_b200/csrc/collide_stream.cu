@@ -560,6 +560,128 @@ __global__ void __launch_bounds__(BX * BY + 32, 1)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Row-staged TMA pull (dense two-population, single slab). Unit of work = one
+// x-row (y, z) of the output. For each direction i the producer warp loads the
+// WHOLE source row (y - c_y, z - c_z), x = -E .. nx + E, as nb boxes of bw
+// elements of a 3-D tensor map (x, row, direction) into one stage of an
+// S-deep shared-memory ring (mbarrier expect_tx) -- every source element is
+// fetched exactly once per step (the x shift of the pull is a shared-memory
+// offset, the y / z shifts select the row), so there are no halo re-reads.
+// The consumer warps walk the row, collide and store straight to HBM, then
+// release the stage. Periodic axes read the envelope, kept current by the
+// kernel itself (boundary cells push their outgoing links into the opposite
+// envelope of the output buffer, as in k_tma).
+template <typename T, int Q, unsigned KM, int NCW>
+__global__ void __launch_bounds__(NCW * 32 + 32, (NCW >= 16 ? 1 : 2))
+    k_tmarow(const __grid_constant__ StepArgs<T> a, const CUtensorMap* __restrict__ tin, int nb, int bw, int S,
+             int tw) {
+    using L = Lat<Q>;
+    constexpr int NT = NCW * 32;
+    constexpr int E = tma_pad<T>();
+    const Geo& g = a.g;
+    const int W = nb * bw;
+    const int stage = Q * W;
+    extern __shared__ __align__(128) unsigned char smem[];
+    T* ring = reinterpret_cast<T*>(smem);
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + size_t(S) * stage * sizeof(T));
+    unsigned long long* empty = full + S;
+    const int tid = threadIdx.x;
+    const int tiles_x = (g.nx + tw - 1) / tw;  // a work unit is tw cells of one row
+    const long long rows = static_cast<long long>(g.ny) * g.nz * tiles_x;
+    if (tid == 0) {
+        for (int st = 0; st < S; ++st) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(full + st)) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(empty + st)), "r"(NCW) : "memory");
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (tid >= NT) {  // ---- producer warp: lane i issues direction i's boxes (parallel TMA issue)
+        const int lane = tid - NT;
+        if (lane == 0)
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(tin)) : "memory");
+        const unsigned long long desc = reinterpret_cast<unsigned long long>(tin);
+        const unsigned bytes = unsigned(stage * sizeof(T));
+        int k = 0;
+        for (long long r = blockIdx.x; r < rows; r += gridDim.x, ++k) {
+            const int st = k % S;
+            if (k >= S) mbar_wait(smem_u32(empty + st), unsigned((k / S) - 1) & 1u);
+            const long long ry = r / tiles_x;
+            const int x0 = int(r - ry * tiles_x) * tw;
+            const int z = int(ry / g.ny), y = int(ry - static_cast<long long>(z) * g.ny);
+            const unsigned bar = smem_u32(full + st);
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+            __syncwarp();
+            const unsigned base = smem_u32(ring + size_t(st) * stage);
+            for (int i = lane; i < Q; i += 32) {
+                const int row = (z - kTmaC[i][2] + 1) * (g.ny + 2) + (y - kTmaC[i][1] + 1);
+#pragma unroll 1
+                for (int b = 0; b < nb; ++b) {
+                    const unsigned dst = base + unsigned((i * W + b * bw) * sizeof(T));
+                    asm volatile(
+                        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+                        "l"(desc), "r"(x0 + b * bw), "r"(row), "r"(i), "r"(bar)
+                        : "memory");
+                }
+            }
+        }
+        return;
+    }
+
+    // ---- consumer warps
+    int k = 0;
+    for (long long r = blockIdx.x; r < rows; r += gridDim.x, ++k) {
+        const int st = k % S;
+        const long long ry = r / tiles_x;
+        const int x0 = int(r - ry * tiles_x) * tw;
+        const int z = int(ry / g.ny), y = int(ry - static_cast<long long>(z) * g.ny);
+        const int x1 = min(g.nx, x0 + tw);
+        mbar_wait(smem_u32(full + st), unsigned(k / S) & 1u);
+        const T* srow = ring + size_t(st) * stage - x0;
+        for (int x = x0 + tid; x < x1; x += NT) {
+            T f[Q];
+            sfor<Q>([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                constexpr int cx = L::c[i][0];
+                f[i] = srow[i * W + x + E - cx];
+            });
+            int s = a.uniform_slot;
+            if (a.slot != nullptr) s = a.slot[(static_cast<long long>(z) * g.ny + y) * g.nx + x];
+            Cell<T, Q>::template apply<KM>(f, a.rec[s]);
+            const int center = z * g.plane + y * g.pitch + x;
+            sfor<Q>([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                a.fout[i][center] = f[i];
+            });
+            const bool bx_lo = g.per_x && x == 0, bx_hi = g.per_x && x == g.nx - 1;
+            const bool by_lo = g.per_y && y == 0, by_hi = g.per_y && y == g.ny - 1;
+            const bool bz_lo = g.per_z && z == 0, bz_hi = g.per_z && z == g.nz - 1;
+            if (bx_lo || bx_hi || by_lo || by_hi || bz_lo || bz_hi) {
+                sfor<Q>([&](auto I) {
+                    constexpr int i = decltype(I)::value;
+                    constexpr int cx = L::c[i][0], cy = L::c[i][1], cz = L::c[i][2];
+                    int X = x, Y = y, Z = z;
+                    bool moved = false;
+                    if (cx > 0 && bx_hi) { X = x - g.nx; moved = true; }
+                    if (cx < 0 && bx_lo) { X = x + g.nx; moved = true; }
+                    if (cy > 0 && by_hi) { Y = y - g.ny; moved = true; }
+                    if (cy < 0 && by_lo) { Y = y + g.ny; moved = true; }
+                    if (cz > 0 && bz_hi) { Z = z - g.nz; moved = true; }
+                    if (cz < 0 && bz_lo) { Z = z + g.nz; moved = true; }
+                    if (moved) a.fout[i][Z * g.plane + Y * g.pitch + X] = f[i];
+                });
+            }
+        }
+        __syncwarp();
+        if ((tid & 31) == 0)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(empty + st)) : "memory");
+    }
+}
+
 #define DLB_STR2(x) #x
 #define DLB_STR(x) DLB_STR2(x)
 #define ENTRY(T, Q, KM)                                                                  \
@@ -580,6 +702,17 @@ __global__ void __launch_bounds__(BX * BY + 32, 1)
     AA_PAIR(T, 19, KM_BGK), AA_PAIR(T, 19, KM_TRT), AA_PAIR(T, 19, KM_RR),               \
         AA_PAIR(T, 19, KM_TRT | KM_BB | KM_MBB), AA_PAIR(T, 19, KM_ALL), AA_PAIR(T, 27, KM_RR), \
         AA_PAIR(T, 27, KM_ALL)
+
+#define TMAROW_ENTRY1(T, Q, KM, NCW)                                                     \
+    KernelEntry {                                                                        \
+        int(sizeof(T) * 8), Q, unsigned(KM), LAYOUT_TMAROW,                               \
+            reinterpret_cast<const void*>(&k_tmarow<T, Q, unsigned(KM), NCW>),            \
+            "k_tmarow<" #T ",D3Q" #Q "," #KM ",w" #NCW ">[" DLB_STR(DLB_MODE) "]", 0, 0, 0, 1, NCW \
+    }
+#define TMAROW_ENTRY(T, Q, KM) TMAROW_ENTRY1(T, Q, KM, 16), TMAROW_ENTRY1(T, Q, KM, 8)
+#define TMAROW_SET(T)                                                                     \
+    TMAROW_ENTRY(T, 19, KM_BGK), TMAROW_ENTRY(T, 19, KM_TRT), TMAROW_ENTRY(T, 19, KM_BGK | KM_BB | KM_MBB), \
+        TMAROW_ENTRY(T, 19, KM_TRT | KM_BB | KM_MBB)
 
 #define SEG_ENTRY1(T, Q, KM, CPT)                                                        \
     KernelEntry {                                                                        \
@@ -645,7 +778,7 @@ __global__ void __launch_bounds__(BX * BY + 32, 1)
 static const KernelEntry kTable[] = {
     Q19_SET(float), Q19_SET(double), Q27_SET(float), Q27_SET(double), AA_SET(float), AA_SET(double),
     LIST_SET(float, 19), LIST_SET(double, 19), LIST_SET(float, 27), LIST_SET(double, 27),
-    TMA_SET, SEG_SET(float), SEG_SET(double),
+    TMA_SET, SEG_SET(float), SEG_SET(double), TMAROW_SET(float), TMAROW_SET(double),
 };
 
 const KernelEntry* kernel_table(int* n) {

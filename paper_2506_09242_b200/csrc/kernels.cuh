@@ -64,7 +64,7 @@ struct StepArgs {
 
 // kernel families: dense two-population, AA even / odd, sparse lists (fluid / masked walls)
 enum Layout : int { LAYOUT_TWO_POP = 0, LAYOUT_AA = 1, LAYOUT_AA_ODD = 2, LAYOUT_LIST = 3, LAYOUT_LIST_MASKED = 4,
-                    LAYOUT_TMA = 5, LAYOUT_SEG = 6 };
+                    LAYOUT_TMA = 5, LAYOUT_SEG = 6, LAYOUT_TMAROW = 7 };
 
 struct KernelEntry {
     int precision_bits;
@@ -75,6 +75,7 @@ struct KernelEntry {
     const char* name;
     int tile_x = 0, tile_y = 0, stages = 0;  // TMA kernels: tile shape and ring depth
     int cpt = 1;                             // segment kernels: cells per thread
+    int warps = 0;                           // row-staged TMA kernels: consumer warps per CTA
 };
 
 // Kernel tables of the two arithmetic modes (one translation unit each).

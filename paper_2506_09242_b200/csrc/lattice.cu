@@ -688,8 +688,47 @@ void Lattice::setup_tma() {
             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return;
     }
-    cuda_check(cudaMalloc(&d_tmap_, 2 * sizeof(CUtensorMap)), "cudaMalloc tensor maps");
-    cuda_check(cudaMemcpy(d_tmap_, tmap_, 2 * sizeof(CUtensorMap), cudaMemcpyHostToDevice), "tensor maps");
+    // Row-staged variant (k_tmarow, DLB_TMA_ROW != 0): the buffer as a 3-D
+    // tensor (x, row = (z + 1)(ny + 2) + y + 1, direction), boxes of row_bw_ x 1 x 1
+    // covering x = -e .. nx + e of one row in row_nb_ pieces.
+    const char* re = std::getenv("DLB_TMA_ROW");
+    row_ok_ = false;
+    if (!(re && re[0] == '0') && geo_.pitch >= geo_.nx + e + 1) {
+        // work unit = row_tw_ cells of one row, as many x-splits as it takes
+        // for two ring stages to fit the per-CTA budget (DLB_TMAROW_SMEM_KB)
+        const char* be = std::getenv("DLB_TMAROW_SMEM_KB");
+        const std::size_t budget = std::size_t(be ? std::atoi(be) : 200) << 10;
+        int splits = 1;
+        auto tile_w = [&](int sp) { return ((geo_.nx + sp - 1) / sp + 31) / 32 * 32; };
+        while (splits < 16 &&
+               std::size_t(2) * d_.q * std::size_t(tile_w(splits) + 2 * (128 / s)) * s > budget)
+            ++splits;
+        row_tw_ = splits == 1 ? geo_.nx : tile_w(splits);
+        const int span = row_tw_ + e + 1;
+        // TMA shared-memory destinations must be 128-B aligned: box widths are
+        // multiples of 128 B (elements past the row's pitch are zero-filled
+        // out-of-bounds reads, no HBM traffic)
+        const int al = 128 / s;
+        row_nb_ = (span + 255) / 256;
+        row_bw_ = ((span + row_nb_ - 1) / row_nb_ + al - 1) / al * al;
+        if (row_bw_ > 256) row_bw_ = 256, row_nb_ = (span + 255) / 256;
+        bool ok = true;
+        for (int b = 0; b < 2 && ok; ++b) {
+            char* base = static_cast<char*>(buf_[b]) + std::size_t(align_ - e) * s;
+            const cuuint64_t dims[3] = {cuuint64_t(geo_.pitch), cuuint64_t(geo_.ny + 2) * cuuint64_t(geo_.nz + 2),
+                                        cuuint64_t(d_.q)};
+            const cuuint64_t strides[2] = {cuuint64_t(geo_.pitch) * s, cuuint64_t(geo_.dstride) * s};
+            const cuuint32_t box[3] = {cuuint32_t(row_bw_), 1u, 1u};
+            const cuuint32_t estr[3] = {1u, 1u, 1u};
+            ok = reinterpret_cast<EncodeFn>(fn)(
+                     &tmap_[2 + b], s == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
+                     base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+        }
+        row_ok_ = ok;
+    }
+    cuda_check(cudaMalloc(&d_tmap_, 4 * sizeof(CUtensorMap)), "cudaMalloc tensor maps");
+    cuda_check(cudaMemcpy(d_tmap_, tmap_, 4 * sizeof(CUtensorMap), cudaMemcpyHostToDevice), "tensor maps");
     tma_xoff_ = e;
     tma_ok_ = true;
 }
@@ -708,6 +747,34 @@ template <typename T>
 void Lattice::launch_tma(StepArgs<T>& a, int parity) {
     const KernelEntry* k = kernel_tma_;
     const int e = int(16 / sizeof(T));
+    if (k->layout == LAYOUT_TMAROW) {
+        const std::size_t stage = std::size_t(d_.q) * row_nb_ * row_bw_ * sizeof(T);
+        // two ring stages per CTA by default (DLB_TMAROW_STAGES); one CTA of a
+        // producer warp + 16 consumer warps (96 registers) per SM
+        static const int stages_env = [] {
+            const char* e = std::getenv("DLB_TMAROW_STAGES");
+            return e ? std::max(2, std::atoi(e)) : 2;
+        }();
+        const int S = stages_env;
+        const std::size_t smem = std::size_t(S) * stage + std::size_t(2 * S) * 8 + 128;
+        if (tma_grid_ == 0) {
+            cuda_check(cudaFuncSetAttribute(k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
+                       "smem attr");
+            int sms = 0, per_sm = 0;
+            cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_), "sm count");
+            cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k->fn, k->warps * 32 + 32, smem),
+                       "occupancy");
+            tma_grid_ = std::max(1, per_sm) * sms;
+        }
+        if (!envelope_valid_) refresh_envelope(parity);
+        const CUtensorMap* map = d_tmap_ + 2 + parity;
+        int nb = row_nb_, bw = row_bw_, ns = S, tw = row_tw_;
+        void* args[] = {&a, &map, &nb, &bw, &ns, &tw};
+        cuda_check(cudaLaunchKernel(k->fn, dim3(unsigned(tma_grid_)), dim3(unsigned(k->warps * 32 + 32)), args, smem,
+                                    stream_), "launch tma rows");
+        envelope_valid_ = true;
+        return;
+    }
     const std::size_t smem = std::size_t(k->stages) * d_.q * (k->tile_x + 2 * e) * k->tile_y * sizeof(T) + 128;
     if (tma_grid_ == 0) {
         cuda_check(cudaFuncSetAttribute(k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "smem attr");
@@ -784,8 +851,24 @@ void Lattice::select_kernel() {
     }
     kernel_tma_ = nullptr;
     tma_grid_ = 0;
-    if (tma_ok_ && fixups_.empty() && !(km_needed_ & KM_SKIP))
-        kernel_tma_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_, LAYOUT_TMA);
+    if (tma_ok_ && fixups_.empty() && !(km_needed_ & KM_SKIP)) {
+        const std::size_t stage = std::size_t(d_.q) * row_nb_ * row_bw_ * std::size_t(d_.precision_bits / 8);
+        if (row_ok_ && 2 * stage <= (std::size_t(200) << 10)) {
+            kernel_tma_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_, LAYOUT_TMAROW);
+            // rows short enough for two 2-stage CTAs per SM: 8 consumer warps each
+            // (c3 512-wide rows: 0.75 vs 0.55 of copy bandwidth with one 16-warp CTA)
+            const int want = 4 * stage + 1024 <= (std::size_t(220) << 10) ? 8 : 16;
+            if (kernel_tma_ && kernel_tma_->warps != want) {
+                int nt = 0;
+                const KernelEntry* t = d_.arith == DLB_ARITH_FAST ? fast::kernel_table(&nt) : exact::kernel_table(&nt);
+                for (int k = 0; k < nt; ++k)
+                    if (t[k].layout == LAYOUT_TMAROW && t[k].km == kernel_tma_->km && t[k].warps == want &&
+                        t[k].precision_bits == kernel_tma_->precision_bits && t[k].q == kernel_tma_->q)
+                        kernel_tma_ = &t[k];
+            }
+        }
+        if (!kernel_tma_) kernel_tma_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_, LAYOUT_TMA);
+    }
 }
 
 void Lattice::set_dispatch(const int32_t* tags, std::size_t n) {

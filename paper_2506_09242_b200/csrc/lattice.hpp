@@ -176,7 +176,10 @@ class Lattice {
     // TMA-staged dense kernel (single slab): tensor maps of both buffers, and
     // whether the input buffer's envelope holds the periodic images
     const KernelEntry* kernel_tma_ = nullptr;
-    CUtensorMap tmap_[2];
+    CUtensorMap tmap_[4];            // [0..1] box maps (k_tma), [2..3] row maps (k_tmarow)
+    bool row_ok_ = false;
+    int row_nb_ = 0, row_bw_ = 0;    // k_tmarow: boxes per tile and box width (elements)
+    int row_tw_ = 0;                 // k_tmarow: cells per work unit (a row or an x-split of it)
     CUtensorMap* d_tmap_ = nullptr;  // the two maps in device global memory
     int tma_xoff_ = 0;
     bool tma_ok_ = false;

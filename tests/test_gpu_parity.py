@@ -539,7 +539,7 @@ def test_tma_and_plain_kernels_bit_identical_to_reference(golden, name):
         run.advance(steps)
         assert canonical_hash(run.gather_populations()) == golden[name]["sha256"], run.kernel_name()
         names.append(run.kernel_name())
-    assert "k_tma" in names[0] and "k_pull" in names[1]
+    assert "k_tma" in names[0] and "k_pull" in names[1]  # k_tmarow (row-staged) or k_tma (box-tiled)
 
 
 def test_tma_d3q27_rr(oracle):
