@@ -252,6 +252,13 @@ DLB_API dlb_status dlb_tree_plan(int64_t n_total, int64_t seg_begin, int64_t seg
                                  dlb_tree_part* parts, size_t cap, size_t* n_out);
 /* Host: diag::tree_sum (diagnostics.cpp:10-18) of a host array. */
 DLB_API dlb_status dlb_tree_sum(const double* values, int64_t n, double* sum_out);
+/* Fused collide + reduce (the paper's transform_reduce): the LAST
+ * step of the next dlb_lattice_step call also writes the new state's per-cell
+ * kinetic energy, so the following DLB_Q_KINETIC reduction reads 8 B/cell
+ * instead of the populations (bit-identical values). *fused_out = 0 when the
+ * lattice has no fused variant (fast arithmetic, AA, z-slab, regularized
+ * fix-ups); the reduction then runs unfused. */
+DLB_API dlb_status dlb_lattice_request_kinetic(dlb_lattice* lat, int32_t* fused_out);
 /* Keep the current velocity field on the device as the DU_NUM reference
  * (the runner's prev_ux/uy/uz, runner.cpp:445-448). */
 DLB_API dlb_status dlb_lattice_snapshot_velocity(dlb_lattice* lat);

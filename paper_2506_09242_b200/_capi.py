@@ -118,6 +118,7 @@ _SIGS = {
     "dlb_tree_plan": ([C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
     "dlb_tree_sum": ([C.c_void_p, C.c_int64, C.POINTER(C.c_double)], C.c_int),
     "dlb_lattice_snapshot_velocity": ([C.c_void_p], C.c_int),
+    "dlb_lattice_request_kinetic": ([C.c_void_p, C.POINTER(C.c_int32)], C.c_int),
     "dlb_lattice_velocity_planes": ([C.c_void_p, C.c_int32, C.c_int32, C.c_void_p], C.c_int),
     "dlb_lattice_step_bytes": ([C.c_void_p, C.POINTER(C.c_int64)], C.c_int),
     "dlb_lattice_time_steps": ([C.c_void_p, C.c_int64, C.POINTER(C.c_double)], C.c_int),

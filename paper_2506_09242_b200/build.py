@@ -39,7 +39,7 @@ HEADERS = ["lbm_cell.cuh", "kernels.cuh", "chain.hpp", "lattice.hpp", "canon.cuh
 
 UNITS = [
     # (source, object, extra flags)
-    ("collide_stream.cu", "collide_stream_exact.o", ["-fmad=false", "-DDLB_MODE=exact"]),
+    ("collide_stream.cu", "collide_stream_exact.o", ["-fmad=false", "-DDLB_MODE=exact", "-DDLB_FUSED_KE"]),
     ("collide_stream.cu", "collide_stream_fast.o", ["-fmad=true", "-DDLB_MODE=fast"]),
     ("lattice.cu", "lattice.o", ["-fmad=false"]),
     ("diag.cu", "diag.o", ["-fmad=false"]),

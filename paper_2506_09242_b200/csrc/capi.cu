@@ -345,6 +345,14 @@ DLB_API dlb_status dlb_tree_sum(const double* values, int64_t n, double* sum_out
     return guarded([&] { *sum_out = dlb::tree_sum_host(values, n); });
 }
 
+DLB_API dlb_status dlb_lattice_request_kinetic(dlb_lattice* lat, int32_t* fused_out) {
+    DLB_REQUIRE(lat);
+    return guarded([&] {
+        const bool f = lat->lat->request_kinetic();
+        if (fused_out) *fused_out = f ? 1 : 0;
+    });
+}
+
 DLB_API dlb_status dlb_lattice_snapshot_velocity(dlb_lattice* lat) {
     DLB_REQUIRE(lat);
     return guarded([&] { lat->lat->snapshot_velocity(); });

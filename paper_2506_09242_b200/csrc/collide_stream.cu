@@ -152,13 +152,36 @@ __global__ void __launch_bounds__(256, (min_blocks<T, Q, KM>())) k_pull(const __
         if constexpr ((KM & KM_SKIP) == 0) {
             if (a.slot != nullptr) s = a.slot[(static_cast<long long>(z) * g.ny + y) * g.nx + x];
         }
-        Cell<T, Q>::template apply<KM & ~KM_SKIP>(f, a.rec[s]);
+        Cell<T, Q>::template apply<KM & ~(KM_SKIP | KM_KE)>(f, a.rec[s]);
 
         const int center = z * g.plane + y * g.pitch + x;
         sfor<Q>([&](auto I) {
             constexpr int i = decltype(I)::value;
             a.fout[i][center] = f[i];
         });
+        if constexpr ((KM & KM_KE) != 0) {
+            // Fused reduce input (the paper's transform_reduce): the
+            // kinetic energy of the state just stored, with gather_macroscopic's
+            // semantics (multiblock.cpp:458-478: rho / u in double from the
+            // stored T values; wall velocity on moving walls; 0 elsewhere) and
+            // diag::kinetic_energy's expression (diagnostics.cpp:28).
+            const DevRecipe<T>& r = a.rec[s];
+            double u[3] = {0.0, 0.0, 0.0};
+            if (r.kind == KIND_COLLIDE) {
+                double fd[Q];
+                sfor<Q>([&](auto I) {
+                    constexpr int i = decltype(I)::value;
+                    fd[i] = double(f[i]);
+                });
+                double rho;
+                Cell<double, Q>::rho_u(fd, rho, u);
+            } else if (r.kind == KIND_MBB) {
+                u[0] = double(r.wall_velocity[0]);
+                u[1] = double(r.wall_velocity[1]);
+                u[2] = double(r.wall_velocity[2]);
+            }
+            a.ke[(static_cast<long long>(z) * g.ny + y) * g.nx + x] = 0.5 * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+        }
 
         if (a.push_up != nullptr && z == g.nz - 1) {
             const int ghost = -g.plane + y * g.pitch + x;
@@ -775,10 +798,22 @@ __global__ void __launch_bounds__(NCW * 32 + 32, (NCW >= 16 ? 1 : 2))
 #define Q27_SET(T) ENTRY(T, 27, KM_BGK), ENTRY(T, 27, KM_TRT), ENTRY(T, 27, KM_RR), ENTRY(T, 27, KM_ALL), \
         ENTRY(T, 27, KM_ALL | KM_SKIP)
 
+// fused kinetic-energy variants: exact mode only (the reduce input must carry
+// the diagnostics' non-contracted double arithmetic)
+#ifdef DLB_FUSED_KE
+#define KE_SET(T)                                                                         \
+    , ENTRY(T, 19, KM_BGK | KM_KE), ENTRY(T, 19, KM_TRT | KM_KE), ENTRY(T, 19, KM_RR | KM_KE), \
+        ENTRY(T, 19, KM_BGK | KM_LES | KM_KE), ENTRY(T, 19, KM_TRT | KM_LES | KM_KE),   \
+        ENTRY(T, 19, KM_BGK | KM_BB | KM_MBB | KM_KE), ENTRY(T, 19, KM_TRT | KM_BB | KM_MBB | KM_KE), \
+        ENTRY(T, 19, KM_RR | KM_BB | KM_MBB | KM_KE)
+#else
+#define KE_SET(T)
+#endif
+
 static const KernelEntry kTable[] = {
     Q19_SET(float), Q19_SET(double), Q27_SET(float), Q27_SET(double), AA_SET(float), AA_SET(double),
     LIST_SET(float, 19), LIST_SET(double, 19), LIST_SET(float, 27), LIST_SET(double, 27),
-    TMA_SET, SEG_SET(float), SEG_SET(double), TMAROW_SET(float), TMAROW_SET(double),
+    TMA_SET, SEG_SET(float), SEG_SET(double), TMAROW_SET(float), TMAROW_SET(double) KE_SET(float) KE_SET(double)
 };
 
 const KernelEntry* kernel_table(int* n) {

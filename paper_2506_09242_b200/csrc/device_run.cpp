@@ -75,9 +75,10 @@ void DeviceRun::exchange() {
     for (auto& s : slabs_) s->exchange();
 }
 
-void DeviceRun::advance(int64_t nsteps) {
+void DeviceRun::advance(int64_t nsteps, bool kinetic_last) {
     if (nsteps <= 0) return;
     if (slabs_.size() == 1) {
+        if (kinetic_last) slabs_.front()->request_kinetic();
         slabs_.front()->step(nsteps);
     } else {
         // eager dispatch check on every slab before any of them writes

@@ -37,7 +37,9 @@ class DeviceRun {
     void fill(const std::vector<int32_t>& slot_of_cell, int32_t uniform_slot, const CaseSetup& setup);
     void set_dispatch(const std::set<int>& tags);
     void exchange();
-    void advance(int64_t nsteps);
+    // kinetic_last: fuse the kinetic-energy values into the last step (single
+    // slab; multi-slab runs reduce unfused)
+    void advance(int64_t nsteps, bool kinetic_last = false);
     void synchronize();
 
     std::vector<double> gather_populations();

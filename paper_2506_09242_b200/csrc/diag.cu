@@ -457,6 +457,10 @@ void Lattice::diag_impl(const dlb_reduce_args& a, int64_t n_total, int64_t seg_b
             cnt = static_cast<long long>(box.x1 - box.x0) * (box.y1 - box.y0) * nzc;
             k_enstrophy_values<<<grid_of(cnt), 256, 0, stream_>>>(U, nx, ny, box.x0, box.x1, box.y0, box.y1, nzc, val);
             cuda_check(cudaGetLastError(), "k_enstrophy_values");
+        } else if (q == DLB_Q_KINETIC && kinetic_fused_current()) {
+            // the collide-stream kernel already wrote these values (KM_KE variant)
+            val = d_ke_ + za * pc;
+            cnt = row * nzc;
         } else {
             const long long n = row * nzc;
             val = reinterpret_cast<double*>(p);

@@ -60,6 +60,9 @@ struct StepArgs {
     unsigned long long* sig_up;
     unsigned long long* sig_down;
     DevRecipe<T> rec[kMaxSlots];
+    // KM_KE variant: per-cell kinetic energy of the new state, x fastest
+    // (appended last so the other kernels' parameter offsets do not move)
+    double* ke;
 };
 
 // kernel families: dense two-population, AA even / odd, sparse lists (fluid / masked walls)

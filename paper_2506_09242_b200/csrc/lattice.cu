@@ -245,7 +245,7 @@ const KernelEntry* find_kernel(int arith, int bits, int q, unsigned km, int layo
     for (int k = 0; k < n; ++k) {
         const KernelEntry& e = t[k];
         if (e.precision_bits != bits || e.q != q || e.layout != layout) continue;
-        if ((e.km & km) != km || (e.km & KM_SKIP) != (km & KM_SKIP)) continue;
+        if ((e.km & km) != km || (e.km & (KM_SKIP | KM_KE)) != (km & (KM_SKIP | KM_KE))) continue;
         if (!best || __builtin_popcount(e.km) < __builtin_popcount(best->km)) best = &e;
     }
     return best;
@@ -396,6 +396,7 @@ Lattice::~Lattice() {
     cudaFree(d_slot_);
     cudaFree(d_list_);
     cudaFree(d_seg_);
+    cudaFree(d_ke_);
     cudaFree(d_fix_);
     cudaFree(d_tmap_);
     cudaFree(d_flags_);
@@ -849,6 +850,12 @@ void Lattice::select_kernel() {
                     kernel_seg_ = &t[k];
         }
     }
+    // fused kinetic-energy variant of the dense sweep (exact mode, single
+    // two-population slab, no regularized fix-ups): used for the steps a
+    // kinetic-energy reduction is requested for (request_kinetic)
+    kernel_ke_ = nullptr;
+    if (!aa() && !split() && fixups_.empty() && !(km_needed_ & KM_SKIP) && d_.arith == DLB_ARITH_EXACT)
+        kernel_ke_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_ | KM_KE, LAYOUT_TWO_POP);
     kernel_tma_ = nullptr;
     tma_grid_ = 0;
     if (tma_ok_ && fixups_.empty() && !(km_needed_ & KM_SKIP)) {
@@ -1324,7 +1331,7 @@ void Lattice::launch_step(int parity) {
         aa_odd_layout_ = !aa_odd_layout_;
         return;
     }
-    if (!linked && kernel_tma_) {
+    if (!linked && kernel_tma_ && !(ke_requested_ && kernel_ke_)) {
         launch_tma<T>(a, parity);
         return;
     }
@@ -1345,6 +1352,16 @@ void Lattice::launch_step(int parity) {
             const long long per_block = 256LL * kernel_seg_->cpt;
             cuda_check(cudaLaunchKernel(kernel_seg_->fn, dim3(unsigned((threads + per_block - 1) / per_block)),
                                         dim3(256), sargs, 0, stream_), "launch segments");
+        } else if (ke_requested_ && kernel_ke_) {
+            if (!d_ke_) {
+                cuda_check(cudaMalloc(&d_ke_, std::size_t(cells()) * sizeof(double)), "cudaMalloc kinetic energy");
+                device_bytes_ += cells() * int64_t(sizeof(double));
+            }
+            a.ke = d_ke_;
+            cuda_check(cudaLaunchKernel(kernel_ke_->fn, dim3(gx, gy, geo_.nz), block, args, 0, stream_),
+                       "launch fused kinetic energy");
+            ke_requested_ = false;
+            ke_step_ = steps_ + 1;  // valid for the state after this step
         } else {
             cuda_check(cudaLaunchKernel(split_rare ? kernel_main_->fn : fn, dim3(gx, gy, geo_.nz), block, args, 0,
                                         stream_), "launch");
@@ -1436,10 +1453,21 @@ void Lattice::ensure_graph() {
 // Steps are replayed as a CUDA graph of two consecutive steps (launch latency
 // and host overhead amortised; the halo wait / push / signal nodes are
 // device-side, so linked slabs replay safely too).
+bool Lattice::request_kinetic() {
+    if (!kernel_ke_ || lower_.linked || upper_.linked) return false;
+    ke_requested_ = true;
+    return true;
+}
+
 void Lattice::step(int64_t nsteps) {
     if (nsteps <= 0) return;
     check_dispatch();
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    // a requested fused kinetic energy belongs to the LAST step of this call;
+    // the others (and any captured graph) run the plain kernel
+    const bool ke_last = ke_requested_;
+    ke_requested_ = false;
+    if (ke_last) --nsteps;
     int64_t k = 0;
     if (nsteps >= 4) {
         const bool aligned = aa() ? aa_odd_layout_ : cur_ == 0;
@@ -1454,6 +1482,11 @@ void Lattice::step(int64_t nsteps) {
         }
     }
     for (; k < nsteps; ++k) enqueue_step();
+    if (ke_last) {
+        ke_requested_ = true;
+        enqueue_step();
+        ke_requested_ = false;
+    }
 }
 
 // MultiBlockRun::exchange (multiblock.hpp:142-143) for a z-slab: copy this

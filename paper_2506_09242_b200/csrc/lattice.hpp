@@ -102,6 +102,12 @@ class Lattice {
     void reduce_parts(const dlb_reduce_args& a, int64_t n_total, int64_t seg_begin,
                       std::vector<dlb_tree_part>& out);
     void snapshot_velocity();
+    // The next step also writes the new state's per-cell kinetic energy (one
+    // 8-B store per cell in the collide-stream kernel), so the following
+    // DLB_Q_KINETIC reduction reads 8 B/cell instead of the populations.
+    // Returns false when this lattice has no fused variant (reduction unfused).
+    bool request_kinetic();
+    bool kinetic_fused_current() const { return d_ke_ && ke_step_ == steps_; }
     void velocity_planes(int z0, int nz, double* out);
 
   private:
@@ -127,6 +133,12 @@ class Lattice {
     unsigned* d_seg_ = nullptr;
     long long nseg_ = 0;
     const KernelEntry* kernel_seg_ = nullptr;
+    // fused kinetic energy (KM_KE variant): per-cell values of the state after
+    // step ke_step_, consumed by the next DLB_Q_KINETIC reduction
+    const KernelEntry* kernel_ke_ = nullptr;
+    double* d_ke_ = nullptr;
+    bool ke_requested_ = false;
+    int64_t ke_step_ = -1;
     long long base_off_ = 0;    // elements from array start to the interior origin
     void* buf_[2] = {nullptr, nullptr};
     int cur_ = 0;               // buffer holding the current state (f_in)

@@ -114,6 +114,7 @@ enum : unsigned {
     KM_LES = 64u, KM_REGV = 128u, KM_REGP = 256u,
     KM_ALL = 511u,
     KM_SKIP = 512u,  // variant flag: NoDynamics cells skipped (no loads / stores)
+    KM_KE = 1024u,   // variant flag: also write the new state's per-cell kinetic energy (fused reduce input)
 };
 
 template <typename T, int Q>

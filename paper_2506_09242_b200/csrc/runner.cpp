@@ -594,8 +594,8 @@ RunArtifacts Driver::execute() {
     while (step < limit) {
         const int64_t chunk = std::min(plan_.output_every, limit - step);
         const auto t0 = std::chrono::steady_clock::now();
-        run_.advance(chunk);
-        run_.synchronize();  // the chunk's device work is inside the timed region
+        run_.advance(chunk, true);  // the sample's kinetic energy fused into the chunk's last step
+        run_.synchronize();         // the chunk's device work is inside the timed region
         seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         step += chunk;
         sample(step);

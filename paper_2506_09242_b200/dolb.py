@@ -645,6 +645,16 @@ class DeviceRun:
         """diag::enstrophy(diag::vorticity_fd8(u, periodic)) (diagnostics.cpp:65-120)."""
         return self._tree_mean(_capi.Q_ENSTROPHY)
 
+    def request_kinetic(self) -> bool:
+        """Fuse the next kinetic-energy reduction into the last step of the next
+        advance() (dlb_lattice_request_kinetic); False when unfused."""
+        fused = True
+        for s in self.slabs:
+            f = C.c_int32()
+            check(_capi.lib().dlb_lattice_request_kinetic(s.handle, C.byref(f)))
+            fused = fused and bool(f.value)
+        return fused
+
     def snapshot_velocity(self):
         """Keep the current velocity on the device (the runner's prev_u, runner.cpp:445-448)."""
         for s in self.slabs:

@@ -229,3 +229,40 @@ def test_du_without_snapshot_is_an_error():
     run, _ = product_run("tgv16_bgk_f64")
     with pytest.raises(dlb.DlbError):
         run.tree_reduce(_capi.Q_DU_NUM)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,fused", [("tgv16_bgk_f64", True), ("tgv12_bgk_f32", True), ("tgv32_rr_f64", True),
+                                        ("tgv24_smag_trt_f32", True), ("tgv128_bgk_f32_c5", True),
+                                        ("cavity64_bgk_f64_c1", True), ("cavity32_trt_f32", True),
+                                        ("cavity24_rr_f64", True), ("plates16_trt_vel_f64", False)])
+def test_fused_kinetic_energy_bit_identical(name, fused):
+    """Fused collide + reduce (dlb_lattice_request_kinetic): the last step of
+    the advance writes the per-cell kinetic energy, the reduction reads those
+    values -- the same bits as the unfused sampling and the reference's
+    diag::kinetic_energy. Regularized inlet / outlet lattices (fix-up lists)
+    fall back to the unfused path."""
+    a, b = DIAG_CASES[name]
+    run, _ = product_run(name, 1, "twopop")
+    run.advance(a)
+    assert run.request_kinetic() == fused
+    run.advance(b)
+    k = run.kinetic_energy()
+    assert bits(k) == bits(float.fromhex(load_golden()[name]["values"]["k"]))
+    # the values belong to that state only: after one more step the reduction is unfused again
+    run.advance(1)
+    k1 = run.kinetic_energy()
+    run2, _ = product_run(name, 1, "twopop")
+    run2.advance(a + b + 1)
+    assert bits(k1) == bits(run2.kinetic_energy())
+
+
+@pytest.mark.gpu
+def test_fused_kinetic_energy_unavailable_paths():
+    """fast arithmetic, the AA layout and z-slabs have no fused variant."""
+    name = "tgv16_bgk_f64"
+    for kw in ({"layout": "aa"}, {"slabs": 2}):
+        run, _ = product_run(name, kw.get("slabs", 1), kw.get("layout", "twopop"))
+        assert not run.request_kinetic()
+        run.advance(10)
+        assert bits(run.kinetic_energy()) == bits(float.fromhex(load_golden()[name]["values"]["k"]))
