@@ -813,6 +813,8 @@ void Lattice::set_uniform_slot(int32_t slot) {
 
 void Lattice::select_kernel() {
     invalidate_graph();
+    kernel_ke_ = nullptr;
+    ke_requested_ = false;
     if (sparse_) return;
     km_needed_ = 0;
     for (int32_t s : present_slots_) km_needed_ |= kind_bits(chains_[std::size_t(s)]);
