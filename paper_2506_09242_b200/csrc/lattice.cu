@@ -866,7 +866,9 @@ void Lattice::select_kernel() {
             kernel_tma_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_, LAYOUT_TMAROW);
             // rows short enough for two 2-stage CTAs per SM: 8 consumer warps each
             // (c3 512-wide rows: 0.75 vs 0.55 of copy bandwidth with one 16-warp CTA)
-            const int want = 4 * stage + 1024 <= (std::size_t(220) << 10) ? 8 : 16;
+            const char* se = std::getenv("DLB_TMAROW_STAGES");
+            const std::size_t ring = std::size_t(se ? std::max(2, std::atoi(se)) : 2) * stage + 1024;
+            const int want = 2 * ring <= (std::size_t(220) << 10) ? 8 : 16;
             if (kernel_tma_ && kernel_tma_->warps != want) {
                 int nt = 0;
                 const KernelEntry* t = d_.arith == DLB_ARITH_FAST ? fast::kernel_table(&nt) : exact::kernel_table(&nt);
