@@ -32,6 +32,7 @@ struct CaseConfig {
     double lambda = 3.0 / 16.0;
     double omega_bulk_ho = 1.0;
     int precision_bits = 64;
+    int q = 19;  // device-runtime extension (case.lattice = d3q27): the reference is D3Q19 only
     std::array<int, 3> block_grid = {1, 1, 1};
     int workers = 1;
     // porous

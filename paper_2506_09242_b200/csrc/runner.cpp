@@ -222,6 +222,14 @@ RunPlan resolve(const Config& config) {
     }
     cc.geometry = config.get_or("case.geometry", "");
     cc.plate_layers = parse_int(config, "case.H", 11);
+    {
+        const std::string lat = config.get_or("case.lattice", "d3q19");
+        if (lat == "d3q19") cc.q = 19;
+        else if (lat == "d3q27") cc.q = 27;
+        else throw std::invalid_argument("unknown lattice \"" + lat + "\"; valid lattices: d3q19, d3q27");
+        if (cc.q == 27 && cc.kind == CaseKind::Porous)
+            throw std::invalid_argument("case.lattice d3q27: porous media use the D3Q19 wall classification");
+    }
     cc.tau = parse_double(config, "case.tau", 1.0);
     cc.delta_rho = parse_double(config, "case.delta_rho", 2e-3);
     cc.upstream = parse_int(config, "case.upstream", 40);
@@ -526,6 +534,7 @@ void Driver::write_manifest() const {
     m.set("case.lambda", g17(cc.lambda));
     m.set("case.omega_bulk_ho", g17(cc.omega_bulk_ho));
     m.set("case.precision", cc.precision_bits == 32 ? "f32" : "f64");
+    if (cc.q == 27) m.set("case.lattice", "d3q27");
     if (cc.kind == CaseKind::Porous) {
         m.set("case.drive", cc.drive == DriveKind::Velocity ? "velocity" : "pressure");
         m.set("case.geometry", cc.geometry);
@@ -656,7 +665,7 @@ RunArtifacts execute(const Config& config) {
         }
         for (int d = 0; d < n; ++d) devices.push_back(d);
     }
-    DeviceRun run(setup.dims, setup.periodic, reg, 19, cc.precision_bits, slabs, devices, plan.arith, plan.flags,
+    DeviceRun run(setup.dims, setup.periodic, reg, cc.q, cc.precision_bits, slabs, devices, plan.arith, plan.flags,
                   plan.layout);
     std::vector<int32_t> slots;
     if (!setup.chain_index.empty()) {

@@ -307,3 +307,33 @@ def test_variant_keys_validated(api, tmp_path):
         with pytest.raises(DolbError) as e:
             api.run({key: bad, "run.out": str(tmp_path)})
         assert e.value.status == CONFIG and msg in e.value.message
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("bits", [64, 32])
+def test_d3q27_through_dolb_run(api, oracle, bits, tmp_path):
+    """Config 2's lattice through the public API (case.lattice = d3q27, a
+    device-runtime extension: the reference is D3Q19 only): the DOLB1 dump of
+    a TGV RR run equals the oracle's D3Q27 restatement bit for bit."""
+    import numpy as np
+    from paper_2506_09242_b200.dolb import read_field_dump
+    from pyoracle import RR, Case
+    out = str(tmp_path / "q27")
+    steps, _ = api.run({"case.kind": "tgv", "case.L": "16", "case.Re": "400", "case.Ma": "0.1",
+                        "case.collision": "rr", "case.lattice": "d3q27", "case.precision": f"f{bits}",
+                        "run.tmax": "20", "run.output_every": "10", "run.dump_every": "20", "run.out": out})
+    assert steps == 20
+    dims, prec, got = read_field_dump(os.path.join(out, "dump_00000020.dolb"))
+    assert dims == (16, 16, 16) and prec == bits // 8
+    dt = np.float64 if bits == 64 else np.float32
+    want = oracle.run_case(Case(kind="tgv", L=16, Re=400.0, Ma=0.1, collision=RR, q=27), dt, 20)
+    assert np.array_equal(got, np.asarray(want, np.float64).reshape(-1))
+    with open(os.path.join(out, "manifest")) as fh:
+        assert "lattice = d3q27" in fh.read()
+
+
+def test_d3q27_porous_rejected(api, tmp_path):
+    with pytest.raises(DolbError) as e:
+        api.run({"case.kind": "porous", "case.geometry": "plates", "case.lattice": "d3q27",
+                 "run.out": str(tmp_path)})
+    assert e.value.status == CONFIG and "d3q27" in e.value.message
