@@ -805,7 +805,7 @@ __global__ void __launch_bounds__(NCW * 32 + 32, (NCW >= 16 ? 1 : 2))
     , ENTRY(T, 19, KM_BGK | KM_KE), ENTRY(T, 19, KM_TRT | KM_KE), ENTRY(T, 19, KM_RR | KM_KE), \
         ENTRY(T, 19, KM_BGK | KM_LES | KM_KE), ENTRY(T, 19, KM_TRT | KM_LES | KM_KE),   \
         ENTRY(T, 19, KM_BGK | KM_BB | KM_MBB | KM_KE), ENTRY(T, 19, KM_TRT | KM_BB | KM_MBB | KM_KE), \
-        ENTRY(T, 19, KM_RR | KM_BB | KM_MBB | KM_KE)
+        ENTRY(T, 19, KM_RR | KM_BB | KM_MBB | KM_KE), ENTRY(T, 27, KM_RR | KM_KE), ENTRY(T, 27, KM_BGK | KM_KE)
 #else
 #define KE_SET(T)
 #endif

@@ -266,3 +266,23 @@ def test_fused_kinetic_energy_unavailable_paths():
         assert not run.request_kinetic()
         run.advance(10)
         assert bits(run.kinetic_energy()) == bits(float.fromhex(load_golden()[name]["values"]["k"]))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("bits", [64, 32])
+def test_fused_kinetic_energy_d3q27(oracle, bits):
+    """D3Q27 RR (config 2's lattice): fused kinetic energy equals the unfused reduction."""
+    import numpy as np
+    import paper_2506_09242_b200 as dlb
+    cfg = dlb.CaseConfig(kind="tgv", L=24, Re=1600.0, Ma=0.2, collision=dlb.LinkType.RR, q=27)
+    setup = dlb.init_tgv(cfg)
+    a = dlb.build_run(setup, precision=bits)
+    b = dlb.build_run(setup, precision=bits)
+    a.advance(7)
+    assert b.request_kinetic()
+    b.advance(7)
+    assert bits_(a.kinetic_energy()) == bits_(b.kinetic_energy())
+
+
+def bits_(x: float) -> int:
+    return struct.unpack("<q", struct.pack("<d", x))[0]
