@@ -420,9 +420,10 @@ class DeviceRun:
         """MultiBlockRun::fill analogue: slot_of array/scalar, state = ('tgv', L, u) | ('rest',) |
         (rho, ux, uy, uz) arrays."""
         self.fill_slots(slot_of)
-        if isinstance(state, tuple) and state and state[0] == "tgv":
+        tag = state[0] if isinstance(state, tuple) and state and isinstance(state[0], str) else None
+        if tag == "tgv":
             self.fill_tgv(state[1], state[2])
-        elif isinstance(state, tuple) and state and state[0] == "rest":
+        elif tag == "rest":
             self.fill_state()
         else:
             self.fill_state(*state)
