@@ -134,3 +134,27 @@ def test_ragged_porous_variants(dims, periodic, variant, monkeypatch):
                     sparse_lists=variant == "lists")
     run.fill(slot, state)
     compare(run, recipes, slot, dims, periodic, 9, 64, fluid_only=True)
+
+
+TINY = [((1, 1, 1), (1, 1, 1)), ((1, 2, 3), (1, 1, 1)), ((3, 1, 2), (1, 0, 1)), ((2, 3, 1), (0, 1, 1)),
+        ((5, 4, 6), (0, 0, 0))]
+
+
+@pytest.mark.parametrize("dims,periodic", TINY)
+def test_tiny_lattices(dims, periodic):
+    """Degenerate extents: single-cell periodic boxes (every link wraps onto the
+    cell itself), one-plane axes, fully bounded boxes."""
+    reg, recipes, slot, state = ragged_case(dims, periodic, 12)
+    run = DeviceRun(dims, periodic, reg, precision=64)
+    run.fill(slot, state)
+    compare(run, recipes, slot, dims, periodic, 6, 64)
+
+
+@pytest.mark.parametrize("slabs", [2, 4])
+def test_one_plane_slabs(slabs):
+    """z-slabs of a single plane (boundary launch only, no interior launch)."""
+    dims, periodic = (6, 5, 4), (1, 1, 1)
+    reg, recipes, slot, state = ragged_case(dims, periodic, 13)
+    run = DeviceRun(dims, periodic, reg, precision=64, slabs=slabs)
+    run.fill(slot, state)
+    compare(run, recipes, slot, dims, periodic, 7, 64)
