@@ -1,0 +1,39 @@
+"""Small runs of every kernel family for compute-sanitizer (memcheck /
+racecheck / synccheck): dense two-population, AA, z-slabs, row and box TMA,
+masked / compacted / list porous sweeps, the host-block drop-in, diagnostics
+and the fused kinetic energy."""
+import sys
+
+sys.path.insert(0, ".")
+sys.path.insert(0, "tests")
+sys.path.insert(0, "oracle")
+import numpy as np  # noqa: E402
+
+import paper_2506_09242_b200 as dlb  # noqa: E402
+from paper_2506_09242_b200.dolb import DeviceRun  # noqa: E402
+from test_ragged import ragged_case  # noqa: E402
+
+dims, per = (37, 19, 23), (1, 0, 1)
+for kw in ({}, {"layout": "aa"}, {"slabs": 3}, {"tma": True}):
+    reg, rec, slot, st = ragged_case(dims, per, 1)
+    run = DeviceRun(dims, per, reg, precision=32, **kw)
+    run.fill(slot, st)
+    run.advance(5)
+    run.kinetic_energy()
+    print(kw, run.kernel_name(), flush=True)
+for kw in ({"skip_nodynamics": True}, {"sparse_lists": True}):
+    reg, rec, slot, st = ragged_case(dims, per, 2, nodyn=True)
+    run = DeviceRun(dims, per, reg, precision=64, **kw)
+    run.fill(slot, st)
+    run.advance(5)
+    print(kw, run.kernel_name(), flush=True)
+cfg = dlb.CaseConfig(kind="tgv", L=24, Re=400.0, Ma=0.1)
+run = dlb.build_run(dlb.init_tgv(cfg), precision=64)
+assert run.request_kinetic()
+run.advance(3)
+run.kinetic_energy()
+run.enstrophy()
+print("fused kinetic energy + enstrophy", flush=True)
+run = dlb.build_run(dlb.init_tgv(cfg), precision=32, tma=True)
+run.advance(4)
+print("tma", run.kernel_name(), flush=True)
