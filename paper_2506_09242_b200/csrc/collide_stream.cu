@@ -12,6 +12,8 @@
 // This translation unit is compiled twice: DLB_MODE = exact with -fmad=false
 // (bit-identical to the reference CPU solver) and DLB_MODE = fast with FMA
 // contraction.
+#include <cooperative_groups.h>
+
 #include "kernels.cuh"
 
 #ifndef DLB_MODE
@@ -218,6 +220,58 @@ __global__ void __launch_bounds__(256, (min_blocks<T, Q, KM>())) k_pull(const __
                     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a.sig_down), "l"(s) : "memory");
             }
         }
+    }
+}
+
+
+// Persistent multi-step sweep for small lattices (cooperative launch): the
+// whole grid stays resident for nsteps steps, each thread walks its cells
+// (grid stride), then grid-wide barrier and the buffers swap roles. For a
+// lattice that is a few waves of one launch (config 1: 64³, 2.3 waves) the
+// per-step launch ramp and tail dominate; here they are paid once per call.
+// Same per-cell arithmetic as k_pull (bit-identical); single slab only.
+template <typename T, int Q, unsigned KM>
+__global__ void __launch_bounds__(256, (min_blocks<T, Q, KM>()))
+    k_pull_coop(const __grid_constant__ StepArgs<T> a, int nsteps) {
+    using L = Lat<Q>;
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    const Geo& g = a.g;
+    const long long n = static_cast<long long>(g.nx) * g.ny * g.nz;
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    for (int st = 0; st < nsteps; ++st) {
+        const T* const* fin = (st & 1) ? const_cast<const T* const*>(a.fout) : a.fin;
+        T* const* fout = (st & 1) ? const_cast<T* const*>(a.fin) : a.fout;
+        for (long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; c < n; c += stride) {
+            const int x = int(c % g.nx);
+            const long long r = c / g.nx;
+            const int y = int(r % g.ny);
+            const int z = int(r / g.ny);
+            const int xm = (x == 0 && g.per_x) ? g.nx - 1 : x - 1;
+            const int xp = (x == g.nx - 1 && g.per_x) ? 0 : x + 1;
+            const int ym = (y == 0 && g.per_y) ? g.ny - 1 : y - 1;
+            const int yp = (y == g.ny - 1 && g.per_y) ? 0 : y + 1;
+            const int zm = (z == 0 && g.per_z) ? g.nz - 1 : z - 1;
+            const int zp = (z == g.nz - 1 && g.per_z) ? 0 : z + 1;
+            T f[Q];
+            sfor<Q>([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                constexpr int cx = L::c[i][0], cy = L::c[i][1], cz = L::c[i][2];
+                const int sx = cx > 0 ? xm : (cx < 0 ? xp : x);
+                const int sy = cy > 0 ? ym : (cy < 0 ? yp : y);
+                const int sz = cz > 0 ? zm : (cz < 0 ? zp : z);
+                f[i] = fin[i][sz * g.plane + sy * g.pitch + sx];
+            });
+            int s = a.uniform_slot;
+            if (a.slot != nullptr) s = a.slot[c];
+            Cell<T, Q>::template apply<KM>(f, a.rec[s]);
+            const int center = z * g.plane + y * g.pitch + x;
+            sfor<Q>([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                fout[i][center] = f[i];
+            });
+        }
+        grid.sync();
     }
 }
 
@@ -737,6 +791,17 @@ __global__ void __launch_bounds__(NCW * 32 + 32, (NCW >= 16 ? 1 : 2))
     TMAROW_ENTRY(T, 19, KM_BGK), TMAROW_ENTRY(T, 19, KM_TRT), TMAROW_ENTRY(T, 19, KM_BGK | KM_BB | KM_MBB), \
         TMAROW_ENTRY(T, 19, KM_TRT | KM_BB | KM_MBB)
 
+#define COOP_ENTRY(T, Q, KM)                                                             \
+    KernelEntry {                                                                        \
+        int(sizeof(T) * 8), Q, unsigned(KM), LAYOUT_COOP,                                 \
+            reinterpret_cast<const void*>(&k_pull_coop<T, Q, unsigned(KM)>),             \
+            "k_pull_coop<" #T ",D3Q" #Q "," #KM ">[" DLB_STR(DLB_MODE) "]"                  \
+    }
+#define COOP_SET(T)                                                                       \
+    , COOP_ENTRY(T, 19, KM_BGK), COOP_ENTRY(T, 19, KM_TRT), COOP_ENTRY(T, 19, KM_RR),     \
+        COOP_ENTRY(T, 19, KM_BGK | KM_BB | KM_MBB), COOP_ENTRY(T, 19, KM_TRT | KM_BB | KM_MBB), \
+        COOP_ENTRY(T, 19, KM_RR | KM_BB | KM_MBB), COOP_ENTRY(T, 27, KM_RR)
+
 #define SEG_ENTRY1(T, Q, KM, CPT)                                                        \
     KernelEntry {                                                                        \
         int(sizeof(T) * 8), Q, unsigned(KM), LAYOUT_SEG,                                  \
@@ -814,6 +879,7 @@ static const KernelEntry kTable[] = {
     Q19_SET(float), Q19_SET(double), Q27_SET(float), Q27_SET(double), AA_SET(float), AA_SET(double),
     LIST_SET(float, 19), LIST_SET(double, 19), LIST_SET(float, 27), LIST_SET(double, 27),
     TMA_SET, SEG_SET(float), SEG_SET(double), TMAROW_SET(float), TMAROW_SET(double) KE_SET(float) KE_SET(double)
+        COOP_SET(float) COOP_SET(double)
 };
 
 const KernelEntry* kernel_table(int* n) {

@@ -858,6 +858,18 @@ void Lattice::select_kernel() {
     kernel_ke_ = nullptr;
     if (!aa() && !split() && fixups_.empty() && !(km_needed_ & KM_SKIP) && d_.arith == DLB_ARITH_EXACT)
         kernel_ke_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_ | KM_KE, LAYOUT_TWO_POP);
+    // persistent cooperative sweep for small single-slab lattices (whole call
+    // in one launch). Opt-in (DLB_COOP_MAX_CELLS = largest lattice, default 0):
+    // config 1 runs 11.6 vs 12.5 us per step over 1000 steps but 14.7 vs 12.7
+    // over 100 (cooperative launch cost), profiles/r01_summary.md
+    kernel_coop_ = nullptr;
+    coop_grid_ = 0;
+    {
+        const char* ce = std::getenv("DLB_COOP_MAX_CELLS");
+        const long long maxc = ce ? std::atoll(ce) : 0;
+        if (cells() <= maxc && !aa() && !split() && fixups_.empty() && !(km_needed_ & KM_SKIP))
+            kernel_coop_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_, LAYOUT_COOP);
+    }
     kernel_tma_ = nullptr;
     tma_grid_ = 0;
     if (tma_ok_ && fixups_.empty() && !(km_needed_ & KM_SKIP)) {
@@ -1294,6 +1306,44 @@ void Lattice::step_host_block(void* f_in, const int64_t ext[3]) {
 }
 
 template <typename T>
+void Lattice::launch_coop(int64_t nsteps) {
+    StepArgs<T> a{};
+    for (int i = 0; i < d_.q; ++i) {
+        a.fin[i] = static_cast<const T*>(origin(cur_)) + i * geo_.dstride;
+        a.fout[i] = static_cast<T*>(origin(1 - cur_)) + i * geo_.dstride;
+    }
+    a.slot = d_slot_;
+    a.uniform_slot = uniform_slot_;
+    a.skip_group = skip_group_;
+    a.g = geo_;
+    for (std::size_t s = 0; s < chains_.size(); ++s) a.rec[s] = compile_recipe<T>(chains_[s]);
+    if (coop_grid_ == 0) {
+        int per_sm = 0, sms = 0;
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel_coop_->fn, 256, 0), "occupancy");
+        cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_), "sm count");
+        coop_grid_ = int(std::min<long long>(std::max(1, per_sm) * (long long)sms, (cells() + 255) / 256));
+    }
+    // chunks of at most 2^30 steps (int argument); parity follows the step count
+    int64_t done = 0;
+    while (done < nsteps) {
+        int n = int(std::min<int64_t>(nsteps - done, 1 << 30));
+        void* args[] = {&a, &n};
+        cuda_check(cudaLaunchCooperativeKernel(kernel_coop_->fn, dim3(unsigned(coop_grid_)), dim3(256), args, 0,
+                                               stream_), "launch cooperative");
+        if (n & 1)  // an odd chunk leaves the state in the other buffer
+            for (int i = 0; i < d_.q; ++i) {
+                T* t = a.fout[i];
+                a.fout[i] = const_cast<T*>(a.fin[i]);
+                a.fin[i] = t;
+            }
+        done += n;
+    }
+    if (nsteps & 1) cur_ = 1 - cur_;
+    steps_ += nsteps;
+    envelope_valid_ = false;
+}
+
+template <typename T>
 void Lattice::launch_step(int parity) {
     StepArgs<T> a{};
     for (int i = 0; i < d_.q; ++i) {
@@ -1473,7 +1523,13 @@ void Lattice::step(int64_t nsteps) {
     ke_requested_ = false;
     if (ke_last) --nsteps;
     int64_t k = 0;
-    if (nsteps >= 4) {
+    if (kernel_coop_ && nsteps >= 2 && !(lower_.linked || upper_.linked) && !kernel_tma_) {
+        // small lattice: all nsteps in one persistent cooperative launch
+        if (d_.precision_bits == 64) launch_coop<double>(nsteps);
+        else launch_coop<float>(nsteps);
+        k = nsteps;
+    }
+    if (nsteps - k >= 4) {
         const bool aligned = aa() ? aa_odd_layout_ : cur_ == 0;
         if (!aligned) {
             enqueue_step();

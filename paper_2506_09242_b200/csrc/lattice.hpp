@@ -136,6 +136,11 @@ class Lattice {
     // fused kinetic energy (KM_KE variant): per-cell values of the state after
     // step ke_step_, consumed by the next DLB_Q_KINETIC reduction
     const KernelEntry* kernel_ke_ = nullptr;
+    // persistent cooperative multi-step sweep for small lattices (k_pull_coop)
+    const KernelEntry* kernel_coop_ = nullptr;
+    int coop_grid_ = 0;
+    template <typename T>
+    void launch_coop(int64_t nsteps);
     double* d_ke_ = nullptr;
     bool ke_requested_ = false;
     int64_t ke_step_ = -1;

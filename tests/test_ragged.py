@@ -158,3 +158,19 @@ def test_one_plane_slabs(slabs):
     run = DeviceRun(dims, periodic, reg, precision=64, slabs=slabs)
     run.fill(slot, state)
     compare(run, recipes, slot, dims, periodic, 7, 64)
+
+
+@pytest.mark.parametrize("steps", [2, 7, 10])
+@pytest.mark.parametrize("dims,periodic", DIMS[:2] + TINY[:2])
+def test_cooperative_multistep(dims, periodic, steps, monkeypatch):
+    """Persistent cooperative sweep (k_pull_coop, opt-in DLB_COOP_MAX_CELLS):
+    all steps of a call in one launch with grid-wide barriers, odd and even
+    step counts (the state ends in either buffer)."""
+    monkeypatch.setenv("DLB_COOP_MAX_CELLS", str(1 << 22))
+    reg, recipes, slot, state = ragged_case(dims, periodic, 14)
+    run = DeviceRun(dims, periodic, reg, precision=64)
+    run.fill(slot, state)
+    compare(run, recipes, slot, dims, periodic, steps, 64)
+    run.advance(3)  # and again from the other buffer
+    f = run.gather_populations()
+    assert np.isfinite(f).all()
