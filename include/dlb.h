@@ -101,11 +101,13 @@ typedef struct dlb_lattice_desc {
  * consumed by a fluid cell, so every Collide-kind cell stays bit-identical to
  * the reference. Works on single slabs and z-slabs. */
 #define DLB_FLAG_SKIP_NODYNAMICS 1
-/* Use a TMA-staged dense kernel for single-slab two-population lattices: the
- * row-staged k_tmarow (each direction's whole source row as 3-D tensor-map
- * boxes into a 2-stage mbarrier ring; DLB_TMA_ROW=0 selects the box-tiled
- * k_tma). Opt-in: on B200 it reaches 0.70-0.82 of the copy roofline against
- * 0.94-0.99 for the default plain-load kernel (profiles/r01_summary.md). */
+/* Use a TMA-staged dense kernel for single-slab two-population lattices:
+ * k_tmablk on uniform lattices (one 2-D tensor box of 256 x R rows per
+ * direction and work unit), else the row-staged k_tmarow (each direction's
+ * whole source row as 3-D tensor-map boxes), both into 2-stage mbarrier rings
+ * (DLB_TMA_ROW=0 selects the box-tiled k_tma). Opt-in: on B200 they reach
+ * 0.70-0.86 of the copy roofline against 0.94-0.99 for the default plain-load
+ * kernel (profiles/r01_summary.md). */
 #define DLB_FLAG_TMA 2
 /* Sparse porous variant (single slab): per-slot, row-major cell lists, one
  * launch per dynamics kind; NoDynamics cells are not listed and wall cells

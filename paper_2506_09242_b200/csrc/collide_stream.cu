@@ -759,6 +759,120 @@ __global__ void __launch_bounds__(NCW * 32 + 32, (NCW >= 16 ? 1 : 2))
     }
 }
 
+// Block-staged TMA pull (the DLB_FLAG_TMA kernel of uniform lattices): work unit =
+// R consecutive rows x (256 - 2E) cells of one plane; per direction ONE 2-D
+// tensor box (256 x R) brings all the unit's source rows, so the number of
+// tensor-copy instructions per cell drops R * 256 / 1040 times against
+// k_tmarow (whose limiter is the copy issue rate).
+template <typename T, int Q, unsigned KM, int NCW, int R>
+__global__ void __launch_bounds__(NCW * 32 + 32, 1)
+    k_tmablk(const __grid_constant__ StepArgs<T> a, const CUtensorMap* __restrict__ tin, int S) {
+    using L = Lat<Q>;
+    constexpr int NT = NCW * 32;
+    constexpr int E = tma_pad<T>();
+    constexpr int BW = 256;
+    constexpr int TW = BW - 2 * E;
+    constexpr int stage = Q * R * BW;
+    const Geo& g = a.g;
+    extern __shared__ __align__(128) unsigned char smem[];
+    T* ring = reinterpret_cast<T*>(smem);
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + size_t(S) * stage * sizeof(T));
+    unsigned long long* empty = full + S;
+    const int tid = threadIdx.x;
+    const int tiles_x = (g.nx + TW - 1) / TW, tiles_y = (g.ny + R - 1) / R;
+    const long long units = static_cast<long long>(tiles_x) * tiles_y * g.nz;
+    if (tid == 0) {
+        for (int st = 0; st < S; ++st) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(full + st)) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(empty + st)), "r"(NCW) : "memory");
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto unit_xyz = [&](long long u, int& x0, int& y0, int& z) {
+        const long long v = u / tiles_x;
+        x0 = int(u - v * tiles_x) * TW;
+        z = int(v / tiles_y);
+        y0 = int(v - static_cast<long long>(z) * tiles_y) * R;
+    };
+    if (tid >= NT) {  // producer warp: lane i loads direction i's 2-D box
+        const int lane = tid - NT;
+        if (lane == 0)
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(tin)) : "memory");
+        const unsigned long long desc = reinterpret_cast<unsigned long long>(tin);
+        int k = 0;
+        for (long long u = blockIdx.x; u < units; u += gridDim.x, ++k) {
+            const int st = k % S;
+            if (k >= S) mbar_wait(smem_u32(empty + st), unsigned((k / S) - 1) & 1u);
+            int x0, y0, z;
+            unit_xyz(u, x0, y0, z);
+            const unsigned bar = smem_u32(full + st);
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                             "r"(unsigned(stage * sizeof(T))) : "memory");
+            __syncwarp();
+            const unsigned base = smem_u32(ring + size_t(st) * stage);
+            for (int i = lane; i < Q; i += 32) {
+                const int row = (z - kTmaC[i][2] + 1) * (g.ny + 2) + (y0 - kTmaC[i][1] + 1);
+                asm volatile(
+                    "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                    " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(base + unsigned(i * R * BW * sizeof(T))),
+                    "l"(desc), "r"(x0), "r"(row), "r"(i), "r"(bar)
+                    : "memory");
+            }
+        }
+        return;
+    }
+    int k = 0;
+    for (long long u = blockIdx.x; u < units; u += gridDim.x, ++k) {
+        const int st = k % S;
+        int x0, y0, z;
+        unit_xyz(u, x0, y0, z);
+        mbar_wait(smem_u32(full + st), unsigned(k / S) & 1u);
+        const T* sb = ring + size_t(st) * stage;
+        for (int idx = tid; idx < TW * R; idx += NT) {
+            const int r = idx / TW, xx = idx - r * TW;
+            const int x = x0 + xx, y = y0 + r;
+            if (x >= g.nx || y >= g.ny) continue;
+            T f[Q];
+            sfor<Q>([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                constexpr int cx = L::c[i][0];
+                f[i] = sb[(i * R + r) * BW + xx + E - cx];
+            });
+            int s = a.uniform_slot;
+            if (a.slot != nullptr) s = a.slot[(static_cast<long long>(z) * g.ny + y) * g.nx + x];
+            Cell<T, Q>::template apply<KM>(f, a.rec[s]);
+            const int center = z * g.plane + y * g.pitch + x;
+            sfor<Q>([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                a.fout[i][center] = f[i];
+            });
+            const bool bx_lo = g.per_x && x == 0, bx_hi = g.per_x && x == g.nx - 1;
+            const bool by_lo = g.per_y && y == 0, by_hi = g.per_y && y == g.ny - 1;
+            const bool bz_lo = g.per_z && z == 0, bz_hi = g.per_z && z == g.nz - 1;
+            if (bx_lo || bx_hi || by_lo || by_hi || bz_lo || bz_hi) {
+                sfor<Q>([&](auto I) {
+                    constexpr int i = decltype(I)::value;
+                    constexpr int cx = L::c[i][0], cy = L::c[i][1], cz = L::c[i][2];
+                    int X = x, Y = y, Z = z;
+                    bool moved = false;
+                    if (cx > 0 && bx_hi) { X = x - g.nx; moved = true; }
+                    if (cx < 0 && bx_lo) { X = x + g.nx; moved = true; }
+                    if (cy > 0 && by_hi) { Y = y - g.ny; moved = true; }
+                    if (cy < 0 && by_lo) { Y = y + g.ny; moved = true; }
+                    if (cz > 0 && bz_hi) { Z = z - g.nz; moved = true; }
+                    if (cz < 0 && bz_lo) { Z = z + g.nz; moved = true; }
+                    if (moved) a.fout[i][Z * g.plane + Y * g.pitch + X] = f[i];
+                });
+            }
+        }
+        __syncwarp();
+        if ((tid & 31) == 0)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(empty + st)) : "memory");
+    }
+}
+
 #define DLB_STR2(x) #x
 #define DLB_STR(x) DLB_STR2(x)
 #define ENTRY(T, Q, KM)                                                                  \
@@ -790,6 +904,16 @@ __global__ void __launch_bounds__(NCW * 32 + 32, (NCW >= 16 ? 1 : 2))
 #define TMAROW_SET(T)                                                                     \
     TMAROW_ENTRY(T, 19, KM_BGK), TMAROW_ENTRY(T, 19, KM_TRT), TMAROW_ENTRY(T, 19, KM_BGK | KM_BB | KM_MBB), \
         TMAROW_ENTRY(T, 19, KM_TRT | KM_BB | KM_MBB)
+
+#define TMABLK_ENTRY(T, Q, KM, R)                                                        \
+    KernelEntry {                                                                        \
+        int(sizeof(T) * 8), Q, unsigned(KM), LAYOUT_TMABLK,                               \
+            reinterpret_cast<const void*>(&k_tmablk<T, Q, unsigned(KM), 16, R>),          \
+            "k_tmablk<" #T ",D3Q" #Q "," #KM ",r" #R ">[" DLB_STR(DLB_MODE) "]", 0, R, 0, 1, 16 \
+    }
+#define TMABLK_SET                                                                        \
+    , TMABLK_ENTRY(float, 19, KM_BGK, 4), TMABLK_ENTRY(float, 19, KM_TRT | KM_BB | KM_MBB, 4), \
+        TMABLK_ENTRY(double, 19, KM_BGK, 2), TMABLK_ENTRY(double, 19, KM_TRT | KM_BB | KM_MBB, 2)
 
 #define COOP_ENTRY(T, Q, KM)                                                             \
     KernelEntry {                                                                        \
@@ -879,7 +1003,7 @@ static const KernelEntry kTable[] = {
     Q19_SET(float), Q19_SET(double), Q27_SET(float), Q27_SET(double), AA_SET(float), AA_SET(double),
     LIST_SET(float, 19), LIST_SET(double, 19), LIST_SET(float, 27), LIST_SET(double, 27),
     TMA_SET, SEG_SET(float), SEG_SET(double), TMAROW_SET(float), TMAROW_SET(double) KE_SET(float) KE_SET(double)
-        COOP_SET(float) COOP_SET(double)
+        COOP_SET(float) COOP_SET(double) TMABLK_SET
 };
 
 const KernelEntry* kernel_table(int* n) {

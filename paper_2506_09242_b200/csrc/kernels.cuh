@@ -68,7 +68,7 @@ struct StepArgs {
 // kernel families: dense two-population, AA even / odd, sparse lists (fluid / masked walls)
 enum Layout : int { LAYOUT_TWO_POP = 0, LAYOUT_AA = 1, LAYOUT_AA_ODD = 2, LAYOUT_LIST = 3, LAYOUT_LIST_MASKED = 4,
                     LAYOUT_TMA = 5, LAYOUT_SEG = 6, LAYOUT_TMAROW = 7,
-                    LAYOUT_COOP = 8 };
+                    LAYOUT_COOP = 8, LAYOUT_TMABLK = 9 };
 
 struct KernelEntry {
     int precision_bits;

@@ -728,8 +728,29 @@ void Lattice::setup_tma() {
         }
         row_ok_ = ok;
     }
-    cuda_check(cudaMalloc(&d_tmap_, 4 * sizeof(CUtensorMap)), "cudaMalloc tensor maps");
-    cuda_check(cudaMemcpy(d_tmap_, tmap_, 4 * sizeof(CUtensorMap), cudaMemcpyHostToDevice), "tensor maps");
+    // Block-staged variant (k_tmablk; DLB_TMA_BLOCKS=0 disables): the same 3-D
+    // tensor with 2-D boxes of 256 x R rows (R = 4 fp32, 2 fp64).
+    blk_ok_ = false;
+    const char* bke = std::getenv("DLB_TMA_BLOCKS");
+    if (!(bke && bke[0] == '0') && geo_.pitch >= geo_.nx + e + 1) {
+        const int R = s == 4 ? 4 : 2;
+        bool ok = true;
+        for (int b = 0; b < 2 && ok; ++b) {
+            char* base = static_cast<char*>(buf_[b]) + std::size_t(align_ - e) * s;
+            const cuuint64_t dims[3] = {cuuint64_t(geo_.pitch), cuuint64_t(geo_.ny + 2) * cuuint64_t(geo_.nz + 2),
+                                        cuuint64_t(d_.q)};
+            const cuuint64_t strides[2] = {cuuint64_t(geo_.pitch) * s, cuuint64_t(geo_.dstride) * s};
+            const cuuint32_t box[3] = {256u, cuuint32_t(R), 1u};
+            const cuuint32_t estr[3] = {1u, 1u, 1u};
+            ok = reinterpret_cast<EncodeFn>(fn)(
+                     &tmap_[4 + b], s == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
+                     base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+        }
+        blk_ok_ = ok;
+    }
+    cuda_check(cudaMalloc(&d_tmap_, 6 * sizeof(CUtensorMap)), "cudaMalloc tensor maps");
+    cuda_check(cudaMemcpy(d_tmap_, tmap_, 6 * sizeof(CUtensorMap), cudaMemcpyHostToDevice), "tensor maps");
     tma_xoff_ = e;
     tma_ok_ = true;
 }
@@ -748,6 +769,26 @@ template <typename T>
 void Lattice::launch_tma(StepArgs<T>& a, int parity) {
     const KernelEntry* k = kernel_tma_;
     const int e = int(16 / sizeof(T));
+    if (k->layout == LAYOUT_TMABLK) {
+        const int S = 2;
+        const std::size_t stage = std::size_t(d_.q) * k->tile_y * 256 * sizeof(T);
+        const std::size_t smem = std::size_t(S) * stage + std::size_t(2 * S) * 8 + 128;
+        if (tma_grid_ == 0) {
+            cuda_check(cudaFuncSetAttribute(k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
+                       "smem attr");
+            int sms = 0;
+            cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_), "sm count");
+            tma_grid_ = sms;
+        }
+        if (!envelope_valid_) refresh_envelope(parity);
+        const CUtensorMap* map = d_tmap_ + 4 + parity;
+        int ns = S;
+        void* args[] = {&a, &map, &ns};
+        cuda_check(cudaLaunchKernel(k->fn, dim3(unsigned(tma_grid_)), dim3(unsigned(k->warps * 32 + 32)), args, smem,
+                                    stream_), "launch tma blocks");
+        envelope_valid_ = true;
+        return;
+    }
     if (k->layout == LAYOUT_TMAROW) {
         const std::size_t stage = std::size_t(d_.q) * row_nb_ * row_bw_ * sizeof(T);
         // two ring stages per CTA by default (DLB_TMAROW_STAGES); one CTA of a
@@ -874,7 +915,11 @@ void Lattice::select_kernel() {
     tma_grid_ = 0;
     if (tma_ok_ && fixups_.empty() && !(km_needed_ & KM_SKIP)) {
         const std::size_t stage = std::size_t(d_.q) * row_nb_ * row_bw_ * std::size_t(d_.precision_bits / 8);
-        if (row_ok_ && 2 * stage <= (std::size_t(200) << 10)) {
+        // uniform lattices: 2-D block boxes (c5 0.84-0.85 vs 0.79-0.82 for rows); with a
+        // slot array the row kernel wins (its slot reads hide behind 2 CTAs per SM)
+        if (blk_ok_ && !d_slot_)
+            kernel_tma_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_, LAYOUT_TMABLK);
+        if (!kernel_tma_ && row_ok_ && 2 * stage <= (std::size_t(200) << 10)) {
             kernel_tma_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_, LAYOUT_TMAROW);
             // rows short enough for two 2-stage CTAs per SM: 8 consumer warps each
             // (c3 512-wide rows: 0.75 vs 0.55 of copy bandwidth with one 16-warp CTA)

@@ -193,7 +193,8 @@ class Lattice {
     // TMA-staged dense kernel (single slab): tensor maps of both buffers, and
     // whether the input buffer's envelope holds the periodic images
     const KernelEntry* kernel_tma_ = nullptr;
-    CUtensorMap tmap_[4];            // [0..1] box maps (k_tma), [2..3] row maps (k_tmarow)
+    CUtensorMap tmap_[6];            // [0..1] box maps (k_tma), [2..3] row maps (k_tmarow), [4..5] k_tmablk
+    bool blk_ok_ = false;
     bool row_ok_ = false;
     int row_nb_ = 0, row_bw_ = 0;    // k_tmarow: boxes per tile and box width (elements)
     int row_tw_ = 0;                 // k_tmarow: cells per work unit (a row or an x-split of it)
