@@ -765,7 +765,7 @@ __global__ void __launch_bounds__(NCW * 32 + 32, (NCW >= 16 ? 1 : 2))
 // tensor-copy instructions per cell drops R * 256 / 1040 times against
 // k_tmarow (whose limiter is the copy issue rate).
 template <typename T, int Q, unsigned KM, int NCW, int R>
-__global__ void __launch_bounds__(NCW * 32 + 32, 1)
+__global__ void __launch_bounds__(NCW * 32 + 32, (NCW >= 16 ? 1 : 2))
     k_tmablk(const __grid_constant__ StepArgs<T> a, const CUtensorMap* __restrict__ tin, int S) {
     using L = Lat<Q>;
     constexpr int NT = NCW * 32;
@@ -905,15 +905,15 @@ __global__ void __launch_bounds__(NCW * 32 + 32, 1)
     TMAROW_ENTRY(T, 19, KM_BGK), TMAROW_ENTRY(T, 19, KM_TRT), TMAROW_ENTRY(T, 19, KM_BGK | KM_BB | KM_MBB), \
         TMAROW_ENTRY(T, 19, KM_TRT | KM_BB | KM_MBB)
 
-#define TMABLK_ENTRY(T, Q, KM, R)                                                        \
+#define TMABLK_ENTRY(T, Q, KM, R, W)                                                     \
     KernelEntry {                                                                        \
         int(sizeof(T) * 8), Q, unsigned(KM), LAYOUT_TMABLK,                               \
-            reinterpret_cast<const void*>(&k_tmablk<T, Q, unsigned(KM), 16, R>),          \
-            "k_tmablk<" #T ",D3Q" #Q "," #KM ",r" #R ">[" DLB_STR(DLB_MODE) "]", 0, R, 0, 1, 16 \
+            reinterpret_cast<const void*>(&k_tmablk<T, Q, unsigned(KM), W, R>),           \
+            "k_tmablk<" #T ",D3Q" #Q "," #KM ",r" #R ",w" #W ">[" DLB_STR(DLB_MODE) "]", 0, R, 0, 1, W \
     }
 #define TMABLK_SET                                                                        \
-    , TMABLK_ENTRY(float, 19, KM_BGK, 4), TMABLK_ENTRY(float, 19, KM_TRT | KM_BB | KM_MBB, 4), \
-        TMABLK_ENTRY(double, 19, KM_BGK, 2), TMABLK_ENTRY(double, 19, KM_TRT | KM_BB | KM_MBB, 2)
+    , TMABLK_ENTRY(float, 19, KM_BGK, 4, 16), TMABLK_ENTRY(float, 19, KM_TRT | KM_BB | KM_MBB, 4, 16), \
+        TMABLK_ENTRY(double, 19, KM_BGK, 2, 16), TMABLK_ENTRY(double, 19, KM_TRT | KM_BB | KM_MBB, 2, 16)
 
 #define COOP_ENTRY(T, Q, KM)                                                             \
     KernelEntry {                                                                        \

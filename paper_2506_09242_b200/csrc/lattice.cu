@@ -733,7 +733,7 @@ void Lattice::setup_tma() {
     blk_ok_ = false;
     const char* bke = std::getenv("DLB_TMA_BLOCKS");
     if (!(bke && bke[0] == '0') && geo_.pitch >= geo_.nx + e + 1) {
-        const int R = s == 4 ? 4 : 2;
+        const int R = s == 4 ? 4 : 2;  // rows per work unit (k_tmablk's R)
         bool ok = true;
         for (int b = 0; b < 2 && ok; ++b) {
             char* base = static_cast<char*>(buf_[b]) + std::size_t(align_ - e) * s;
@@ -776,9 +776,11 @@ void Lattice::launch_tma(StepArgs<T>& a, int parity) {
         if (tma_grid_ == 0) {
             cuda_check(cudaFuncSetAttribute(k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
                        "smem attr");
-            int sms = 0;
+            int sms = 0, per_sm = 0;
             cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_), "sm count");
-            tma_grid_ = sms;
+            cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k->fn, k->warps * 32 + 32, smem),
+                       "occupancy");
+            tma_grid_ = std::max(1, per_sm) * sms;
         }
         if (!envelope_valid_) refresh_envelope(parity);
         const CUtensorMap* map = d_tmap_ + 4 + parity;
@@ -917,8 +919,9 @@ void Lattice::select_kernel() {
         const std::size_t stage = std::size_t(d_.q) * row_nb_ * row_bw_ * std::size_t(d_.precision_bits / 8);
         // uniform lattices: 2-D block boxes (c5 0.84-0.85 vs 0.79-0.82 for rows); with a
         // slot array the row kernel wins (its slot reads hide behind 2 CTAs per SM)
-        if (blk_ok_ && !d_slot_)
+        if (blk_ok_ && !d_slot_) {
             kernel_tma_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_, LAYOUT_TMABLK);
+        }
         if (!kernel_tma_ && row_ok_ && 2 * stage <= (std::size_t(200) << 10)) {
             kernel_tma_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_, LAYOUT_TMAROW);
             // rows short enough for two 2-stage CTAs per SM: 8 consumer warps each
