@@ -174,3 +174,45 @@ def test_cooperative_multistep(dims, periodic, steps, monkeypatch):
     run.advance(3)  # and again from the other buffer
     f = run.gather_populations()
     assert np.isfinite(f).all()
+
+
+@pytest.mark.parametrize("bits,pinned", [(32, True), (32, False), (64, True)])
+def test_ragged_host_block(bits, pinned):
+    """The host-block drop-in (dlb_collide_and_stream on an AcceleratedBlock)
+    on a ragged, partly periodic lattice with walls and a moving wall, through
+    page-locked (pipelined) and pageable (staged) memory."""
+    import ctypes as C
+    from paper_2506_09242_b200 import _capi
+    dims, periodic = (37, 19, 23), (1, 0, 1)
+    nx, ny, nz = dims
+    reg, recipes, slot, state = ragged_case(dims, periodic, 15)
+    run = DeviceRun(dims, periodic, reg, precision=bits)
+    run.fill(slot, state)
+    f0 = run.gather_populations()
+    dt = np.float32 if bits == 32 else np.float64
+    want = f0.astype(dt).copy()
+    Oracle().step(19, dims, periodic, recipes, slot, want, 3)
+    shape = (19, nz + 2, ny + 2, nx + 2)
+    nbytes = int(np.prod(shape)) * np.dtype(dt).itemsize
+    p = C.c_void_p()
+    if pinned:
+        _capi.check(_capi.lib().dlb_host_alloc(nbytes, C.byref(p)))
+        blk = np.ctypeslib.as_array((C.c_uint8 * nbytes).from_address(p.value)).view(dt).reshape(shape)
+        blk[:] = 0
+    else:
+        blk = np.zeros(shape, dt)
+    try:
+        blk[:, 1:-1, 1:-1, 1:-1] = f0.astype(dt).reshape(19, nz, ny, nx)
+        tag = np.full(shape[1:], -1, np.int32)
+        tag[1:-1, 1:-1, 1:-1] = np.vectorize(reg.tag_of_slot)(slot)
+        pidx = np.full(shape[1:], -1, np.int32)
+        pidx[1:-1, 1:-1, 1:-1] = slot
+        for _ in range(3):
+            dlb.refresh_envelope_periodic(blk, periodic)
+            dlb.collide_and_stream(reg, blk, tag, pidx, dlb.DispatchSet.all_of(reg))
+        got = blk[:, 1:-1, 1:-1, 1:-1].reshape(-1).astype(np.float64)
+        assert np.array_equal(got, np.asarray(want, np.float64).reshape(-1))
+    finally:
+        if pinned:
+            del blk
+            _capi.lib().dlb_host_free(p)
