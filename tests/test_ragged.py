@@ -216,3 +216,34 @@ def test_ragged_host_block(bits, pinned):
         if pinned:
             del blk
             _capi.lib().dlb_host_free(p)
+
+
+def test_host_block_d3q27():
+    """The host-block drop-in on a D3Q27 RR block (config 2's lattice)."""
+    from paper_2506_09242_b200.dolb import make_collision_chain as mk
+    from pyoracle import RR
+    dims, periodic = (13, 11, 9), (1, 1, 1)
+    nx, ny, nz = dims
+    reg = DynamicsRegistry()
+    p = CollisionParams().set_trt(1.71, 3.0 / 16.0)
+    s0 = reg.register_chain(mk(LinkType.RR, p))
+    recipes = [Recipe(kind=COLLIDE, base=RR, omega=1.71)]
+    slot = np.zeros((nz, ny, nx), np.int32)
+    rng = np.random.default_rng(3)
+    state = (1.0 + 0.01 * rng.random(nx * ny * nz), 0.02 * rng.random(nx * ny * nz),
+             0.01 * rng.random(nx * ny * nz), -0.01 * rng.random(nx * ny * nz))
+    run = DeviceRun(dims, periodic, reg, q=27, precision=64)
+    run.fill(slot + s0, state)
+    f0 = run.gather_populations()
+    want = f0.copy()
+    Oracle().step(27, dims, periodic, recipes, slot, want, 2)
+    shape = (27, nz + 2, ny + 2, nx + 2)
+    blk = np.zeros(shape)
+    blk[:, 1:-1, 1:-1, 1:-1] = f0.reshape(27, nz, ny, nx)
+    tag = np.full(shape[1:], -1, np.int32)
+    tag[1:-1, 1:-1, 1:-1] = reg.tag_of_slot(s0)
+    pidx = np.where(tag >= 0, s0, -1).astype(np.int32)
+    for _ in range(2):
+        dlb.refresh_envelope_periodic(blk, periodic, q=27)
+        dlb.collide_and_stream(reg, blk, tag, pidx, dlb.DispatchSet.all_of(reg), q=27)
+    assert np.array_equal(blk[:, 1:-1, 1:-1, 1:-1].reshape(-1), want.reshape(-1))
