@@ -216,6 +216,9 @@ def test_capi_null_arguments_and_buffer_protocol():
     assert b"null" in lib.dlb_last_error()
     assert lib.dlb_lattice_step(None, 1) == 1
     assert lib.dlb_collide_and_stream(None, None, None, 0, 1) == 1
+    assert lib.dlb_lattice_request_kinetic(None, None) == 1
+    assert lib.dlb_lattice_reduce(None, None, None, None) == 1
+    assert lib.dlb_refresh_envelope_periodic(None, None) == 1
     n = C.c_size_t()
     assert lib.dlb_chain_canonical(b"Boundary_RegularizedPressure_2_M1|COLL_RR", None, 0, C.byref(n)) == 0
     assert n.value == len("Boundary_RegularizedPressure_2_M1__RR") + 1
