@@ -148,6 +148,9 @@ DLB_API dlb_status dlb_lattice_gather_macroscopic(dlb_lattice* lat, double* rho,
  * modulo 2^64. Independent of layout and decomposition (slab sums add up), so
  * full-size runs can be compared with the reference without moving the state. */
 DLB_API dlb_status dlb_lattice_checksum(dlb_lattice* lat, uint64_t* per_direction);
+/* The same over the cells whose chain is not NoDynamics only (the cells the
+ * masked porous sweep keeps current). */
+DLB_API dlb_status dlb_lattice_checksum_active(dlb_lattice* lat, uint64_t* per_direction);
 /* Advance nsteps (asynchronous on the lattice stream; includes the halo exchange). */
 DLB_API dlb_status dlb_lattice_step(dlb_lattice* lat, int64_t nsteps);
 DLB_API dlb_status dlb_lattice_synchronize(dlb_lattice* lat);
@@ -176,6 +179,16 @@ DLB_API dlb_status dlb_lattice_link_local(dlb_lattice* lower, dlb_lattice* upper
  * the current state. Call on every slab after filling / uploading the state and
  * before the first step (steps then push the halo themselves). */
 DLB_API dlb_status dlb_lattice_exchange(dlb_lattice* lat);
+/* The same for several slabs of ONE process: waits for all of them first. */
+DLB_API dlb_status dlb_lattices_exchange(dlb_lattice** lats, size_t n);
+/* Halo wait limit of a linked slab (default 20 s, or DLB_HALO_TIMEOUT_MS). A
+ * neighbour that has not finished the previous step's boundary planes within
+ * it fails the step: nothing of that step or of any later queued step is
+ * written, the next synchronize / step / download reports DLB_ERROR_EXCHANGE
+ * (the reference's lost-message ExchangeError, multiblock.cpp:305-345), and the
+ * lattice is left at its last completed step. dlb_lattice_exchange clears the
+ * error once the slabs are back at one step count. */
+DLB_API dlb_status dlb_lattice_set_halo_timeout(dlb_lattice* lat, double seconds);
 /* Across processes: export an opaque blob (CUDA IPC handles), ship it with any
  * transport (e.g. torch.distributed), link it as the lower (side 0) or upper
  * (side 1) neighbour. */

@@ -405,6 +405,8 @@ class Reference:
             lib.ref_case_dump.argtypes = [C.POINTER(RefCase), C.c_int, C.c_int64, C.c_char_p]
             lib.ref_case_checksum.argtypes = [C.POINTER(RefCase), C.c_int, C.c_void_p, C.c_int,
                                               C.c_int64, C.c_void_p]
+            lib.ref_case_checksum_masked.argtypes = [C.POINTER(RefCase), C.c_int, C.c_void_p, C.c_int,
+                                                     C.c_int64, C.c_void_p, C.c_void_p]
             lib.ref_case_sample.argtypes = [C.POINTER(RefCase), C.c_int, C.c_int64, C.c_int64, C.c_void_p]
             lib.ref_tree_sum.argtypes = [C.c_void_p, C.c_int64, C.POINTER(C.c_double)]
             Reference._lib = lib
@@ -472,6 +474,17 @@ class Reference:
         self._check(self.lib.ref_case_checksum(C.byref(rc), precision_bits, _ptr(g), workers, nsteps,
                                                _ptr(out)))
         return [int(v) for v in out]
+
+    def checksum_masked(self, case: Case, precision_bits: int, nsteps: int, grid=(1, 1, 1), workers=1):
+        """(checksum of every cell, checksum of the cells whose chain is not
+        NoDynamics), streamed over the reference's blocks (no gather copy)."""
+        out = np.zeros(19, np.uint64)
+        act = np.zeros(19, np.uint64)
+        g = np.asarray(grid, np.int32)
+        rc = case.ref_struct()
+        self._check(self.lib.ref_case_checksum_masked(C.byref(rc), precision_bits, _ptr(g), workers, nsteps,
+                                                      _ptr(out), _ptr(act)))
+        return [int(v) for v in out], [int(v) for v in act]
 
     def bench(self, case: Case, precision_bits: int, workers: int, warmup: int, steps: int, reps: int = 3):
         reps_out = np.zeros(reps)

@@ -11,12 +11,14 @@
 //   - equilibrium2/4 (proj/include/dolb/descriptor.hpp:79-121)
 //   - perf::measure_mlups (proj/src/perfmodel.cpp:94-121)
 // Python tests and bench.py (--impl reference / cpu_baseline) call it via ctypes.
+#include <array>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "dolb/accelerated_lattice.hpp"
@@ -116,23 +118,55 @@ void run_case(const RefCase& rc, const int grid[3], int workers, int64_t steps, 
     std::memcpy(out, pops.data(), pops.size() * sizeof(double));
 }
 
+// Streamed over the run's blocks (public MultiBlockRun::blocks() + the
+// blocks' cell_index): no gather_populations copy, so full-size configs fit in
+// host RAM. out_all: every interior cell; out_active (optional): cells whose
+// chain is not NoDynamics (the masked porous sweep leaves those stale).
 template <typename T>
-void checksum_case(const RefCase& rc, const int grid[3], int workers, int64_t steps, uint64_t* out) {
+void checksum_case(const RefCase& rc, const int grid[3], int workers, int64_t steps, uint64_t* out_all,
+                   uint64_t* out_active) {
     const dolb::CaseSetup setup = make_setup(rc);
     auto registry = std::make_shared<dolb::DynamicsRegistry>();
     auto run = dolb::build_run<T>(setup, {grid[0], grid[1], grid[2]}, workers, registry);
     run.advance(steps);
-    const std::vector<double> pops = run.gather_populations();
-    const std::size_t n = pops.size() / 19;
+    const auto& blocks = run.blocks();
+    const int ntags = registry->num_tags();
+    std::vector<char> nodyn(std::size_t(std::max(ntags, 1)), 0);
+    for (int t = 0; t < ntags; ++t) nodyn[std::size_t(t)] = registry->chain_for(t) == "NoDynamics";
+    std::vector<std::array<uint64_t, 38>> part(blocks.size());
+    std::vector<std::thread> th;
+    for (std::size_t b = 0; b < blocks.size(); ++b) {
+        th.emplace_back([&, b] {
+            const auto& blk = blocks[b];
+            std::array<uint64_t, 38> acc{};
+            const std::size_t vol = std::size_t(blk.vol());
+            for (int64_t z = 1; z <= blk.interior[2]; ++z)
+                for (int64_t y = 1; y <= blk.interior[1]; ++y)
+                    for (int64_t x = 1; x <= blk.interior[0]; ++x) {
+                        const int64_t at = blk.idx(x, y, z);
+                        const uint64_t w = uint64_t(blk.cell_index[std::size_t(at)]) + 1u;
+                        const int32_t tg = blk.tag[std::size_t(at)];
+                        const bool active = !(tg >= 0 && tg < ntags && nodyn[std::size_t(tg)]);
+                        for (int i = 0; i < 19; ++i) {
+                            const double v = double(blk.f_in[std::size_t(i) * vol + std::size_t(at)]) + 0.0;
+                            uint64_t bits;
+                            std::memcpy(&bits, &v, 8);
+                            acc[std::size_t(i)] += bits * w;
+                            if (active) acc[std::size_t(19 + i)] += bits * w;
+                        }
+                    }
+            part[b] = acc;
+        });
+    }
+    for (auto& t : th) t.join();
     for (int i = 0; i < 19; ++i) {
-        uint64_t acc = 0;
-        for (std::size_t c = 0; c < n; ++c) {
-            const double v = pops[i * n + c] + 0.0;
-            uint64_t bits;
-            std::memcpy(&bits, &v, 8);
-            acc += bits * uint64_t(c + 1);
+        uint64_t a = 0, m = 0;
+        for (const auto& p : part) {
+            a += p[std::size_t(i)];
+            m += p[std::size_t(19 + i)];
         }
-        out[i] = acc;
+        out_all[i] = a;
+        if (out_active) out_active[i] = m;
     }
 }
 
@@ -316,8 +350,20 @@ __attribute__((visibility("default"))) int ref_case_checksum(const RefCase* rc, 
                                                              const int* grid, int workers,
                                                              int64_t steps, uint64_t* out) {
     return guarded([&] {
-        if (precision_bits == 64) checksum_case<double>(*rc, grid, workers, steps, out);
-        else checksum_case<float>(*rc, grid, workers, steps, out);
+        if (precision_bits == 64) checksum_case<double>(*rc, grid, workers, steps, out, nullptr);
+        else checksum_case<float>(*rc, grid, workers, steps, out, nullptr);
+    });
+}
+
+// The same, plus the checksum restricted to cells whose chain is not
+// NoDynamics (compare with the masked porous sweep).
+__attribute__((visibility("default"))) int ref_case_checksum_masked(const RefCase* rc, int precision_bits,
+                                                                    const int* grid, int workers,
+                                                                    int64_t steps, uint64_t* out_all,
+                                                                    uint64_t* out_active) {
+    return guarded([&] {
+        if (precision_bits == 64) checksum_case<double>(*rc, grid, workers, steps, out_all, out_active);
+        else checksum_case<float>(*rc, grid, workers, steps, out_all, out_active);
     });
 }
 

@@ -373,6 +373,15 @@ DLB_API dlb_status dlb_lattice_checksum(dlb_lattice* lat, uint64_t* per_directio
     });
 }
 
+DLB_API dlb_status dlb_lattice_checksum_active(dlb_lattice* lat, uint64_t* per_direction) {
+    DLB_REQUIRE(lat);
+    DLB_REQUIRE(per_direction);
+    return guarded([&] {
+        lat->lat->synchronize();
+        lat->lat->checksum(reinterpret_cast<unsigned long long*>(per_direction), true);
+    });
+}
+
 DLB_API dlb_status dlb_lattice_step_bytes(dlb_lattice* lat, int64_t* bytes_out) {
     DLB_REQUIRE(lat);
     DLB_REQUIRE(bytes_out);
@@ -399,10 +408,20 @@ DLB_API dlb_status dlb_lattice_link_local(dlb_lattice* lower, dlb_lattice* upper
 
 DLB_API dlb_status dlb_lattice_exchange(dlb_lattice* lat) {
     DLB_REQUIRE(lat);
+    return guarded([&] { lat->lat->exchange(); });
+}
+
+DLB_API dlb_status dlb_lattices_exchange(dlb_lattice** lats, size_t n) {
+    DLB_REQUIRE(lats || n == 0);
     return guarded([&] {
-        lat->lat->synchronize();
-        lat->lat->exchange();
+        for (size_t k = 0; k < n; ++k) lats[k]->lat->quiesce();
+        for (size_t k = 0; k < n; ++k) lats[k]->lat->exchange();
     });
+}
+
+DLB_API dlb_status dlb_lattice_set_halo_timeout(dlb_lattice* lat, double seconds) {
+    DLB_REQUIRE(lat);
+    return guarded([&] { lat->lat->set_halo_timeout(seconds); });
 }
 
 DLB_API dlb_status dlb_lattice_export_ipc(dlb_lattice* lat, void* blob, size_t cap, size_t* len_out) {

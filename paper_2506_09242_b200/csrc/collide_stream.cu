@@ -106,6 +106,7 @@ __global__ void __launch_bounds__(256, (min_blocks<T, Q, KM>())) k_pull(const __
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int y = blockIdx.y * blockDim.y + threadIdx.y;
     const int z = a.z_begin + int(blockIdx.z) * a.z_step;
+    if (a.err != nullptr && *reinterpret_cast<const volatile unsigned long long*>(a.err) != 0ull) return;
     bool active = x < g.nx && y < g.ny;
     int s = a.uniform_slot;
     if constexpr ((KM & KM_SKIP) != 0) {

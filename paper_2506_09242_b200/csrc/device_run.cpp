@@ -71,7 +71,7 @@ void DeviceRun::set_dispatch(const std::set<int>& tags) {
 
 void DeviceRun::exchange() {
     if (slabs_.size() == 1) return;
-    for (auto& s : slabs_) s->synchronize();
+    for (auto& s : slabs_) s->quiesce();
     for (auto& s : slabs_) s->exchange();
 }
 

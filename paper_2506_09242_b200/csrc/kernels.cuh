@@ -63,6 +63,10 @@ struct StepArgs {
     // KM_KE variant: per-cell kinetic energy of the new state, x fastest
     // (appended last so the other kernels' parameter offsets do not move)
     double* ke;
+    // linked slabs: the exchange error flag (flags[3]); a launch that finds it
+    // set writes nothing (a timed-out halo wait fails the step and every later
+    // one, so the last completed state stays intact)
+    const unsigned long long* err;
 };
 
 // kernel families: dense two-population, AA even / odd, sparse lists (fluid / masked walls)

@@ -119,6 +119,7 @@ __global__ void k_box_copy(TD* dst, const TS* src, Geo g, int bx0, int by0, int 
 // after `timeout_ns` and raises flags[3] (reported as an exchange error).
 __global__ void k_halo_wait(unsigned long long* flags, int have_lower, int have_upper,
                             unsigned long long timeout_ns) {
+    if (*reinterpret_cast<volatile unsigned long long*>(flags + 3) != 0ull) return;  // already failed
     const unsigned long long target = flags[2];
     unsigned long long t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
@@ -143,15 +144,19 @@ __global__ void k_halo_wait(unsigned long long* flags, int have_lower, int have_
 // (mod 2^64). Integer sums commute, so the result does not depend on the
 // reduction order, the slab decomposition or the layout (two-population / AA
 // even / AA odd), and sums of slab checksums equal the monolithic one.
+// skip (optional): per-slot flags; cells whose slot is flagged (NoDynamics)
+// are left out (the masked porous sweep never writes them).
 template <typename T, int Q>
 __global__ void k_checksum(const T* origin0, Geo g, int aa_mode, long long z_origin, long long gnx,
-                           long long gny, unsigned long long* out) {
+                           long long gny, unsigned long long* out, const uint8_t* slot, int uniform_slot,
+                           const uint8_t* skip) {
     using L = Lat<Q>;
     unsigned long long acc[Q];
     for (int i = 0; i < Q; ++i) acc[i] = 0ull;
     const long long n = static_cast<long long>(g.nx) * g.ny * g.nz;
     for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
          c += (long long)gridDim.x * blockDim.x) {
+        if (skip != nullptr && skip[slot ? slot[c] : uniform_slot]) continue;
         const int x = int(c % g.nx);
         const int y = int((c / g.nx) % g.ny);
         const int z = int(c / (static_cast<long long>(g.nx) * g.ny));
@@ -333,8 +338,19 @@ Lattice::Lattice(const dlb_lattice_desc& desc, const DynamicsRegistry& reg) : d_
     for (int t = 0; t < reg.num_tags(); ++t) tag_names_.push_back(reg.chain_for(t));
 
     device_ = d_.device;
-    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    DeviceGuard dg(device_);
     cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+    {
+        // z-slab halo work (wait + boundary planes + peer push) runs on a
+        // high-priority stream beside the interior launch
+        int lo = 0, hi = 0;
+        cuda_check(cudaDeviceGetStreamPriorityRange(&lo, &hi), "stream priorities");
+        cuda_check(cudaStreamCreateWithPriority(&halo_stream_, cudaStreamNonBlocking, hi), "cudaStreamCreate");
+        cuda_check(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "cudaEventCreate");
+        cuda_check(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming), "cudaEventCreate");
+        const char* te = std::getenv("DLB_HALO_TIMEOUT_MS");
+        if (te && std::atof(te) > 0) halo_timeout_ns_ = static_cast<unsigned long long>(std::atof(te) * 1e6);
+    }
     cuda_check(cudaEventCreate(&ev0_), "cudaEventCreate");
     cuda_check(cudaEventCreate(&ev1_), "cudaEventCreate");
 
@@ -386,7 +402,10 @@ Lattice::Lattice(const dlb_lattice_desc& desc, const DynamicsRegistry& reg) : d_
 }
 
 Lattice::~Lattice() {
+    int prev = -1;
+    cudaGetDevice(&prev);
     cudaSetDevice(device_);
+    if (halo_stream_) cudaStreamSynchronize(halo_stream_);
     if (stream_) cudaStreamSynchronize(stream_);
     invalidate_graph();
     for (Peer* p : {&lower_, &upper_})
@@ -410,7 +429,11 @@ Lattice::~Lattice() {
     if (h2d_stream_) cudaStreamDestroy(h2d_stream_);
     if (ev0_) cudaEventDestroy(ev0_);
     if (ev1_) cudaEventDestroy(ev1_);
+    if (ev_fork_) cudaEventDestroy(ev_fork_);
+    if (ev_join_) cudaEventDestroy(ev_join_);
+    if (halo_stream_) cudaStreamDestroy(halo_stream_);
     if (stream_) cudaStreamDestroy(stream_);
+    if (prev >= 0) cudaSetDevice(prev);
 }
 
 void* Lattice::origin(int which) const {
@@ -447,6 +470,7 @@ void Lattice::set_periodic_override(bool x, bool y, bool z) {
 }
 
 void Lattice::set_slots(const int32_t* slots) {
+    DeviceGuard dg(device_);
     invalidate_graph();
     const long long n = cells();
     std::vector<uint8_t> u8(std::size_t(n), 0);
@@ -839,6 +863,7 @@ void Lattice::launch_tma(StepArgs<T>& a, int parity) {
 }
 
 void Lattice::set_uniform_slot(int32_t slot) {
+    DeviceGuard dg(device_);
     if (slot < 0 || slot >= int32_t(chains_.size()))
         throw std::invalid_argument("slot " + std::to_string(slot) + " is not registered");
     cudaFree(d_slot_);
@@ -973,7 +998,7 @@ void Lattice::reset_aa() {
 void Lattice::fill_equilibrium(const double* rho, const double* ux, const double* uy,
                                const double* uz) {
     envelope_valid_ = false;
-    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    DeviceGuard dg(device_);
     reset_aa();
     const long long plane_cells = (long long)geo_.nx * geo_.ny;
     const int zc = int(std::max<long long>(1, (long long)(staging_bytes_ / 32) / plane_cells));
@@ -1014,7 +1039,7 @@ void Lattice::fill_uniform(double rho, double ux, double uy, double uz) {
     std::fill(h.begin() + 2 * n, h.begin() + 3 * n, uy);
     std::fill(h.begin() + 3 * n, h.end(), uz);
     // k_fill_eq indexes the staging arrays chunk-locally: one upload serves every chunk
-    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    DeviceGuard dg(device_);
     envelope_valid_ = false;
     reset_aa();
     double* st = static_cast<double*>(staging_);
@@ -1039,7 +1064,7 @@ void Lattice::fill_uniform(double rho, double ux, double uy, double uz) {
 void Lattice::fill_tgv(int64_t L, double u_inf) {
     if (d_.dims[0] != L || d_.dims[1] != L || d_.global_nz != L)
         throw std::invalid_argument("TGV fill needs an L^3 domain");
-    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    DeviceGuard dg(device_);
     reset_aa();
     envelope_valid_ = false;
     // cases.cpp:145-156: x = 2 pi / L * (i + 0.5); glibc sin / cos on the host.
@@ -1069,7 +1094,7 @@ void Lattice::fill_tgv(int64_t L, double u_inf) {
 // Canonical (direction-major, x fastest, interior only) <-> device layout,
 // chunked over z planes through the staging buffer.
 void Lattice::copy_canonical(void* host, bool to_device, bool as_double, int elem_bytes) {
-    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    DeviceGuard dg(device_);
     if (to_device) {
         reset_aa();
         envelope_valid_ = false;
@@ -1127,7 +1152,7 @@ void Lattice::download_raw(void* canon) {
 // box of every direction, including the envelope the caller refreshed.
 void Lattice::upload_block(const void* f, const int64_t ext[3]) {
     envelope_valid_ = false;
-    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    DeviceGuard dg(device_);
     const int s = d_.precision_bits / 8;
     const long long vol = ext[0] * ext[1] * ext[2];
     const long long plane_cells = ext[0] * ext[1];
@@ -1153,7 +1178,7 @@ void Lattice::upload_block(const void* f, const int64_t ext[3]) {
 // Interior of buffer `which` (0 = current state) back into an envelope-
 // inclusive host block; the host envelope is left untouched.
 void Lattice::download_block_interior(void* f, const int64_t ext[3], int which) {
-    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    DeviceGuard dg(device_);
     const int s = d_.precision_bits / 8;
     const long long vol = ext[0] * ext[1] * ext[2];
     const long long plane_cells = ext[0] * ext[1];
@@ -1308,7 +1333,7 @@ void Lattice::block_copy(cudaStream_t st, void* dev, bool up, int p0, int p1) {
 }
 
 void Lattice::begin_host_block(void* f_in, const int64_t ext[3]) {
-    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    DeviceGuard dg(device_);
     if (aa()) throw std::invalid_argument("host-block stepping uses the two-population layout");
     if (blk_.pending) abort_host_block();
     if (d_.precision_bits == 64) launch_host_block<double>(f_in, ext);
@@ -1483,11 +1508,22 @@ void Lattice::launch_step(int parity) {
         }
         return;
     }
-    // 1. wait until both neighbours completed the boundary planes of the previous step
-    k_halo_wait<<<1, 1, 0, stream_>>>(d_flags_, lower_.linked, upper_.linked,
-                                      20ull * 1000 * 1000 * 1000);
+    // Linked z-slab (halo exchange over peer memory), per step:
+    //   halo_stream_ (high priority): k_halo_wait (both neighbours finished the
+    //     boundary planes of the previous step, i.e. our ghost planes are
+    //     current) -> boundary launch (planes 0 and nz-1, peer push of the
+    //     z-crossing links into the neighbours' ghost planes, completion signal)
+    //   stream_: interior launch (planes 1..nz-2; reads no ghost plane)
+    // forked after the previous step and joined before the next one: the
+    // interior of step s needs both launches of step s-1 (its input planes, and
+    // the boundary launch's reads of the buffer it overwrites), so the wait,
+    // the boundary sweep and the NVLink transfer all overlap the interior.
+    a.err = d_flags_ + 3;
+    ++halo_steps_;
+    cuda_check(cudaEventRecord(ev_fork_, stream_), "fork");
+    cuda_check(cudaStreamWaitEvent(halo_stream_, ev_fork_, 0), "fork");
+    k_halo_wait<<<1, 1, 0, halo_stream_>>>(d_flags_, lower_.linked, upper_.linked, halo_timeout_ns_);
     cuda_check(cudaGetLastError(), "k_halo_wait");
-    // 2. boundary planes with the fused halo push + completion signal
     StepArgs<T> b = a;
     b.z_begin = 0;
     b.z_step = geo_.nz > 1 ? geo_.nz - 1 : 1;
@@ -1506,10 +1542,10 @@ void Lattice::launch_step(int parity) {
     b.my_step = d_flags_ + 2;
     {
         void* args[] = {&b};
-        cuda_check(cudaLaunchKernel(fn, dim3(gx, gy, geo_.nz > 1 ? 2 : 1), block, args, 0, stream_),
+        cuda_check(cudaLaunchKernel(fn, dim3(gx, gy, geo_.nz > 1 ? 2 : 1), block, args, 0, halo_stream_),
                    "launch boundary");
     }
-    // 3. interior planes (independent of the ghost planes)
+    cuda_check(cudaEventRecord(ev_join_, halo_stream_), "join");
     if (geo_.nz > 2) {
         a.z_begin = 1;
         a.z_step = 1;
@@ -1517,9 +1553,11 @@ void Lattice::launch_step(int parity) {
         cuda_check(cudaLaunchKernel(fn, dim3(gx, gy, geo_.nz - 2), block, args, 0, stream_),
                    "launch interior");
     }
+    cuda_check(cudaStreamWaitEvent(stream_, ev_join_, 0), "join");
 }
 
 void Lattice::enqueue_step() {
+    DeviceGuard dg(device_);
     if (d_.precision_bits == 64) launch_step<double>(cur_);
     else launch_step<float>(cur_);
     if (!aa()) cur_ = 1 - cur_;
@@ -1539,7 +1577,7 @@ void Lattice::ensure_graph() {
     }
     const int cur = cur_;
     const bool odd = aa_odd_layout_;
-    const int64_t steps = steps_;
+    const int64_t steps = steps_, halo_steps = halo_steps_;
     cudaGraph_t g = nullptr;
     cuda_check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "begin capture");
     enqueue_step();
@@ -1548,7 +1586,10 @@ void Lattice::ensure_graph() {
     cur_ = cur;
     aa_odd_layout_ = odd;
     steps_ = steps;
-    cuda_check(cudaGraphInstantiate(&graph_, g, 0), "graph instantiate");
+    halo_steps_ = halo_steps;
+    // keep the halo branch's stream priority inside the replayed graph
+    cuda_check(cudaGraphInstantiateWithFlags(&graph_, g, cudaGraphInstantiateFlagUseNodePriority),
+               "graph instantiate");
     cudaGraphDestroy(g);
 }
 
@@ -1564,7 +1605,7 @@ bool Lattice::request_kinetic() {
 void Lattice::step(int64_t nsteps) {
     if (nsteps <= 0) return;
     check_dispatch();
-    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    DeviceGuard dg(device_);
     // a requested fused kinetic energy belongs to the LAST step of this call;
     // the others (and any captured graph) run the plain kernel
     const bool ke_last = ke_requested_;
@@ -1587,6 +1628,7 @@ void Lattice::step(int64_t nsteps) {
         for (; k + 2 <= nsteps; k += 2) {
             cuda_check(cudaGraphLaunch(graph_, stream_), "graph launch");
             steps_ += 2;
+            if (lower_.linked || upper_.linked) halo_steps_ += 2;
         }
     }
     for (; k < nsteps; ++k) enqueue_step();
@@ -1603,8 +1645,18 @@ void Lattice::step(int64_t nsteps) {
 // read from there). Needed once before the first step after (re)filling the
 // state; afterwards every step's boundary launch pushes the halo itself.
 // Neighbours must be quiescent (lockstep, as in the reference).
+void Lattice::quiesce() {
+    DeviceGuard dg(device_);
+    cuda_check(cudaStreamSynchronize(halo_stream_), "sync");
+    cuda_check(cudaStreamSynchronize(stream_), "sync");
+}
+
 void Lattice::exchange() {
-    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    DeviceGuard dg(device_);
+    quiesce();
+    // (re)priming the ghosts clears a previous exchange error: the caller has
+    // brought the slabs back to one step count (MultiBlockRun::exchange)
+    cuda_check(cudaMemsetAsync(d_flags_ + 3, 0, sizeof(unsigned long long), stream_), "clear error");
     const int s = d_.precision_bits / 8;
     const std::size_t plane_bytes = std::size_t(geo_.plane) * s;
     auto plane_ptr = [&](void* origin_dir0, long long dstride, int i, int z) {
@@ -1625,21 +1677,29 @@ void Lattice::exchange() {
     cuda_check(cudaStreamSynchronize(stream_), "halo exchange");
 }
 
-void Lattice::checksum(unsigned long long* per_dir) {
-    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+void Lattice::checksum(unsigned long long* per_dir, bool active_only) {
+    DeviceGuard dg(device_);
     cuda_check(cudaStreamSynchronize(stream_), "sync");
     unsigned long long* d = static_cast<unsigned long long*>(staging_);
     cuda_check(cudaMemsetAsync(d, 0, 27 * 8, stream_), "memset");
+    const uint8_t* skip = nullptr;
+    if (active_only) {
+        std::vector<uint8_t> nd(256, 0);
+        for (std::size_t k = 0; k < chains_.size(); ++k) nd[k] = kind_bits(chains_[k]) == KM_NODYN;
+        uint8_t* dsk = static_cast<uint8_t*>(staging_) + 4096;
+        cuda_check(cudaMemcpyAsync(dsk, nd.data(), nd.size(), cudaMemcpyHostToDevice, stream_), "h2d");
+        skip = dsk;
+    }
     const int mode = !aa() ? 0 : (aa_odd_layout_ ? 2 : 1);
     const int grid = grid_for(cells());
     const void* o = origin(cur_);
     const long long gnx = geo_.nx, gny = geo_.ny;
     if (d_.precision_bits == 64) {
-        if (d_.q == 19) k_checksum<double, 19><<<grid, 256, 0, stream_>>>((const double*)o, geo_, mode, d_.z_origin, gnx, gny, d);
-        else k_checksum<double, 27><<<grid, 256, 0, stream_>>>((const double*)o, geo_, mode, d_.z_origin, gnx, gny, d);
+        if (d_.q == 19) k_checksum<double, 19><<<grid, 256, 0, stream_>>>((const double*)o, geo_, mode, d_.z_origin, gnx, gny, d, d_slot_, uniform_slot_, skip);
+        else k_checksum<double, 27><<<grid, 256, 0, stream_>>>((const double*)o, geo_, mode, d_.z_origin, gnx, gny, d, d_slot_, uniform_slot_, skip);
     } else {
-        if (d_.q == 19) k_checksum<float, 19><<<grid, 256, 0, stream_>>>((const float*)o, geo_, mode, d_.z_origin, gnx, gny, d);
-        else k_checksum<float, 27><<<grid, 256, 0, stream_>>>((const float*)o, geo_, mode, d_.z_origin, gnx, gny, d);
+        if (d_.q == 19) k_checksum<float, 19><<<grid, 256, 0, stream_>>>((const float*)o, geo_, mode, d_.z_origin, gnx, gny, d, d_slot_, uniform_slot_, skip);
+        else k_checksum<float, 27><<<grid, 256, 0, stream_>>>((const float*)o, geo_, mode, d_.z_origin, gnx, gny, d, d_slot_, uniform_slot_, skip);
     }
     cuda_check(cudaGetLastError(), "k_checksum");
     cuda_check(cudaMemcpyAsync(per_dir, d, size_t(d_.q) * 8, cudaMemcpyDeviceToHost, stream_), "d2h");
@@ -1647,7 +1707,7 @@ void Lattice::checksum(unsigned long long* per_dir) {
 }
 
 void Lattice::gather_macroscopic(double* rho, double* ux, double* uy, double* uz) {
-    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    DeviceGuard dg(device_);
     cuda_check(cudaStreamSynchronize(stream_), "sync");
     std::vector<MacroSlot> ms(std::max<std::size_t>(chains_.size(), 1));
     for (std::size_t s = 0; s < chains_.size(); ++s) {
@@ -1691,23 +1751,41 @@ void Lattice::gather_macroscopic(double* rho, double* ux, double* uy, double* uz
 }
 
 void Lattice::check_error_flag() {
+    DeviceGuard dg(device_);
     if (!(lower_.linked || upper_.linked)) return;
-    unsigned long long err = 0;
-    cuda_check(cudaMemcpy(&err, d_flags_ + 3, sizeof(err), cudaMemcpyDeviceToHost), "read flags");
-    if (err)
-        throw ExchangeError("halo exchange timed out waiting for a neighbour at step " +
-                            std::to_string(err));
+    unsigned long long fl[4] = {0, 0, 0, 0};
+    cuda_check(cudaMemcpy(fl, d_flags_, sizeof(fl), cudaMemcpyDeviceToHost), "read flags");
+    if (!fl[3]) return;
+    // flags[3] = 1-based index of the step whose halo wait timed out; that step
+    // and every later one wrote nothing, so the state after the last completed
+    // step (flags[2] of them) is intact in the buffer of its parity.
+    const int64_t done = int64_t(fl[3]) - 1;
+    const int64_t failed = halo_steps_ - done;  // enqueued linked steps that wrote nothing
+    if (failed > 0) {
+        if (failed & 1) cur_ = 1 - cur_;
+        steps_ -= failed;
+        halo_steps_ = done;
+        invalidate_graph();
+    }
+    throw ExchangeError("halo exchange timed out waiting for a neighbour at step " + std::to_string(fl[3]) +
+                        " (state kept after step " + std::to_string(done) + ")");
+}
+
+void Lattice::set_halo_timeout(double seconds) {
+    if (!(seconds > 0)) throw std::invalid_argument("halo timeout must be positive");
+    halo_timeout_ns_ = static_cast<unsigned long long>(seconds * 1e9);
+    invalidate_graph();
 }
 
 void Lattice::synchronize() {
-    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    DeviceGuard dg(device_);
     cuda_check(cudaStreamSynchronize(stream_), "step");
     check_error_flag();
 }
 
 double Lattice::time_steps(int64_t nsteps) {
     check_dispatch();
-    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    DeviceGuard dg(device_);
     if (nsteps >= 4) {  // build the graph outside the timed region
         const bool aligned = aa() ? aa_odd_layout_ : cur_ == 0;
         if (!aligned) step(1);
@@ -1777,7 +1855,7 @@ std::vector<uint8_t> Lattice::export_ipc() const {
     b.nz = geo_.nz;
     b.dstride = geo_.dstride;
     b.base_off_bytes = base_off_ * (d_.precision_bits / 8);
-    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    DeviceGuard dg(device_);
     for (int k = 0; k < 2; ++k) cuda_check(cudaIpcGetMemHandle(&b.buf[k], buf_[k]), "ipc handle");
     cuda_check(cudaIpcGetMemHandle(&b.flags, d_flags_), "ipc handle");
     std::vector<uint8_t> out(sizeof(b));
@@ -1794,7 +1872,7 @@ void Lattice::link_ipc(int side, const void* blob, std::size_t len) {
     if (b.magic != kIpcMagic) throw std::invalid_argument("bad IPC blob");
     if (b.nx != geo_.nx || b.ny != geo_.ny || b.q != d_.q || b.bits != d_.precision_bits)
         throw std::invalid_argument("linked slabs must share nx, ny, q and precision");
-    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    DeviceGuard dg(device_);
     Peer& p = side == 0 ? lower_ : upper_;
     void* bases[3];
     for (int k = 0; k < 2; ++k)

@@ -24,6 +24,26 @@ namespace dlb {
 
 void cuda_check(cudaError_t e, const char* what);
 
+// Makes `dev` current for the scope of a Lattice entry point and restores the
+// caller's device afterwards: slabs of one process may sit on different GPUs,
+// and every launch / allocation must land on the slab's own device.
+class DeviceGuard {
+  public:
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev_) != cudaSuccess) prev_ = -1;
+        if (prev_ == dev) prev_ = -1;
+        else cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+    }
+    ~DeviceGuard() {
+        if (prev_ >= 0) cudaSetDevice(prev_);
+    }
+    DeviceGuard(const DeviceGuard&) = delete;
+    DeviceGuard& operator=(const DeviceGuard&) = delete;
+
+  private:
+    int prev_ = -1;
+};
+
 // Halo neighbour of a slab (the lower one at z = -1, the upper at z = nz).
 struct Peer {
     bool linked = false;
@@ -69,12 +89,16 @@ class Lattice {
     void enqueue_step();  // one step, no dispatch check (group stepping)
     void check_dispatch() const;
     void synchronize();
-    void checksum(unsigned long long* per_dir);
+    void checksum(unsigned long long* per_dir, bool active_only = false);
     void gather_macroscopic(double* rho, double* ux, double* uy, double* uz);  // q order-independent 64-bit sums
     double time_steps(int64_t nsteps);
 
+    // Halo wait limit per step (a neighbour that does not finish its boundary
+    // planes within it makes the step fail with DLB_ERROR_EXCHANGE).
+    void set_halo_timeout(double seconds);
     void link_lower(Lattice& lower);  // same process
-    void exchange();                  // prime the neighbours' ghost planes
+    void exchange();                  // prime the neighbours' ghost planes (clears an exchange error)
+    void quiesce();                   // wait for this slab's streams (no error check)
     std::vector<uint8_t> export_ipc() const;
     void link_ipc(int side, const void* blob, std::size_t len);
 
@@ -125,6 +149,11 @@ class Lattice {
     int device_ = 0;
     cudaStream_t stream_ = nullptr;
     cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+    // linked slabs: halo wait + boundary launch on halo_stream_ (high priority)
+    // concurrent with the interior launch on stream_, forked / joined per step
+    cudaStream_t halo_stream_ = nullptr;
+    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+    unsigned long long halo_timeout_ns_ = 20ull * 1000 * 1000 * 1000;  // DLB_HALO_TIMEOUT_MS / set_halo_timeout
     Geo geo_{};
     int align_ = 32;            // elements per 128 B
     int skip_group_ = 8;        // masked porous sweep: cells per skip group (power of two <= 32)
@@ -168,6 +197,7 @@ class Lattice {
     unsigned long long* d_flags_ = nullptr;  // [0] from lower, [1] from upper, [2] my step, [3] error
     unsigned int* d_counter_ = nullptr;      // last-block ticket of the boundary launch
     int64_t steps_ = 0;
+    int64_t halo_steps_ = 0;  // linked steps enqueued (host mirror of flags[2] once they ran)
     int64_t device_bytes_ = 0;
     void* staging_ = nullptr;
     std::size_t staging_bytes_ = 0;

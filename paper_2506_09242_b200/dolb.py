@@ -435,8 +435,11 @@ class DeviceRun:
         state fill / upload of a decomposed run."""
         if len(self.slabs) == 1 and self.dist is None:
             return
-        for s in self.slabs:
-            check(_capi.lib().dlb_lattice_exchange(s.handle))
+        if len(self.slabs) > 1:
+            arr = (C.c_void_p * len(self.slabs))(*[s.handle.value for s in self.slabs])
+            check(_capi.lib().dlb_lattices_exchange(arr, len(self.slabs)))
+        else:
+            check(_capi.lib().dlb_lattice_exchange(self.slabs[0].handle))
         if self.dist is not None and self.dist[1] > 1:
             import torch.distributed as dist
             dist.barrier()
@@ -457,6 +460,18 @@ class DeviceRun:
         else:
             arr = (C.c_void_p * len(self.slabs))(*[s.handle.value for s in self.slabs])
             check(_capi.lib().dlb_lattices_step(arr, len(self.slabs), nsteps))
+
+    def set_halo_timeout(self, seconds: float, k: int | None = None):
+        """Halo wait limit of slab k (all slabs if None); a neighbour that stays
+        silent longer fails the step with ExchangeError (state kept at the last
+        completed step)."""
+        for j, s in enumerate(self.slabs):
+            if k is None or j == k:
+                check(_capi.lib().dlb_lattice_set_halo_timeout(s.handle, float(seconds)))
+
+    def step_slab(self, k: int, nsteps: int):
+        """Advance slab k alone (its neighbours must keep up; fault tests)."""
+        check(_capi.lib().dlb_lattice_step(self.slabs[k].handle, nsteps))
 
     def synchronize(self):
         for s in self.slabs:
@@ -481,13 +496,15 @@ class DeviceRun:
         check(_capi.lib().dlb_lattice_traffic(self.slabs[k].handle, C.byref(b), C.byref(d), C.byref(l)))
         return b.value, d.value, l.value
 
-    def checksum(self) -> list:
+    def checksum(self, active_only: bool = False) -> list:
         """Per-direction exact checksums of this process's cells (sum of slab
-        checksums mod 2^64; equal to the reference's for identical states)."""
+        checksums mod 2^64; equal to the reference's for identical states).
+        active_only: only the cells whose chain is not NoDynamics."""
         tot = np.zeros(self.q, np.uint64)
+        fn = _capi.lib().dlb_lattice_checksum_active if active_only else _capi.lib().dlb_lattice_checksum
         for s in self.slabs:
             buf = np.zeros(self.q, np.uint64)
-            check(_capi.lib().dlb_lattice_checksum(s.handle, buf.ctypes.data))
+            check(fn(s.handle, buf.ctypes.data))
             tot = tot + buf  # uint64 wraps
         return [int(v) for v in tot]
 
