@@ -138,14 +138,23 @@ def run_reference_arm(args, cfgname):
     if q != 19:
         print(json.dumps({"impl": "reference", "unavailable": "the reference has no D3Q27 path"}))
         return
-    Ls = min(L, 256 if bits == 32 else 192)
-    res = cpu_reference(kind, Ls, Re, Ma, coll, q, bits, args.warmup, args.steps, reps=1)
+    # bounded sample: 512^3 (fp32) / 256^3 (fp64); the full 1024^3 fp32 lattice
+    # needs ~187 GB in the reference's block layout (two populations + 16 B of
+    # tag / param / cell index per cell, one envelope per worker block), more
+    # than the box's host RAM leaves for it
+    Ls = min(L, 512 if bits == 32 else 256)
+    if kind == "porous":
+        Ls = min(L, 256)
+    res = cpu_reference(kind, Ls, Re, Ma, coll, q, bits, args.warmup, args.steps, reps=3)
     if res is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
     mean, reps_, workers = res
     sample = (f"{kind} {Ls}^3 D3Q{q} {coll} fp{bits}, {workers} workers x z-blocks, "
-              f"warmup {args.warmup} + {args.steps} steps (measure_mlups semantics)")
+              f"warmup {args.warmup} + 3 repetitions x {args.steps} steps, mean (perf::measure_mlups "
+              f"semantics, perfmodel.cpp:94-121); per-repetition MLUPS {[round(v, 1) for v in reps_]}")
+    if Ls < L:
+        sample += f"; {Ls}^3 instead of {L}^3: host RAM (the reference's full-size layout does not fit)"
     ms = Ls ** 3 / (mean * 1e6) * 1e3
     line = {
         "impl": "reference", "metric": "MLUPS", "value": mean, "unit": "MLUPS",
@@ -160,54 +169,100 @@ def run_reference_arm(args, cfgname):
     print(json.dumps(line), flush=True)
 
 
-def e2e_block(L, bits, steps, warmup):
+def e2e_block(L, bits, steps, warmup, rank=0, world=1, barrier=lambda: None, max_over_ranks=lambda v: v):
     """The same metric through dlb_collide_and_stream on pinned HOST buffers
     (reference-facing drop-in for collide_and_stream(AcceleratedBlock<T>&, ...)):
     per step the caller refreshes the periodic envelope, the call copies the
-    block host->device, steps, and copies the new state device->host."""
+    block host->device, steps, and copies the new state device->host. With N
+    ranks every rank steps its own z-slab block of the L^3 domain (the
+    reference's one block per worker) on its GPU; the envelope is refreshed
+    from the block itself (the bytes of the host exchange, without the
+    transport); the time is the max over ranks."""
     import ctypes as C
 
     import paper_2506_09242_b200 as dlb
     from paper_2506_09242_b200 import _capi
+    from paper_2506_09242_b200.dolb import _Lattice
     cfg = dlb.CaseConfig(kind="tgv", L=L, Re=1600.0, Ma=0.2)
     setup = dlb.init_tgv(cfg)
     reg = dlb.DynamicsRegistry()
     slot = reg.register_chain(setup.chains[0])
     dt = np.float32 if bits == 32 else np.float64
-    e = L + 2
-    nbytes = 19 * e ** 3 * np.dtype(dt).itemsize
-    p = C.c_void_p()
+    z0, nz = dlb.partition(L, world)[rank]
+    ex, ez = L + 2, nz + 2
+    nbytes = 19 * ex * ex * ez * np.dtype(dt).itemsize
+    p, p2 = C.c_void_p(), C.c_void_p()
     _capi.check(_capi.lib().dlb_host_alloc(nbytes, C.byref(p)))
+    _capi.check(_capi.lib().dlb_host_alloc(nbytes, C.byref(p2)))
     try:
-        blk = np.ctypeslib.as_array((C.c_uint8 * nbytes).from_address(p.value)).view(dt).reshape(19, e, e, e)
-        # initial state from the device path (same TGV fill), written into the block
-        run = dlb.build_run(setup, reg, precision=bits)
-        blk[:, 1:-1, 1:-1, 1:-1] = run.gather_raw().reshape(19, L, L, L)
-        del run
-        tag = np.full((e, e, e), -1, np.int32)
+        blk = np.ctypeslib.as_array((C.c_uint8 * nbytes).from_address(p.value)).view(dt).reshape(19, ez, ex, ex)
+        out = np.ctypeslib.as_array((C.c_uint8 * nbytes).from_address(p2.value)).view(dt).reshape(19, ez, ex, ex)
+        out[:] = 0
+        # initial state: this block's planes of the TGV state, built on the device
+        d = _capi.LatticeDesc()
+        d.dims[0], d.dims[1], d.dims[2] = L, L, nz
+        for a in range(3):
+            d.periodic[a] = 1
+        d.q, d.precision_bits, d.arith = 19, bits, _capi.ARITH_EXACT
+        d.layout = _capi.LAYOUT_AA if world == 1 else _capi.LAYOUT_TWO_POP  # (AA: single-slab lattices)
+        d.device = int(__import__("torch").cuda.current_device())
+        d.z_origin, d.global_nz = z0, L
+        lat = _Lattice(d, reg)
+        _capi.check(_capi.lib().dlb_lattice_set_uniform_slot(lat.handle, slot))
+        _capi.check(_capi.lib().dlb_lattice_fill_tgv(lat.handle, L, cfg.lattice_velocity()))
+        raw = np.zeros(19 * L * L * nz, dt)
+        _capi.check(_capi.lib().dlb_lattice_download_raw(lat.handle, raw.ctypes.data))
+        del lat
+        blk[:, 1:-1, 1:-1, 1:-1] = raw.reshape(19, nz, L, L)
+        del raw
+        tag = np.full((ez, ex, ex), -1, np.int32)
         tag[1:-1, 1:-1, 1:-1] = reg.tag_of_slot(slot)
         pidx = np.where(tag >= 0, slot, -1).astype(np.int32)
         ds = dlb.DispatchSet.all_of(reg)
 
-        def refresh():  # refresh_envelope_periodic (accelerated_lattice.cpp:202-238), C ABI
-            dlb.refresh_envelope_periodic(blk, (1, 1, 1))
+        f = [blk, out]  # the block's f_in / f_out, swapped by every call (accelerated_lattice.cpp:199)
+
+        def step():
+            # refresh_envelope_periodic (accelerated_lattice.cpp:202-238), then the step; C ABI
+            dlb.refresh_envelope_periodic(f[0], (1, 1, 1))
+            f[0], f[1] = dlb.collide_and_stream(reg, f[0], tag, pidx, ds, f_out=f[1])
 
         for _ in range(warmup):
-            refresh()
-            dlb.collide_and_stream(reg, blk, tag, pidx, ds)
+            step()
+        barrier()
         t0 = time.perf_counter()
         for _ in range(steps):
-            refresh()
-            dlb.collide_and_stream(reg, blk, tag, pidx, ds)
+            step()
         t1 = time.perf_counter()
-        mlups = L ** 3 * steps / (t1 - t0) / 1e6
-        return {"value": mlups, "unit": "MLUPS", "h2d_bytes_per_step": int(nbytes),
-                "d2h_bytes_per_step": int(19 * L ** 3 * np.dtype(dt).itemsize),
-                "sample": f"host AcceleratedBlock {L}^3 (+envelope) fp{bits}, pinned, {steps} steps, "
-                          "wall clock incl. envelope refresh, H2D, step, D2H",
-                "finite": bool(np.isfinite(blk[:, 1:-1, 1:-1, 1:-1]).all())}
+        barrier()
+        dt_max = max_over_ranks(t1 - t0)
+        mlups = L ** 3 * steps / dt_max / 1e6
+        return {"value": mlups, "unit": "MLUPS", "h2d_bytes_per_step": int(nbytes) * world,
+                "d2h_bytes_per_step": int(19 * L * L * nz * np.dtype(dt).itemsize) * world,
+                "sample": f"host AcceleratedBlock {L}^3 (+envelope) fp{bits} as {world} z-slab block(s), one per "
+                          f"GPU, pinned f_in + f_out swapped per call, {steps} steps, wall clock incl. envelope "
+                          "refresh, H2D, step, D2H",
+                "finite": bool(np.isfinite(f[0][:, 1:-1, 1:-1, 1:-1]).all())}
     finally:
         _capi.lib().dlb_host_free(p)
+        _capi.lib().dlb_host_free(p2)
+
+
+def free_port():
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    return port
+
+
+def spawn_ranks(n):
+    """--gpus N without a launcher: start N ranks (one process per GPU) with
+    torch.distributed.run on this node and pass rank 0's line through."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=dict(os.environ, DLB_BENCH_SPAWNED="1"))
 
 
 def main():
@@ -217,11 +272,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
-    ap.add_argument("--L", type=int, default=None, help="override the edge length (profiling only)")
+    ap.add_argument("--L", type=int, default=None,
+                    help="edge length at N = 1 (profiling / tests; weak-scaling configs still grow with N)")
     ap.add_argument("--arith", default="exact", choices=["exact", "fast"])
     ap.add_argument("--layout", default="twopop", choices=["twopop", "aa"])
     ap.add_argument("--tma", action="store_true", help="TMA-staged dense kernel instead of the plain-load one")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-L", type=int, default=None, help="edge length of the e2e host-block sample")
     ap.add_argument("--porous", default="masked", choices=["dense", "masked", "lists"],
                     help="c4 kernel variant: dense sweep of every cell (reference behaviour), masked "
                          "sweep (NoDynamics segments skipped), or kind-sorted sparse lists")
@@ -233,27 +290,50 @@ def main():
         run_reference_arm(args, args.config)
         return
 
+    rank, world = env_int("RANK", 0), env_int("WORLD_SIZE", 1)
+    if world == 1 and args.gpus > 1 and not os.environ.get("DLB_BENCH_SPAWNED"):
+        sys.exit(spawn_ranks(args.gpus))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but the launcher started {world} rank(s)")
+
     import torch
     import torch.distributed as tdist
 
     import paper_2506_09242_b200 as dlb
 
-    rank, world = env_int("RANK", 0), env_int("WORLD_SIZE", 1)
     local = env_int("LOCAL_RANK", 0)
-    if os.environ.get("DLB_SAME_DEVICE") == "1":  # protocol test: all ranks share GPU 0
+    same_device = os.environ.get("DLB_SAME_DEVICE") == "1"  # protocol test: all ranks share GPU 0
+    if same_device:
         local = 0
-    if world > 1:
-        tdist.init_process_group("gloo")
+    elif torch.cuda.device_count() < world:
+        sys.exit(f"bench.py: {world} ranks but only {torch.cuda.device_count()} visible GPU(s)")
     torch.cuda.set_device(local)
+    # plumbing only (IPC-handle exchange, barriers, the max over ranks): NCCL
+    # with one GPU per rank, gloo when the ranks share a device
+    backend = "gloo" if same_device else "nccl"
+    if world > 1:
+        tdist.init_process_group(backend, device_id=None if same_device else torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            tdist.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cpu" if same_device else f"cuda:{local}")
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        return float(t.item())
 
     kind, L, Re, Ma, coll, q, bits, scaling, desc = CONFIGS[args.config]
-    if scaling == "weak":
-        L = int(round(L * world ** (1.0 / 3.0)))  # perfmodel.cpp:76-85 weak sizes
     if args.L:
         L = args.L
+    if scaling == "weak":
+        L = int(round(L * world ** (1.0 / 3.0)))  # perfmodel.cpp:76-85 weak sizes
     lt = {"BGK": dlb.LinkType.BGK, "TRT": dlb.LinkType.TRT, "RR": dlb.LinkType.RR}[coll]
     skip = False
     extra = {}
+    variant = "dense"
     if kind == "porous":
         cfg = dlb.CaseConfig(kind="porous", L=L, Ma=Ma, collision=lt, q=q, tau=1.0, upstream=40,
                              downstream=40)
@@ -278,25 +358,23 @@ def main():
                         dist=(rank, world) if world > 1 else None, devices=[local], layout=layout,
                         skip_nodynamics=skip, tma=args.tma,
                         sparse_lists=kind == "porous" and variant == "lists")
+    del setup
     cells_total = run.num_cells()
     bpc, dev_bytes, launches = run.traffic()
     kernel = run.kernel_name()
+    links = dict(run.links(0), rank=rank, device=local, slab_z=list(run.parts[rank]))
 
     for _ in range(args.warmup):
         run.advance(1)
     run.synchronize()
-    if world > 1:
-        tdist.barrier()
+    barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         ms = run.time_steps(args.steps)  # CUDA events on the lattice stream
         run.synchronize()
     torch.cuda.synchronize()
-    t = torch.tensor([ms], dtype=torch.float64)
-    if world > 1:
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-        tdist.barrier()
-    ms_max = float(t.item())
+    barrier()
+    ms_max = max_over_ranks(ms)
     ms_step = ms_max / args.steps
     mlups = cells_total * args.steps / (ms_max * 1e-3) / 1e6
 
@@ -319,47 +397,53 @@ def main():
                 traffic = tr[key]["bytes_per_cell"] * my_cells
         except Exception:
             traffic = None
-
-    if rank != 0:
-        if world > 1:
-            tdist.barrier()
-        return
+    all_links = [links]
+    if world > 1:
+        all_links = [None] * world
+        tdist.all_gather_object(all_links, links)
 
     cpu = None
-    if world == 1 and not args.no_cpu and q == 19:
-        Ls = min(L, 128 if kind != "porous" else 96)
+    if rank == 0 and world == 1 and not args.no_cpu and q == 19:
+        Ls = min(L, 256 if (kind == "porous" or bits == 64) else 512)
         res = cpu_reference(kind, Ls, Re, Ma, coll, q, bits, 2, 8, reps=3)
         if res:
             mean, reps_, workers = res
             cpu = {"value": mean, "unit": "MLUPS", "cores": workers, "kind": "reference",
                    "sample": f"{kind} {Ls}^3 D3Q{q} {coll} fp{bits}: reference MultiBlockRun, "
-                             f"{workers} workers x z-blocks, warmup 2, 3 reps x 8 steps"}
+                             f"{workers} workers x z-blocks, warmup 2, 3 reps x 8 steps (mean)"}
     e2e = None
     if not args.no_e2e and q == 19 and kind == "tgv":
         del run
         torch.cuda.empty_cache()
-        e2e = e2e_block(min(L, 512), bits, max(2, min(args.steps, 5)), 1)
-    line = {
-        "metric": "MLUPS", "value": mlups, "unit": "MLUPS", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling,
-        "vs_baseline": None, "dtype": "f32" if bits == 32 else "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: {desc}", "L": L, "cells": cells_total,
-                   "parallelism": f"z-slab x{world}",
-                   "layout": "AA in-place SoA" if layout == "aa" else "two-population SoA",
-                   "arith": args.arith, "kernel": kernel,
-                   "l2": "inputs larger than L2 (state resident in HBM)",
-                   "device_bytes_per_gpu": dev_bytes, **extra},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "bytes_per_cell": bpc},
-        "gpu_launches": launches * args.steps,
-        "clocks": clk.summary(),
-        "cpu_baseline": cpu,
-        "e2e": e2e,
-    }
-    print(json.dumps(line), flush=True)
+        e2e = e2e_block(args.e2e_L or min(L, 512), bits, max(2, min(args.steps, 5)), 1, rank, world,
+                        barrier, max_over_ranks)
+    if rank == 0:
+        line = {
+            "metric": "MLUPS", "value": mlups, "unit": "MLUPS", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling,
+            "vs_baseline": None, "dtype": "f32" if bits == 32 else "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {desc}", "L": L, "cells": cells_total,
+                       "parallelism": f"z-slab x{world}",
+                       "layout": "AA in-place SoA" if layout == "aa" else "two-population SoA",
+                       "arith": args.arith, "kernel": kernel,
+                       "l2": "inputs larger than L2 (state resident in HBM)",
+                       "device_bytes_per_gpu": dev_bytes,
+                       "halo": {"transport": "peer-memory stores from the boundary-plane kernel (CUDA IPC "
+                                             "mappings over NVLink), overlapped with the interior launch; "
+                                             f"torch.distributed/{backend if world > 1 else '-'} for plumbing",
+                                "per_rank": all_links}, **extra},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                         "bytes_per_cell": bpc},
+            "gpu_launches": launches * args.steps,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+        }
+        print(json.dumps(line), flush=True)
+    barrier()
     if world > 1:
-        tdist.barrier()
+        tdist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -189,6 +189,18 @@ DLB_API dlb_status dlb_lattices_exchange(dlb_lattice** lats, size_t n);
  * lattice is left at its last completed step. dlb_lattice_exchange clears the
  * error once the slabs are back at one step count. */
 DLB_API dlb_status dlb_lattice_set_halo_timeout(dlb_lattice* lat, double seconds);
+/* Link state of a slab: *lower / *upper = 0 not linked, 1 linked to a slab on
+ * the same GPU, 2 linked to a slab on another GPU (peer memory over NVLink);
+ * *halo_bytes_per_step = population bytes this slab pushes into its
+ * neighbours' ghost planes per step (nx * ny * 5 (D3Q19) or 9 (D3Q27) links
+ * per linked face). */
+DLB_API dlb_status dlb_lattice_links(dlb_lattice* lat, int32_t* lower, int32_t* upper,
+                                     int64_t* halo_bytes_per_step);
+/* With DLB_TRACE_HALO set (CUDA graphs then off): timeline of the linked steps
+ * since the last call, ms from the first event, 5 values per step (halo wait
+ * begin / end and boundary-launch end on the halo stream, interior launch
+ * begin / end on the main stream). out may be NULL to query the count. */
+DLB_API dlb_status dlb_lattice_halo_trace(dlb_lattice* lat, double* out, size_t cap, size_t* n_out);
 /* Across processes: export an opaque blob (CUDA IPC handles), ship it with any
  * transport (e.g. torch.distributed), link it as the lower (side 0) or upper
  * (side 1) neighbour. */
@@ -285,9 +297,15 @@ DLB_API dlb_status dlb_lattice_velocity_planes(dlb_lattice* lat, int32_t z0, int
 /* ---- drop-in for collide_and_stream<T> on a host AcceleratedBlock ----------- */
 /* Envelope-inclusive SoA arrays exactly as AcceleratedBlock<T> holds them
  * (accelerated_lattice.hpp:86-112): f_in/f_out q*ext[0]*ext[1]*ext[2] values,
- * tag/param_index ext-volume int32. Pre: envelope of f_in current. Post: f_in
- * holds the new state and f_out the previous one (the reference's swap,
- * accelerated_lattice.cpp:199); f_out may be NULL to skip that copy. */
+ * tag/param_index ext-volume int32. Pre: envelope of f_in current.
+ * Post, f_out != NULL: the new interior state was written into the f_out
+ * buffer (its envelope untouched), the previous state is left in the f_in
+ * buffer, and the view's two pointers are SWAPPED -- view->f_in is the new
+ * state, as after the reference's std::swap of the two arrays
+ * (accelerated_lattice.cpp:199); callers owning the arrays swap them when the
+ * pointers came back swapped. f_out == NULL: the new state
+ * overwrites the interior of f_in in place (its envelope untouched).
+ * Errors (DLB_ERROR_DISPATCH ...) leave both buffers and the view unchanged. */
 typedef struct dlb_block_view {
     int32_t precision_bits;
     int32_t q;
@@ -304,6 +322,12 @@ DLB_API dlb_status dlb_collide_and_stream(const dlb_registry* reg, dlb_block_vie
  * host block: copy interior edge planes into the opposite envelope along the
  * periodic axes (x, then y over full x rows, then z over full planes). */
 DLB_API dlb_status dlb_refresh_envelope_periodic(dlb_block_view* block, const int32_t* periodic);
+/* The call keeps a device context per block shape (mirrors, slots, recipes)
+ * for the next call on the same block; it is tied to the registry's content
+ * (a new registration or dlb_registry_free invalidates it). Release them all
+ * (device memory back) / query how many are held. */
+DLB_API void dlb_block_cache_release(void);
+DLB_API dlb_status dlb_block_cache_info(size_t* entries, int64_t* device_bytes);
 /* Pinned host memory for the block API (page-locked, for full-rate copies). */
 DLB_API dlb_status dlb_host_alloc(size_t bytes, void** out);
 DLB_API void dlb_host_free(void* ptr);

@@ -113,6 +113,10 @@ _SIGS = {
     "dlb_lattice_checksum_active": ([C.c_void_p, C.c_void_p], C.c_int),
     "dlb_lattice_set_halo_timeout": ([C.c_void_p, C.c_double], C.c_int),
     "dlb_lattices_exchange": ([C.c_void_p, C.c_size_t], C.c_int),
+    "dlb_block_cache_release": ([], None),
+    "dlb_block_cache_info": ([C.c_void_p, C.c_void_p], C.c_int),
+    "dlb_lattice_links": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+    "dlb_lattice_halo_trace": ([C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p], C.c_int),
     "dlb_lattice_reduce_count": ([C.c_void_p, C.POINTER(ReduceArgs), C.POINTER(C.c_int64)], C.c_int),
     "dlb_lattice_reduce_parts": ([C.c_void_p, C.POINTER(ReduceArgs), C.c_int64, C.c_int64, C.c_void_p,
                                   C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),

@@ -5,6 +5,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
+#include <atomic>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -19,6 +21,10 @@
 
 struct dlb_registry {
     dlb::DynamicsRegistry reg;
+    // identity of this registry's content for the host-block device cache:
+    // a process-unique serial, and a generation bumped by every registration
+    uint64_t serial = 0;
+    uint64_t generation = 0;
 };
 
 struct dlb_lattice {
@@ -72,15 +78,18 @@ void write_string(const std::string& s, char* buf, size_t cap, size_t* len_out) 
     std::memcpy(buf, s.c_str(), s.size() + 1);
 }
 
-// Cached device lattice for the host-block drop-in (one per block shape).
+// Cached device lattice for the host-block drop-in (one per block shape),
+// valid for one registry content (serial + generation): a freed registry or a
+// new registration never reuses stale recipes. Released by dlb_registry_free
+// (its entries) and dlb_block_cache_release (all).
 struct BlockCtx {
     std::unique_ptr<dlb::Lattice> lat;
-    const dlb_registry* reg = nullptr;
-    int instances = -1;
+    uint64_t reg_serial = 0, reg_generation = 0;
     std::vector<int32_t> slots;
 };
 std::mutex g_block_mu;
 std::map<std::vector<int64_t>, BlockCtx> g_blocks;
+std::atomic<uint64_t> g_registry_serial{0};
 
 }  // namespace
 
@@ -100,10 +109,40 @@ DLB_API dlb_status dlb_chain_canonical(const char* chain, char* buf, size_t cap,
 
 DLB_API dlb_status dlb_registry_new(dlb_registry** out) {
     DLB_REQUIRE(out);
-    return guarded([&] { *out = new dlb_registry(); });
+    return guarded([&] {
+        auto* r = new dlb_registry();
+        r->serial = ++g_registry_serial;
+        *out = r;
+    });
 }
 
-DLB_API void dlb_registry_free(dlb_registry* reg) { delete reg; }
+DLB_API void dlb_registry_free(dlb_registry* reg) {
+    if (!reg) return;
+    {
+        std::lock_guard<std::mutex> lock(g_block_mu);
+        for (auto it = g_blocks.begin(); it != g_blocks.end();)
+            it = it->second.reg_serial == reg->serial ? g_blocks.erase(it) : std::next(it);
+    }
+    delete reg;
+}
+
+DLB_API void dlb_block_cache_release(void) {
+    std::lock_guard<std::mutex> lock(g_block_mu);
+    g_blocks.clear();
+}
+
+DLB_API dlb_status dlb_block_cache_info(size_t* entries, int64_t* device_bytes) {
+    DLB_REQUIRE(entries);
+    std::lock_guard<std::mutex> lock(g_block_mu);
+    *entries = g_blocks.size();
+    if (device_bytes) {
+        int64_t b = 0;
+        for (const auto& kv : g_blocks)
+            if (kv.second.lat) b += kv.second.lat->device_bytes();
+        *device_bytes = b;
+    }
+    return DLB_OK;
+}
 
 DLB_API dlb_status dlb_registry_register(dlb_registry* reg, const char* chain, const double* params,
                                          size_t n_params, int32_t* slot_out) {
@@ -117,6 +156,7 @@ DLB_API dlb_status dlb_registry_register(dlb_registry* reg, const char* chain, c
         dlb::validate_chain(c.links);
         c.params = dlb::deserialize_params(c.links, params, n_params);
         *slot_out = reg->reg.register_chain(c);
+        ++reg->generation;
     });
 }
 
@@ -424,6 +464,28 @@ DLB_API dlb_status dlb_lattice_set_halo_timeout(dlb_lattice* lat, double seconds
     return guarded([&] { lat->lat->set_halo_timeout(seconds); });
 }
 
+DLB_API dlb_status dlb_lattice_links(dlb_lattice* lat, int32_t* lower, int32_t* upper,
+                                     int64_t* halo_bytes_per_step) {
+    DLB_REQUIRE(lat);
+    DLB_REQUIRE(lower && upper && halo_bytes_per_step);
+    return guarded([&] {
+        int lo = 0, up = 0;
+        lat->lat->links(&lo, &up, halo_bytes_per_step);
+        *lower = lo;
+        *upper = up;
+    });
+}
+
+DLB_API dlb_status dlb_lattice_halo_trace(dlb_lattice* lat, double* out, size_t cap, size_t* n_out) {
+    DLB_REQUIRE(lat);
+    DLB_REQUIRE(n_out);
+    return guarded([&] {
+        const auto t = lat->lat->halo_trace(out != nullptr);  // NULL: count only, keep the events
+        *n_out = t.size();
+        if (out) std::memcpy(out, t.data(), std::min(cap, t.size()) * sizeof(double));
+    });
+}
+
 DLB_API dlb_status dlb_lattice_export_ipc(dlb_lattice* lat, void* blob, size_t cap, size_t* len_out) {
     DLB_REQUIRE(lat);
     return guarded([&] {
@@ -472,7 +534,7 @@ DLB_API dlb_status dlb_collide_and_stream(const dlb_registry* reg, dlb_block_vie
         std::lock_guard<std::mutex> lock(g_block_mu);
         const std::vector<int64_t> key = {nx, ny, nz, block->q, block->precision_bits};
         BlockCtx& ctx = g_blocks[key];
-        const bool have_ctx = ctx.lat && ctx.reg == reg && ctx.instances == reg->reg.num_instances() &&
+        const bool have_ctx = ctx.lat && ctx.reg_serial == reg->serial && ctx.reg_generation == reg->generation &&
                               ctx.slots.size() == size_t(nx * ny * nz);
         const auto t_call = std::chrono::steady_clock::now();
         const int nw = int(std::max<int64_t>(1, std::min<int64_t>(nz, std::thread::hardware_concurrency())));
@@ -504,17 +566,21 @@ DLB_API dlb_status dlb_collide_and_stream(const dlb_registry* reg, dlb_block_vie
                     }
             });
         }
-        cudaPointerAttributes attr{};
-        const bool pinned = cudaPointerGetAttributes(&attr, block->f_in) == cudaSuccess &&
-                            attr.type == cudaMemoryTypeHost && attr.devicePointer == block->f_in;
-        cudaGetLastError();
+        auto is_pinned = [](const void* p) {
+            cudaPointerAttributes attr{};
+            const bool ok = cudaPointerGetAttributes(&attr, p) == cudaSuccess && attr.type == cudaMemoryTypeHost &&
+                            attr.devicePointer == p;
+            cudaGetLastError();
+            return ok;
+        };
+        const bool pinned = is_pinned(block->f_in) && (!block->f_out || is_pinned(block->f_out));
         // While the scan runs, speculatively start the pinned pipeline with the
         // cached slots: host->device copies and the step write device memory
         // only; the copy-back into the caller's block waits for the verdict.
         bool speculative = false;
         if (have_ctx && pinned) {
             try {
-                ctx.lat->begin_host_block(block->f_in, ext);
+                ctx.lat->begin_host_block(block->f_in, ext, block->f_out);
                 speculative = true;
             } catch (...) {
                 for (auto& t : th) t.join();
@@ -554,8 +620,9 @@ DLB_API dlb_status dlb_collide_and_stream(const dlb_registry* reg, dlb_block_vie
             ctx.lat.reset();
             ctx.lat = std::make_unique<dlb::Lattice>(d, reg->reg);  // envelope on every axis
             ctx.lat->set_periodic_override(false, false, false);
-            ctx.reg = reg;
-            ctx.instances = reg->reg.num_instances();
+            ctx.reg_serial = reg->serial;
+            ctx.reg_generation = reg->generation;
+            ctx.slots.clear();
         }
         bool any_change = !have_ctx;
         for (char c : changed) any_change = any_change || c;
@@ -569,9 +636,6 @@ DLB_API dlb_status dlb_collide_and_stream(const dlb_registry* reg, dlb_block_vie
                                 size_t(nx) * sizeof(int32_t));
             ctx.lat->set_slots(ctx.slots.data());
         }
-        const size_t bytes = size_t(block->q) * size_t(ext[0] * ext[1] * ext[2]) *
-                             size_t(block->precision_bits / 8);
-        if (block->f_out) std::memcpy(block->f_out, block->f_in, bytes);
         if (speculative) {
             ctx.lat->finish_host_block();
             if (std::getenv("DLB_TRACE_BLOCK")) {
@@ -582,52 +646,82 @@ DLB_API dlb_status dlb_collide_and_stream(const dlb_registry* reg, dlb_block_vie
             }
         } else if (pinned) {
             // pinned: 3-stage H2D / compute / D2H pipeline (Lattice::step_host_block)
-            ctx.lat->step_host_block(block->f_in, ext);
+            ctx.lat->step_host_block(block->f_in, ext, block->f_out);
         } else {
             // pageable memory: staged copies through device memory
             ctx.lat->upload_block(block->f_in, ext);
             ctx.lat->enqueue_step();
-            ctx.lat->download_block_interior(block->f_in, ext, 0);
+            ctx.lat->download_block_interior(block->f_out ? block->f_out : block->f_in, ext, 0);
             ctx.lat->synchronize();
         }
+        // the reference's swap (accelerated_lattice.cpp:199): the buffer that
+        // received the new state becomes f_in, the untouched previous state f_out
+        if (block->f_out) std::swap(block->f_in, block->f_out);
     });
 }
 
 // refresh_envelope_periodic<T> (accelerated_lattice.cpp:202-238) on a host
-// block: axis-by-axis, later axes spanning the full extent of earlier ones;
-// parallel over directions.
+// block: axis-by-axis, later axes spanning the full extent of earlier ones.
+// Three phases (x, y, z) with a barrier between them; inside a phase the
+// (direction, z-range) pieces run on all host threads.
+}  // extern "C"
+namespace {
+template <typename T>
+void refresh_host_envelope(T* base, const int64_t n[3], const int32_t* periodic, int q) {
+    const int64_t e0 = n[0] + 2, e1 = n[1] + 2, e2 = n[2] + 2;
+    const int64_t vol = e0 * e1 * e2;
+    const int nt = int(std::max(1u, std::min(64u, std::thread::hardware_concurrency())));
+    auto parallel = [&](int64_t items, const std::function<void(int64_t, int64_t)>& fn) {
+        const int64_t per = (items + nt - 1) / nt;
+        std::vector<std::thread> th;
+        for (int64_t b = 0; b < items; b += per) th.emplace_back(fn, b, std::min(items, b + per));
+        for (auto& t : th) t.join();
+    };
+    const int64_t rows = int64_t(q) * n[2];  // (direction, interior z) pairs
+    if (periodic[0])  // x: interior y, z
+        parallel(rows, [&](int64_t r0, int64_t r1) {
+            for (int64_t r = r0; r < r1; ++r) {
+                T* f = base + (r / n[2]) * vol + ((r % n[2]) + 1) * e0 * e1;
+                for (int64_t y = 1; y <= n[1]; ++y) {
+                    T* row = f + y * e0;
+                    row[0] = row[n[0]];
+                    row[n[0] + 1] = row[1];
+                }
+            }
+        });
+    if (periodic[1])  // y: full x rows, interior z
+        parallel(rows, [&](int64_t r0, int64_t r1) {
+            for (int64_t r = r0; r < r1; ++r) {
+                T* f = base + (r / n[2]) * vol + ((r % n[2]) + 1) * e0 * e1;
+                std::memcpy(f, f + n[1] * e0, std::size_t(e0) * sizeof(T));
+                std::memcpy(f + (n[1] + 1) * e0, f + e0, std::size_t(e0) * sizeof(T));
+            }
+        });
+    if (periodic[2])  // z: full planes
+        parallel(int64_t(q) * 2, [&](int64_t k0, int64_t k1) {
+            for (int64_t k = k0; k < k1; ++k) {
+                T* f = base + (k / 2) * vol;
+                const std::size_t pb = std::size_t(e0 * e1) * sizeof(T);
+                if (k % 2 == 0) std::memcpy(f, f + n[2] * e0 * e1, pb);
+                else std::memcpy(f + (n[2] + 1) * e0 * e1, f + e0 * e1, pb);
+            }
+        });
+    (void)e2;
+}
+}  // namespace
+extern "C" {
+
 DLB_API dlb_status dlb_refresh_envelope_periodic(dlb_block_view* block, const int32_t* periodic) {
     DLB_REQUIRE(block);
     DLB_REQUIRE(block->f_in);
     DLB_REQUIRE(periodic);
     return guarded([&] {
-        const int64_t e[3] = {block->interior[0] + 2, block->interior[1] + 2, block->interior[2] + 2};
         const int64_t n[3] = {block->interior[0], block->interior[1], block->interior[2]};
-        const int64_t vol = e[0] * e[1] * e[2];
-        const int s = block->precision_bits / 8;
-        char* base = static_cast<char*>(block->f_in);
-        auto work = [&](int i) {
-            char* f = base + std::size_t(i) * vol * s;
-            auto at = [&](int64_t x, int64_t y, int64_t z) { return f + ((z * e[1] + y) * e[0] + x) * s; };
-            if (periodic[0])  // x: interior y, z
-                for (int64_t z = 1; z <= n[2]; ++z)
-                    for (int64_t y = 1; y <= n[1]; ++y) {
-                        std::memcpy(at(0, y, z), at(n[0], y, z), s);
-                        std::memcpy(at(n[0] + 1, y, z), at(1, y, z), s);
-                    }
-            if (periodic[1])  // y: full x rows, interior z
-                for (int64_t z = 1; z <= n[2]; ++z) {
-                    std::memcpy(at(0, 0, z), at(0, n[1], z), e[0] * s);
-                    std::memcpy(at(0, n[1] + 1, z), at(0, 1, z), e[0] * s);
-                }
-            if (periodic[2]) {  // z: full planes
-                std::memcpy(at(0, 0, 0), at(0, 0, n[2]), e[0] * e[1] * s);
-                std::memcpy(at(0, 0, n[2] + 1), at(0, 0, 1), e[0] * e[1] * s);
-            }
-        };
-        std::vector<std::thread> th;
-        for (int i = 0; i < block->q; ++i) th.emplace_back(work, i);
-        for (auto& t : th) t.join();
+        if (n[0] < 1 || n[1] < 1 || n[2] < 1) throw std::invalid_argument("block extents must be >= 1");
+        if (block->precision_bits == 64)
+            refresh_host_envelope(static_cast<double*>(block->f_in), n, periodic, block->q);
+        else
+            refresh_host_envelope(static_cast<float*>(block->f_in), n, periodic, block->q);
     });
 }
 

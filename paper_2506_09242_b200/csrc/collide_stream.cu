@@ -27,9 +27,13 @@ namespace DLB_MODE {
 // lean dispatch sets (BGK / TRT / walls): fp32 6 blocks (<= 42 regs), D3Q19
 // fp64 3 (<= 85); sets with RR, LES or regularized links, and D3Q27 fp64, get 2
 // (fp32 3) so their larger live state does not spill.
+// The pure-BGK fp32 set gets 5 (<= 48 regs): at 6 it spilled 8 B per thread
+// and c5 ran 2 % slower (26.95 vs 26.41 ms per 1024^3 step,
+// profiles/r02_summary.md); the wall sets stay at 6 (c3: 3.34 vs 3.43 ms).
 template <typename T, int Q, unsigned KM>
 constexpr int min_blocks() {
     constexpr bool heavy = (KM & (KM_RR | KM_LES | KM_REGV | KM_REGP)) != 0;
+    if (sizeof(T) == 4 && Q == 19 && (KM & ~(KM_KE | KM_SKIP)) == KM_BGK) return 5;
     if (sizeof(T) == 4) return (heavy || Q == 27) ? 3 : 6;
     if (Q == 27) return 2;
     return heavy ? 2 : 3;
@@ -99,14 +103,19 @@ __device__ __forceinline__ void cell_update(const StepArgs<T>& a, int x, int y, 
     collide_store_cell<T, Q, KM>(a, x, y, z, s, f);
 }
 
-template <typename T, int Q, unsigned KM>
-__global__ void __launch_bounds__(256, (min_blocks<T, Q, KM>())) k_pull(const __grid_constant__ StepArgs<T> a) {
+// MINB != 0 overrides the occupancy target (register cap) of an instantiation
+// (tuning entries, DLB_PULL_MINB).
+template <typename T, int Q, unsigned KM, int MINB = 0>
+__global__ void __launch_bounds__(256, (MINB ? MINB : min_blocks<T, Q, KM>()))
+    k_pull(const __grid_constant__ StepArgs<T> a) {
     using L = Lat<Q>;
     const Geo& g = a.g;
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int y = blockIdx.y * blockDim.y + threadIdx.y;
     const int z = a.z_begin + int(blockIdx.z) * a.z_step;
-    if (a.err != nullptr && *reinterpret_cast<const volatile unsigned long long*>(a.err) != 0ull) return;
+    // (L1-cached load: the flag only changes between launches of this slab's
+    // later steps; the interior launch of the failing step may read either value)
+    if (a.err != nullptr && __ldca(a.err) != 0ull) return;
     bool active = x < g.nx && y < g.ny;
     int s = a.uniform_slot;
     if constexpr ((KM & KM_SKIP) != 0) {
@@ -883,6 +892,16 @@ __global__ void __launch_bounds__(NCW * 32 + 32, (NCW >= 16 ? 1 : 2))
             "k_pull<" #T ",D3Q" #Q "," #KM ">[" DLB_STR(DLB_MODE) "]"                      \
     }
 
+#define ENTRY_MB(T, Q, KM, MB)                                                           \
+    KernelEntry {                                                                        \
+        int(sizeof(T) * 8), Q, unsigned(KM), LAYOUT_TWO_POP,                              \
+            reinterpret_cast<const void*>(&k_pull<T, Q, unsigned(KM), MB>),               \
+            "k_pull<" #T ",D3Q" #Q "," #KM ",b" #MB ">[" DLB_STR(DLB_MODE) "]", 0, 0, 0, 1, 0, MB \
+    }
+#define MB_SET                                                                            \
+    , ENTRY_MB(float, 19, KM_BGK, 5), ENTRY_MB(float, 19, KM_BGK, 4), ENTRY_MB(float, 19, KM_TRT | KM_BB | KM_MBB, 5), \
+        ENTRY_MB(double, 19, KM_BGK, 2), ENTRY_MB(double, 27, KM_RR, 1)
+
 #define AA_ENTRY(T, Q, KM, ODD)                                                          \
     KernelEntry {                                                                        \
         int(sizeof(T) * 8), Q, unsigned(KM), ODD ? LAYOUT_AA_ODD : LAYOUT_AA,               \
@@ -1004,7 +1023,7 @@ static const KernelEntry kTable[] = {
     Q19_SET(float), Q19_SET(double), Q27_SET(float), Q27_SET(double), AA_SET(float), AA_SET(double),
     LIST_SET(float, 19), LIST_SET(double, 19), LIST_SET(float, 27), LIST_SET(double, 27),
     TMA_SET, SEG_SET(float), SEG_SET(double), TMAROW_SET(float), TMAROW_SET(double) KE_SET(float) KE_SET(double)
-        COOP_SET(float) COOP_SET(double) TMABLK_SET
+        COOP_SET(float) COOP_SET(double) TMABLK_SET MB_SET
 };
 
 const KernelEntry* kernel_table(int* n) {

@@ -84,6 +84,7 @@ struct KernelEntry {
     int tile_x = 0, tile_y = 0, stages = 0;  // TMA kernels: tile shape and ring depth
     int cpt = 1;                             // segment kernels: cells per thread
     int warps = 0;                           // row-staged TMA kernels: consumer warps per CTA
+    int minb = 0;                            // k_pull tuning entries: occupancy target override
 };
 
 // Kernel tables of the two arithmetic modes (one translation unit each).

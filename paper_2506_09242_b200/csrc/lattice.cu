@@ -4,6 +4,8 @@
 #include "lattice.hpp"
 #include "canon.cuh"
 
+#include <cstddef>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -249,7 +251,7 @@ const KernelEntry* find_kernel(int arith, int bits, int q, unsigned km, int layo
     const KernelEntry* best = nullptr;
     for (int k = 0; k < n; ++k) {
         const KernelEntry& e = t[k];
-        if (e.precision_bits != bits || e.q != q || e.layout != layout) continue;
+        if (e.precision_bits != bits || e.q != q || e.layout != layout || e.minb != 0) continue;
         if ((e.km & km) != km || (e.km & (KM_SKIP | KM_KE)) != (km & (KM_SKIP | KM_KE))) continue;
         if (!best || __builtin_popcount(e.km) < __builtin_popcount(best->km)) best = &e;
     }
@@ -348,6 +350,9 @@ Lattice::Lattice(const dlb_lattice_desc& desc, const DynamicsRegistry& reg) : d_
         cuda_check(cudaStreamCreateWithPriority(&halo_stream_, cudaStreamNonBlocking, hi), "cudaStreamCreate");
         cuda_check(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "cudaEventCreate");
         cuda_check(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming), "cudaEventCreate");
+        trace_halo_ = std::getenv("DLB_TRACE_HALO") != nullptr;
+        const char* oe = std::getenv("DLB_HALO_OVERLAP");
+        overlap_ = !(oe && oe[0] == '0');
         const char* te = std::getenv("DLB_HALO_TIMEOUT_MS");
         if (te && std::atof(te) > 0) halo_timeout_ns_ = static_cast<unsigned long long>(std::atof(te) * 1e6);
     }
@@ -429,6 +434,7 @@ Lattice::~Lattice() {
     if (h2d_stream_) cudaStreamDestroy(h2d_stream_);
     if (ev0_) cudaEventDestroy(ev0_);
     if (ev1_) cudaEventDestroy(ev1_);
+    for (cudaEvent_t e : trace_ev_) cudaEventDestroy(e);
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_join_) cudaEventDestroy(ev_join_);
     if (halo_stream_) cudaStreamDestroy(halo_stream_);
@@ -898,6 +904,15 @@ void Lattice::select_kernel() {
     }
     kernel_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_, LAYOUT_TWO_POP);
     if (!kernel_) throw std::invalid_argument("no kernel instantiation covers this dynamics set");
+    if (const char* mb = std::getenv("DLB_PULL_MINB")) {
+        // occupancy-target variant of the same instantiation (tuning knob)
+        int nt = 0;
+        const KernelEntry* t = d_.arith == DLB_ARITH_FAST ? fast::kernel_table(&nt) : exact::kernel_table(&nt);
+        for (int k = 0; k < nt; ++k)
+            if (t[k].layout == LAYOUT_TWO_POP && t[k].km == kernel_->km && t[k].minb == std::atoi(mb) &&
+                t[k].precision_bits == kernel_->precision_bits && t[k].q == kernel_->q)
+                kernel_ = &t[k];
+    }
     kernel_main_ = nullptr;
     if (!fixups_.empty())
         kernel_main_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_ & ~(KM_REGV | KM_REGP),
@@ -985,6 +1000,8 @@ void Lattice::check_dispatch() const {
     }
     if (split() && d_.periodic[2] && !(lower_.linked && upper_.linked))
         throw ExchangeError("periodic z-slab is not linked to both neighbours");
+    if (exchange_failed_)
+        throw ExchangeError("a halo exchange failed; bring the slabs to one step count and call exchange first");
 }
 
 void Lattice::reset_aa() {
@@ -1223,10 +1240,14 @@ void Lattice::fill_recipes(StepArgs<T>& a) const {
 // on the device, so every transfer is one contiguous range per direction):
 //   copy engine 1: host planes needed by chunk k -> device input mirror
 //   SMs:           collide-and-stream of chunk k (input mirror -> output mirror)
-//   copy engine 2: finished planes of chunk k - 1 -> back into the host f_in
-// The two PCIe directions run concurrently with the compute.
+//   copy engine 2: finished planes of chunk k -> the caller's f_out (or back
+//                  into f_in: those planes are no longer read by later chunks)
+// The two PCIe directions run concurrently with the compute. The H2D copies
+// run at most `ahead` chunks in front of the copy-back (each waits for the
+// D2H of chunk k - ahead): left alone the H2D direction wins the link
+// arbitration and the copy-back finishes alone at the end.
 template <typename T>
-void Lattice::launch_host_block(void* f_in, const int64_t ext[3]) {
+void Lattice::launch_host_block(void* f_in, const int64_t ext[3], void* f_out) {
     const long long vol = ext[0] * ext[1] * ext[2];
     Geo hg{};
     hg.nx = geo_.nx;
@@ -1255,30 +1276,42 @@ void Lattice::launch_host_block(void* f_in, const int64_t ext[3]) {
         a.fin[i] = din + i * vol + org;
         a.fout[i] = dout + i * vol + org;
     }
-    const int bx = hg.nx >= 128 ? 128 : (hg.nx > 32 ? 64 : 32);
-    const int by = 256 / bx;
-    const dim3 block(bx, by, 1);
-    const unsigned gx = unsigned((hg.nx + bx - 1) / bx), gy = unsigned((hg.ny + by - 1) / by);
+    a.z_step = 1;
+    blk_args_.resize(sizeof(a));
+    std::memcpy(blk_args_.data(), &a, sizeof(a));
+    blk_.bx = hg.nx >= 128 ? 128 : (hg.nx > 32 ? 64 : 32);
+    blk_.by = 256 / blk_.bx;
+    blk_.gx = unsigned((hg.nx + blk_.bx - 1) / blk_.bx);
+    blk_.gy = unsigned((hg.ny + blk_.by - 1) / blk_.by);
     // 32 z-chunks (2-D copies keep the per-chunk cost low; shorter fill / drain), >= 1 plane each
     static const int kChunks = [] {
         const char* e = std::getenv("DLB_BLOCK_CHUNKS");
         return e ? std::max(1, std::atoi(e)) : 32;
     }();
+    static const int kAhead = [] {
+        const char* e = std::getenv("DLB_BLOCK_AHEAD");
+        return e ? std::max(0, std::atoi(e)) : 2;
+    }();
     const int zc = std::max(1, (hg.nz + kChunks - 1) / kChunks);
     const int nchunks = (hg.nz + zc - 1) / zc;
-    while (int(blk_ev_.size()) < 2 * nchunks) {
+    while (int(blk_ev_.size()) < 3 * nchunks) {
         cudaEvent_t e;
         cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
         blk_ev_.push_back(e);
     }
     blk_.f_in = f_in;
+    blk_.f_out = f_out ? f_out : f_in;
+    blk_.din = din;
+    blk_.dout = dout;
     blk_.vol = vol;
     blk_.plane = hg.plane;
     blk_.nz = hg.nz;
     blk_.zc = zc;
     blk_.nchunks = nchunks;
     blk_.elem = int(sizeof(T));
-    blk_.dout = dout;
+    blk_.ahead = kAhead == 0 ? nchunks : kAhead;
+    blk_.issued = 0;
+    blk_.loaded = 0;
     blk_.pending = true;
     static const bool trace = std::getenv("DLB_TRACE_BLOCK") != nullptr;
     if (trace) {  // timeline events (DLB_TRACE_BLOCK): begin, end of H2D, end of compute
@@ -1286,36 +1319,50 @@ void Lattice::launch_host_block(void* f_in, const int64_t ext[3]) {
             if (!e) cuda_check(cudaEventCreate(&e), "event");
         cuda_check(cudaEventRecord(blk_tr_[0], h2d_stream_), "event");
     }
-    int loaded = 0;  // host planes [0, loaded) are on the device
-    for (int c = 0; c < nchunks; ++c) {
-        const int z0 = c * zc, z1 = std::min(hg.nz, z0 + zc);
-        // chunk [z0, z1) reads host planes [z0, z1 + 2)
-        block_copy(h2d_stream_, din, true, loaded, z1 + 2);
-        loaded = z1 + 2;
-        cuda_check(cudaEventRecord(blk_ev_[2 * c], h2d_stream_), "event");
-        cuda_check(cudaStreamWaitEvent(stream_, blk_ev_[2 * c], 0), "wait");
-        a.z_begin = z0;
-        a.z_step = 1;
-        void* args[] = {&a};
-        cuda_check(cudaLaunchKernel(kernel_->fn, dim3(gx, gy, z1 - z0), block, args, 0, stream_), "launch");
-        cuda_check(cudaEventRecord(blk_ev_[2 * c + 1], stream_), "event");
-    }
-    if (trace) {
-        cuda_check(cudaEventRecord(blk_tr_[1], h2d_stream_), "event");
-        cuda_check(cudaEventRecord(blk_tr_[2], stream_), "event");
-    }
+    // speculative part (device-side writes only, runs while the caller's tag
+    // scan decides): the first max(ahead, DLB_BLOCK_SPEC = 4) chunks
+    static const int kSpec = [] {
+        const char* e = std::getenv("DLB_BLOCK_SPEC");
+        return e ? std::max(1, std::atoi(e)) : 4;
+    }();
+    blk_.copied = 0;
+    while (blk_.issued < std::min(std::max(blk_.ahead, kSpec), nchunks)) issue_block_chunk(blk_.issued++);
 }
 
-// One direction-strided copy of host planes [p0, p1) between the caller's block
+// H2D of the host planes chunk c reads (after the D2H of chunk c - ahead) and
+// its compute. Events per chunk: [3c] H2D done, [3c+1] compute done, [3c+2] D2H done.
+void Lattice::issue_block_chunk(int c) {
+    const int z0 = c * blk_.zc, z1 = std::min(blk_.nz, z0 + blk_.zc);
+    if (c >= blk_.ahead && c - blk_.ahead < blk_.copied)
+        cuda_check(cudaStreamWaitEvent(h2d_stream_, blk_ev_[3 * (c - blk_.ahead) + 2], 0), "wait");
+    // chunk [z0, z1) reads host planes [z0, z1 + 2)
+    block_copy(h2d_stream_, blk_.f_in, blk_.din, true, blk_.loaded, z1 + 2);
+    blk_.loaded = z1 + 2;
+    cuda_check(cudaEventRecord(blk_ev_[3 * c], h2d_stream_), "event");
+    if (c == blk_.nchunks - 1 && blk_tr_[1]) cuda_check(cudaEventRecord(blk_tr_[1], h2d_stream_), "event");
+    cuda_check(cudaStreamWaitEvent(stream_, blk_ev_[3 * c], 0), "wait");
+    // the kernel reads z_begin from its argument block (StepArgs<T> is a POD image)
+    std::vector<uint8_t> args(blk_args_);
+    const std::size_t zoff = d_.precision_bits == 64 ? offsetof(StepArgs<double>, z_begin)
+                                                     : offsetof(StepArgs<float>, z_begin);
+    std::memcpy(args.data() + zoff, &z0, sizeof(int));
+    void* kargs[] = {args.data()};
+    cuda_check(cudaLaunchKernel(kernel_->fn, dim3(blk_.gx, blk_.gy, unsigned(z1 - z0)), dim3(blk_.bx, blk_.by, 1),
+                                kargs, 0, stream_), "launch");
+    cuda_check(cudaEventRecord(blk_ev_[3 * c + 1], stream_), "event");
+    if (c == blk_.nchunks - 1 && blk_tr_[2]) cuda_check(cudaEventRecord(blk_tr_[2], stream_), "event");
+}
+
+// One direction-strided copy of host planes [p0, p1) between a caller block
 // and a device mirror (the same envelope-inclusive layout).
-void Lattice::block_copy(cudaStream_t st, void* dev, bool up, int p0, int p1) {
+void Lattice::block_copy(cudaStream_t st, void* host, void* dev, bool up, int p0, int p1) {
     if (p1 <= p0) return;
     const std::size_t plane_bytes = std::size_t(blk_.plane) * blk_.elem;
     {
         // all q direction arrays in one 2-D copy (rows = directions, pitch = one array)
         const std::size_t off = std::size_t(p0) * blk_.plane * blk_.elem;
         const std::size_t pitch = std::size_t(blk_.vol) * blk_.elem;
-        char* h = static_cast<char*>(blk_.f_in) + off;
+        char* h = static_cast<char*>(host) + off;
         char* d = static_cast<char*>(dev) + off;
         const cudaError_t e = cudaMemcpy2DAsync(up ? d : h, pitch, up ? h : d, pitch, std::size_t(p1 - p0) * plane_bytes,
                                                 d_.q, up ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, st);
@@ -1324,7 +1371,7 @@ void Lattice::block_copy(cudaStream_t st, void* dev, bool up, int p0, int p1) {
     }
     for (int i = 0; i < d_.q; ++i) {
         const std::size_t off = (std::size_t(i) * blk_.vol + std::size_t(p0) * blk_.plane) * blk_.elem;
-        char* h = static_cast<char*>(blk_.f_in) + off;
+        char* h = static_cast<char*>(host) + off;
         char* d = static_cast<char*>(dev) + off;
         cuda_check(cudaMemcpyAsync(up ? d : h, up ? h : d, std::size_t(p1 - p0) * plane_bytes,
                                    up ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, st),
@@ -1332,26 +1379,29 @@ void Lattice::block_copy(cudaStream_t st, void* dev, bool up, int p0, int p1) {
     }
 }
 
-void Lattice::begin_host_block(void* f_in, const int64_t ext[3]) {
+void Lattice::begin_host_block(void* f_in, const int64_t ext[3], void* f_out) {
     DeviceGuard dg(device_);
     if (aa()) throw std::invalid_argument("host-block stepping uses the two-population layout");
     if (blk_.pending) abort_host_block();
-    if (d_.precision_bits == 64) launch_host_block<double>(f_in, ext);
-    else launch_host_block<float>(f_in, ext);
+    if (d_.precision_bits == 64) launch_host_block<double>(f_in, ext, f_out);
+    else launch_host_block<float>(f_in, ext, f_out);
 }
 
-// Copy-back: finished planes go back as soon as their chunk is computed (the
-// old interior planes z < z1 are no longer read once the host copy of them is
-// on the device), on a second copy engine, overlapping the remaining H2D.
+// Copy-back: finished planes go back as soon as their chunk is computed, on a
+// second copy engine, interleaved with the remaining H2D chunks.
 void Lattice::finish_host_block() {
+    DeviceGuard dg(device_);
     if (!blk_.pending) throw std::logic_error("finish_host_block without begin_host_block");
     int written = 1;  // host planes [1, written) copied back (plane 0 is envelope)
     for (int c = 0; c < blk_.nchunks; ++c) {
         const int z1 = std::min(blk_.nz, (c + 1) * blk_.zc);
-        cuda_check(cudaStreamWaitEvent(copy_stream_, blk_ev_[2 * c + 1], 0), "wait");
+        cuda_check(cudaStreamWaitEvent(copy_stream_, blk_ev_[3 * c + 1], 0), "wait");
         if (c == 0 && blk_tr_[3]) cuda_check(cudaEventRecord(blk_tr_[3], copy_stream_), "event");
-        block_copy(copy_stream_, blk_.dout, false, written, z1 + 1);
+        block_copy(copy_stream_, blk_.f_out, blk_.dout, false, written, z1 + 1);
         written = z1 + 1;
+        cuda_check(cudaEventRecord(blk_ev_[3 * c + 2], copy_stream_), "event");
+        blk_.copied = c + 1;
+        while (blk_.issued < blk_.nchunks && blk_.issued <= c + blk_.ahead) issue_block_chunk(blk_.issued++);
     }
     if (blk_tr_[4]) cuda_check(cudaEventRecord(blk_tr_[4], copy_stream_), "event");
     blk_.pending = false;
@@ -1368,13 +1418,14 @@ void Lattice::finish_host_block() {
 
 // Drop a begun step: nothing was written to the caller's block.
 void Lattice::abort_host_block() {
+    DeviceGuard dg(device_);
     blk_.pending = false;
     cuda_check(cudaStreamSynchronize(h2d_stream_), "block abort");
     cuda_check(cudaStreamSynchronize(stream_), "block abort");
 }
 
-void Lattice::step_host_block(void* f_in, const int64_t ext[3]) {
-    begin_host_block(f_in, ext);
+void Lattice::step_host_block(void* f_in, const int64_t ext[3], void* f_out) {
+    begin_host_block(f_in, ext, f_out);
     finish_host_block();
 }
 
@@ -1520,10 +1571,27 @@ void Lattice::launch_step(int parity) {
     // the boundary sweep and the NVLink transfer all overlap the interior.
     a.err = d_flags_ + 3;
     ++halo_steps_;
-    cuda_check(cudaEventRecord(ev_fork_, stream_), "fork");
-    cuda_check(cudaStreamWaitEvent(halo_stream_, ev_fork_, 0), "fork");
-    k_halo_wait<<<1, 1, 0, halo_stream_>>>(d_flags_, lower_.linked, upper_.linked, halo_timeout_ns_);
+    // DLB_TRACE_HALO: timing events around the two branches (graphs disabled)
+    cudaEvent_t* tr = nullptr;
+    if (trace_halo_ && trace_ev_.size() + 5 <= 5 * 256) {
+        for (int k = 0; k < 5; ++k) {
+            cudaEvent_t e;
+            cuda_check(cudaEventCreate(&e), "event");
+            trace_ev_.push_back(e);
+        }
+        tr = trace_ev_.data() + trace_ev_.size() - 5;
+    }
+    // DLB_HALO_OVERLAP=0: the serialised variant (wait, boundary, interior on
+    // one stream), kept for comparison
+    const cudaStream_t hs = overlap_ ? halo_stream_ : stream_;
+    if (overlap_) {
+        cuda_check(cudaEventRecord(ev_fork_, stream_), "fork");
+        cuda_check(cudaStreamWaitEvent(halo_stream_, ev_fork_, 0), "fork");
+    }
+    if (tr) cuda_check(cudaEventRecord(tr[0], hs), "trace");
+    k_halo_wait<<<1, 1, 0, hs>>>(d_flags_, lower_.linked, upper_.linked, halo_timeout_ns_);
     cuda_check(cudaGetLastError(), "k_halo_wait");
+    if (tr) cuda_check(cudaEventRecord(tr[1], hs), "trace");
     StepArgs<T> b = a;
     b.z_begin = 0;
     b.z_step = geo_.nz > 1 ? geo_.nz - 1 : 1;
@@ -1542,10 +1610,12 @@ void Lattice::launch_step(int parity) {
     b.my_step = d_flags_ + 2;
     {
         void* args[] = {&b};
-        cuda_check(cudaLaunchKernel(fn, dim3(gx, gy, geo_.nz > 1 ? 2 : 1), block, args, 0, halo_stream_),
+        cuda_check(cudaLaunchKernel(fn, dim3(gx, gy, geo_.nz > 1 ? 2 : 1), block, args, 0, hs),
                    "launch boundary");
     }
-    cuda_check(cudaEventRecord(ev_join_, halo_stream_), "join");
+    if (tr) cuda_check(cudaEventRecord(tr[2], hs), "trace");
+    if (overlap_) cuda_check(cudaEventRecord(ev_join_, halo_stream_), "join");
+    if (tr) cuda_check(cudaEventRecord(tr[3], stream_), "trace");
     if (geo_.nz > 2) {
         a.z_begin = 1;
         a.z_step = 1;
@@ -1553,7 +1623,8 @@ void Lattice::launch_step(int parity) {
         cuda_check(cudaLaunchKernel(fn, dim3(gx, gy, geo_.nz - 2), block, args, 0, stream_),
                    "launch interior");
     }
-    cuda_check(cudaStreamWaitEvent(stream_, ev_join_, 0), "join");
+    if (tr) cuda_check(cudaEventRecord(tr[4], stream_), "trace");
+    if (overlap_) cuda_check(cudaStreamWaitEvent(stream_, ev_join_, 0), "join");
 }
 
 void Lattice::enqueue_step() {
@@ -1618,7 +1689,7 @@ void Lattice::step(int64_t nsteps) {
         else launch_coop<float>(nsteps);
         k = nsteps;
     }
-    if (nsteps - k >= 4) {
+    if (nsteps - k >= 4 && !trace_halo_) {
         const bool aligned = aa() ? aa_odd_layout_ : cur_ == 0;
         if (!aligned) {
             enqueue_step();
@@ -1657,6 +1728,7 @@ void Lattice::exchange() {
     // (re)priming the ghosts clears a previous exchange error: the caller has
     // brought the slabs back to one step count (MultiBlockRun::exchange)
     cuda_check(cudaMemsetAsync(d_flags_ + 3, 0, sizeof(unsigned long long), stream_), "clear error");
+    exchange_failed_ = false;
     const int s = d_.precision_bits / 8;
     const std::size_t plane_bytes = std::size_t(geo_.plane) * s;
     auto plane_ptr = [&](void* origin_dir0, long long dstride, int i, int z) {
@@ -1753,9 +1825,11 @@ void Lattice::gather_macroscopic(double* rho, double* ux, double* uy, double* uz
 void Lattice::check_error_flag() {
     DeviceGuard dg(device_);
     if (!(lower_.linked || upper_.linked)) return;
+    if (exchange_failed_) return;  // reported once; the kept state stays readable
     unsigned long long fl[4] = {0, 0, 0, 0};
     cuda_check(cudaMemcpy(fl, d_flags_, sizeof(fl), cudaMemcpyDeviceToHost), "read flags");
     if (!fl[3]) return;
+    exchange_failed_ = true;
     // flags[3] = 1-based index of the step whose halo wait timed out; that step
     // and every later one wrote nothing, so the state after the last completed
     // step (flags[2] of them) is intact in the buffer of its parity.
@@ -1769,6 +1843,34 @@ void Lattice::check_error_flag() {
     }
     throw ExchangeError("halo exchange timed out waiting for a neighbour at step " + std::to_string(fl[3]) +
                         " (state kept after step " + std::to_string(done) + ")");
+}
+
+std::vector<double> Lattice::halo_trace(bool consume) {
+    DeviceGuard dg(device_);
+    quiesce();
+    std::vector<double> out;
+    if (trace_ev_.empty()) return out;
+    if (!consume) {
+        out.resize(trace_ev_.size());
+        return out;
+    }
+    for (std::size_t k = 0; k < trace_ev_.size(); ++k) {
+        float ms = 0.f;
+        cuda_check(cudaEventElapsedTime(&ms, trace_ev_[0], trace_ev_[k]), "elapsed");
+        out.push_back(double(ms));
+    }
+    for (cudaEvent_t e : trace_ev_) cudaEventDestroy(e);
+    trace_ev_.clear();
+    return out;
+}
+
+void Lattice::links(int* lower, int* upper, int64_t* halo_bytes) const {
+    auto code = [](const Peer& p) { return p.linked ? (p.other_gpu ? 2 : 1) : 0; };
+    *lower = code(lower_);
+    *upper = code(upper_);
+    const int cross = d_.q == 19 ? 5 : 9;  // links with c_z = +1 (or -1)
+    *halo_bytes = int64_t(int(lower_.linked) + int(upper_.linked)) * geo_.nx * geo_.ny * cross *
+                  (d_.precision_bits / 8);
 }
 
 void Lattice::set_halo_timeout(double seconds) {
@@ -1821,6 +1923,10 @@ void Lattice::link_lower(Lattice& lower) {
         cudaGetLastError();
     }
     lower_.linked = true;
+    lower_.other_gpu = lower.upper_.other_gpu = lower.device_ != device_;
+    // the z neighbours now provide the wrap (a single slab may be linked to
+    // itself: the one-slab-per-GPU step on one GPU)
+    geo_.per_z = lower.geo_.per_z = 0;
     lower_.buf[0] = lower.origin(0);
     lower_.buf[1] = lower.origin(1);
     lower_.dstride = lower.geo_.dstride;
@@ -1838,6 +1944,8 @@ namespace {
 struct IpcBlob {
     uint32_t magic;
     int32_t q, bits, nx, ny, nz;
+    int32_t device;
+    char pci_bus[32];  // the exporting slab's GPU (reported by links(): peer on another GPU or not)
     long long dstride, base_off_bytes;
     cudaIpcMemHandle_t buf[2];
     cudaIpcMemHandle_t flags;
@@ -1856,6 +1964,8 @@ std::vector<uint8_t> Lattice::export_ipc() const {
     b.dstride = geo_.dstride;
     b.base_off_bytes = base_off_ * (d_.precision_bits / 8);
     DeviceGuard dg(device_);
+    b.device = device_;
+    cuda_check(cudaDeviceGetPCIBusId(b.pci_bus, int(sizeof(b.pci_bus)), device_), "pci bus id");
     for (int k = 0; k < 2; ++k) cuda_check(cudaIpcGetMemHandle(&b.buf[k], buf_[k]), "ipc handle");
     cuda_check(cudaIpcGetMemHandle(&b.flags, d_flags_), "ipc handle");
     std::vector<uint8_t> out(sizeof(b));
@@ -1884,6 +1994,9 @@ void Lattice::link_ipc(int side, const void* blob, std::size_t len) {
     p.buf[1] = static_cast<char*>(bases[1]) + b.base_off_bytes;
     p.dstride = b.dstride;
     p.nz = b.nz;
+    char mine[32] = {0};
+    cuda_check(cudaDeviceGetPCIBusId(mine, int(sizeof(mine)), device_), "pci bus id");
+    p.other_gpu = std::strncmp(mine, b.pci_bus, sizeof(mine)) != 0;
     // we are the peer's upper neighbour if it is our lower one, and vice versa
     p.flag = static_cast<unsigned long long*>(bases[2]) + (side == 0 ? 1 : 0);
 }

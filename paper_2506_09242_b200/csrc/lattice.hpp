@@ -47,6 +47,7 @@ class DeviceGuard {
 // Halo neighbour of a slab (the lower one at z = -1, the upper at z = nz).
 struct Peer {
     bool linked = false;
+    bool other_gpu = false;              // the neighbour's memory is on another GPU (NVLink / P2P)
     void* buf[2] = {nullptr, nullptr};   // peer populations, interior origin of direction 0
     long long dstride = 0;
     int nz = 0;
@@ -77,12 +78,13 @@ class Lattice {
     // included, refreshed by the caller), pipelined over z-chunks: host->device
     // copies of the next chunk, the step of this chunk and device->host copies
     // of the previous one run concurrently (both PCIe directions busy).
-    void step_host_block(void* f_in, const int64_t ext[3]);
+    // f_out (may be null): the new state goes into f_out instead of back into f_in
+    void step_host_block(void* f_in, const int64_t ext[3], void* f_out = nullptr);
     // The same in two halves: begin enqueues every H2D chunk and its compute
     // (device-side writes only), finish enqueues the copy-back into the
     // caller's block; abort drops a begun step. Lets the caller's eager
     // dispatch scan overlap the transfers while still failing before any write.
-    void begin_host_block(void* f_in, const int64_t ext[3]);
+    void begin_host_block(void* f_in, const int64_t ext[3], void* f_out = nullptr);
     void finish_host_block();
     void abort_host_block();
     void step(int64_t nsteps);
@@ -96,6 +98,13 @@ class Lattice {
     // Halo wait limit per step (a neighbour that does not finish its boundary
     // planes within it makes the step fail with DLB_ERROR_EXCHANGE).
     void set_halo_timeout(double seconds);
+    // 0 = not linked, 1 = linked to a slab on the same GPU, 2 = on another GPU;
+    // halo_bytes = bytes this slab pushes to its neighbours per step
+    void links(int* lower, int* upper, int64_t* halo_bytes) const;
+    // DLB_TRACE_HALO timeline of the linked steps since the last call (ms from
+    // the first event; 5 per step: halo wait begin / end, boundary end on the
+    // halo stream, interior begin / end on the main stream)
+    std::vector<double> halo_trace(bool consume = true);
     void link_lower(Lattice& lower);  // same process
     void exchange();                  // prime the neighbours' ghost planes (clears an exchange error)
     void quiesce();                   // wait for this slab's streams (no error check)
@@ -154,6 +163,10 @@ class Lattice {
     cudaStream_t halo_stream_ = nullptr;
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
     unsigned long long halo_timeout_ns_ = 20ull * 1000 * 1000 * 1000;  // DLB_HALO_TIMEOUT_MS / set_halo_timeout
+    bool trace_halo_ = false;             // DLB_TRACE_HALO
+    bool exchange_failed_ = false;        // a timed-out halo wait was reported (cleared by exchange)
+    bool overlap_ = true;                 // DLB_HALO_OVERLAP (0: serialised halo + interior)
+    std::vector<cudaEvent_t> trace_ev_;   // 5 per linked step: wait0, wait1, boundary1, interior0, interior1
     Geo geo_{};
     int align_ = 32;            // elements per 128 B
     int skip_group_ = 8;        // masked porous sweep: cells per skip group (power of two <= 32)
@@ -251,16 +264,25 @@ class Lattice {
     cudaEvent_t blk_tr_[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // DLB_TRACE_BLOCK timeline
     struct BlockPlan {
         void* f_in = nullptr;
+        void* f_out = nullptr;  // where the new state goes (f_in when in place)
+        void* din = nullptr;
         void* dout = nullptr;
         long long vol = 0;
         int plane = 0, nz = 0, zc = 1, nchunks = 0, elem = 4;
+        int issued = 0;         // chunks whose H2D + compute are enqueued
+        int ahead = 2;          // H2D chunks allowed ahead of the D2H copy-back (DLB_BLOCK_AHEAD, 0 = all)
+        unsigned gx = 1, gy = 1, bx = 32, by = 8;
+        int loaded = 0;         // host planes [0, loaded) on the device
+        int copied = 0;         // chunks whose copy-back is enqueued
         bool pending = false;
     } blk_;
-    void block_copy(cudaStream_t st, void* dev, bool up, int p0, int p1);
+    std::vector<uint8_t> blk_args_;  // the StepArgs<T> of the pending block step
+    void issue_block_chunk(int c);
+    void block_copy(cudaStream_t st, void* host, void* dev, bool up, int p0, int p1);
     template <typename T>
     void fill_recipes(StepArgs<T>& a) const;
     template <typename T>
-    void launch_host_block(void* f_in, const int64_t ext[3]);
+    void launch_host_block(void* f_in, const int64_t ext[3], void* f_out);
     // diagnostics state (diag.cu)
     double* d_uprev_ = nullptr;  // velocity snapshot [ux | uy | uz] x cells
     void* diag_buf_ = nullptr;

@@ -37,7 +37,7 @@ __all__ = [
     "make_collision_chain", "make_bounce_back", "make_no_dynamics", "make_moving_bounce_back",
     "make_regularized_velocity", "make_regularized_pressure", "chain_string", "serialize_params",
     "DynamicsRegistry", "DispatchSet", "DispatchError", "ExchangeError", "ConfigError", "DlbError",
-    "DeviceRun", "partition", "collide_and_stream", "refresh_envelope_periodic", "read_field_dump", "D3Q19", "D3Q27",
+    "DeviceRun", "partition", "collide_and_stream", "block_cache_release", "block_cache_info", "refresh_envelope_periodic", "read_field_dump", "D3Q19", "D3Q27",
 ]
 
 
@@ -469,6 +469,14 @@ class DeviceRun:
             if k is None or j == k:
                 check(_capi.lib().dlb_lattice_set_halo_timeout(s.handle, float(seconds)))
 
+    def links(self, k: int = 0) -> dict:
+        """Link state of slab k: lower / upper = 'none' | 'same_gpu' | 'peer_gpu',
+        and the halo bytes it pushes per step."""
+        lo, up, hb = C.c_int32(), C.c_int32(), C.c_int64()
+        check(_capi.lib().dlb_lattice_links(self.slabs[k].handle, C.byref(lo), C.byref(up), C.byref(hb)))
+        name = {0: "none", 1: "same_gpu", 2: "peer_gpu"}
+        return {"lower": name[lo.value], "upper": name[up.value], "halo_bytes_per_step": hb.value}
+
     def step_slab(self, k: int, nsteps: int):
         """Advance slab k alone (its neighbours must keep up; fault tests)."""
         check(_capi.lib().dlb_lattice_step(self.slabs[k].handle, nsteps))
@@ -720,8 +728,10 @@ def collide_and_stream(registry: DynamicsRegistry, f_in: np.ndarray, tag: np.nda
                        q: int = 19):
     """Drop-in for collide_and_stream<T>(AcceleratedBlock<T>&, ...) on host arrays
     (accelerated_lattice.hpp:124-127). f_in: (q, ez, ey, ex) envelope-inclusive,
-    tag / param_index: (ez, ey, ex). On return f_in holds the new state and f_out
-    (if given) the previous one."""
+    tag / param_index: (ez, ey, ex). Without f_out the new state overwrites
+    f_in's interior and f_in is returned. With f_out the new state is written
+    into f_out (f_in keeps the previous state) and (f_out, f_in) is returned:
+    the reference's swap -- the first is the block's new f_in."""
     assert f_in.flags.c_contiguous and f_in.ndim == 4
     ez, ey, ex = f_in.shape[1:]
     v = _capi.BlockView()
@@ -736,6 +746,22 @@ def collide_and_stream(registry: DynamicsRegistry, f_in: np.ndarray, tag: np.nda
     tags = np.asarray(sorted(dispatch.tags), np.int32)
     check(_capi.lib().dlb_collide_and_stream(registry.handle, C.byref(v),
                                              tags.ctypes.data if tags.size else None, tags.size, 1))
+    if f_out is None:
+        return f_in
+    assert v.f_in == f_out.ctypes.data  # the view came back swapped
+    return f_out, f_in
+
+
+def block_cache_release():
+    """Free the device contexts dlb_collide_and_stream keeps per block shape."""
+    _capi.lib().dlb_block_cache_release()
+
+
+def block_cache_info():
+    """(entries, device bytes) held by the host-block device cache."""
+    n, b = C.c_size_t(), C.c_int64()
+    check(_capi.lib().dlb_block_cache_info(C.byref(n), C.byref(b)))
+    return n.value, b.value
 
 
 def read_field_dump(path: str):

@@ -44,3 +44,31 @@ def test_bench_two_ranks_protocol(tmp_path):
         d = json.loads(lines[0])
         assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == scaling
         assert d["config"]["parallelism"] == "z-slab x2" and d["gpu_launches"] > 0
+
+
+def test_bench_spawns_ranks_without_launcher():
+    """`bench.py --gpus 2` without torchrun (the driver's plain form) starts two
+    ranks itself and reports n_gpus 2; c5 is strong scaling (fixed L), c3 weak
+    (L grows with the cube root of N: perfmodel.cpp:76-85). Every rank reports
+    its halo links and bytes."""
+    import json
+    env = dict(os.environ, DLB_SAME_DEVICE="1")
+    env.pop("WORLD_SIZE", None)
+    for cfg, L, scaling, want_L in (("c5", "128", "strong", 128), ("c3", "96", "weak", 121)):
+        cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--config", cfg, "--L", L,
+               "--steps", "4", "--warmup", "3", "--no-cpu", "--e2e-L", "64"]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+        assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+        lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+        assert len(lines) == 1, r.stdout
+        d = json.loads(lines[0])
+        assert d["n_gpus"] == 2 and d["scaling"] == scaling and d["config"]["L"] == want_L
+        ranks = d["config"]["halo"]["per_rank"]
+        assert [x["rank"] for x in ranks] == [0, 1]
+        for x in ranks:
+            assert x["halo_bytes_per_step"] > 0
+            if cfg == "c5":  # periodic ring: both neighbours linked (same GPU in this test)
+                assert x["lower"] == x["upper"] == "same_gpu"
+        if cfg == "c5":
+            assert d["e2e"]["value"] > 0 and d["e2e"]["finite"]
+
