@@ -97,9 +97,14 @@ typedef struct dlb_lattice_desc {
 /* Masked porous variant: NoDynamics cells are neither loaded nor stored, at the
  * granularity of x-aligned groups of one 32-B segment per direction array (a
  * group moves nothing only when all its cells are NoDynamics; the NoDynamics
- * cells of a mixed group run their dense update). The skipped values are never
- * consumed by a fluid cell, so every Collide-kind cell stays bit-identical to
- * the reference. Works on single slabs and z-slabs. */
+ * cells of a mixed group run their dense update). Precondition (checked by
+ * dlb_lattice_set_slots, DLB_ERROR_CONFIG otherwise): no collision cell has a
+ * NoDynamics neighbour -- a solid cell next to fluid must be BounceBack, as the
+ * reference's porous setup assigns (cases.cpp:239-249; z neighbours in other
+ * slabs are not checked). Then the skipped values are never consumed by a
+ * collision cell (bounce-back cells only return a cell's own populations to
+ * it), so every collision cell stays bit-identical to the reference
+ * (SURVEY.md A.4). Works on single slabs and z-slabs. */
 #define DLB_FLAG_SKIP_NODYNAMICS 1
 /* Use a TMA-staged dense kernel for single-slab two-population lattices:
  * k_tmablk on uniform lattices (one 2-D tensor box of 256 x R rows per

@@ -33,7 +33,7 @@ namespace DLB_MODE {
 template <typename T, int Q, unsigned KM>
 constexpr int min_blocks() {
     constexpr bool heavy = (KM & (KM_RR | KM_LES | KM_REGV | KM_REGP)) != 0;
-    if (sizeof(T) == 4 && Q == 19 && (KM & ~(KM_KE | KM_SKIP)) == KM_BGK) return 5;
+    if (sizeof(T) == 4 && Q == 19 && (KM & ~(KM_KE | KM_SKIP | KM_XREC)) == KM_BGK) return 5;
     if (sizeof(T) == 4) return (heavy || Q == 27) ? 3 : 6;
     if (Q == 27) return 2;
     return heavy ? 2 : 3;
@@ -69,7 +69,7 @@ template <typename T, int Q, unsigned KM>
 __device__ __forceinline__ void collide_store_cell(const StepArgs<T>& a, int x, int y, int z, int s, T (&f)[Q]) {
     using L = Lat<Q>;
     const Geo& g = a.g;
-    Cell<T, Q>::template apply<KM>(f, a.rec[s]);
+    Cell<T, Q>::template apply<KM>(f, recipe_of<KM>(a, s));
 
     const int center = z * g.plane + y * g.pitch + x;
     sfor<Q>([&](auto I) {
@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(256, (MINB ? MINB : min_blocks<T, Q, KM>()))
         bool need = false;
         if (active && a.slot != nullptr) {
             s = a.slot[(static_cast<long long>(z) * g.ny + y) * g.nx + x];
-            need = a.rec[s].kind != KIND_NODYN;
+            need = recipe_of<KM>(a, s).kind != KIND_NODYN;
         }
         const unsigned ball = __ballot_sync(0xffffffffu, need);
         const int G = a.skip_group;
@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(256, (MINB ? MINB : min_blocks<T, Q, KM>()))
         if constexpr ((KM & KM_SKIP) == 0) {
             if (a.slot != nullptr) s = a.slot[(static_cast<long long>(z) * g.ny + y) * g.nx + x];
         }
-        Cell<T, Q>::template apply<KM & ~(KM_SKIP | KM_KE)>(f, a.rec[s]);
+        Cell<T, Q>::template apply<KM & ~(KM_SKIP | KM_KE)>(f, recipe_of<KM>(a, s));
 
         const int center = z * g.plane + y * g.pitch + x;
         sfor<Q>([&](auto I) {
@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(256, (MINB ? MINB : min_blocks<T, Q, KM>()))
             // semantics (multiblock.cpp:458-478: rho / u in double from the
             // stored T values; wall velocity on moving walls; 0 elsewhere) and
             // diag::kinetic_energy's expression (diagnostics.cpp:28).
-            const DevRecipe<T>& r = a.rec[s];
+            const DevRecipe<T>& r = recipe_of<KM>(a, s);
             double u[3] = {0.0, 0.0, 0.0};
             if (r.kind == KIND_COLLIDE) {
                 double fd[Q];
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(256, (min_blocks<T, Q, KM>()))
             });
             int s = a.uniform_slot;
             if (a.slot != nullptr) s = a.slot[c];
-            Cell<T, Q>::template apply<KM>(f, a.rec[s]);
+            Cell<T, Q>::template apply<KM>(f, recipe_of<KM>(a, s));
             const int center = z * g.plane + y * g.pitch + x;
             sfor<Q>([&](auto I) {
                 constexpr int i = decltype(I)::value;
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(256, (min_blocks<T, Q, KM>())) k_aa(const __gr
     }
     int s = a.uniform_slot;
     if (a.slot != nullptr) s = a.slot[(static_cast<long long>(z) * g.ny + y) * g.nx + x];
-    Cell<T, Q>::template apply<KM>(f, a.rec[s]);
+    Cell<T, Q>::template apply<KM>(f, recipe_of<KM>(a, s));
     if constexpr (!ODD) {
         sfor<Q>([&](auto I) {
             constexpr int i = decltype(I)::value;
@@ -456,7 +456,7 @@ __global__ void __launch_bounds__(256, (min_blocks<T, Q, KM>()))
             if constexpr (MASKED) use = i != 0 && ((mask >> (i - 1)) & 1u);
             f[i] = use ? __ldg(a.fin[i] + (sz * g.plane + sy * g.pitch + sx)) : T(0);
         });
-        Cell<T, Q>::template apply<KM>(f, a.rec[slot]);
+        Cell<T, Q>::template apply<KM>(f, recipe_of<KM>(a, slot));
         const int center = z * g.plane + y * g.pitch + x;
         sfor<Q>([&](auto I) {
             constexpr int i = decltype(I)::value;
@@ -618,7 +618,7 @@ __global__ void __launch_bounds__(BX * BY + 32, 1)
             T (&f)[Q] = fr[r];
             int s = a.uniform_slot;
             if (a.slot != nullptr) s = a.slot[(static_cast<long long>(z) * g.ny + y) * g.nx + x];
-            Cell<T, Q>::template apply<KM>(f, a.rec[s]);
+            Cell<T, Q>::template apply<KM>(f, recipe_of<KM>(a, s));
             const int center = z * g.plane + y * g.pitch + x;
             sfor<Q>([&](auto I) {
                 constexpr int i = decltype(I)::value;
@@ -738,7 +738,7 @@ __global__ void __launch_bounds__(NCW * 32 + 32, (NCW >= 16 ? 1 : 2))
             });
             int s = a.uniform_slot;
             if (a.slot != nullptr) s = a.slot[(static_cast<long long>(z) * g.ny + y) * g.nx + x];
-            Cell<T, Q>::template apply<KM>(f, a.rec[s]);
+            Cell<T, Q>::template apply<KM>(f, recipe_of<KM>(a, s));
             const int center = z * g.plane + y * g.pitch + x;
             sfor<Q>([&](auto I) {
                 constexpr int i = decltype(I)::value;
@@ -852,7 +852,7 @@ __global__ void __launch_bounds__(NCW * 32 + 32, (NCW >= 16 ? 1 : 2))
             });
             int s = a.uniform_slot;
             if (a.slot != nullptr) s = a.slot[(static_cast<long long>(z) * g.ny + y) * g.nx + x];
-            Cell<T, Q>::template apply<KM>(f, a.rec[s]);
+            Cell<T, Q>::template apply<KM>(f, recipe_of<KM>(a, s));
             const int center = z * g.plane + y * g.pitch + x;
             sfor<Q>([&](auto I) {
                 constexpr int i = decltype(I)::value;
@@ -1007,6 +1007,12 @@ __global__ void __launch_bounds__(NCW * 32 + 32, (NCW >= 16 ? 1 : 2))
 #define Q27_SET(T) ENTRY(T, 27, KM_BGK), ENTRY(T, 27, KM_TRT), ENTRY(T, 27, KM_RR), ENTRY(T, 27, KM_ALL), \
         ENTRY(T, 27, KM_ALL | KM_SKIP)
 
+// registries beyond kMaxSlots instances: the catch-all sets reading the
+// recipe table from global memory
+#define XREC_SET(T)                                                                       \
+    , ENTRY(T, 19, KM_ALL | KM_XREC), ENTRY(T, 19, KM_ALL | KM_XREC | KM_SKIP), ENTRY(T, 27, KM_ALL | KM_XREC), \
+        AA_PAIR(T, 19, KM_ALL | KM_XREC), AA_PAIR(T, 27, KM_ALL | KM_XREC)
+
 // fused kinetic-energy variants: exact mode only (the reduce input must carry
 // the diagnostics' non-contracted double arithmetic)
 #ifdef DLB_FUSED_KE
@@ -1023,7 +1029,7 @@ static const KernelEntry kTable[] = {
     Q19_SET(float), Q19_SET(double), Q27_SET(float), Q27_SET(double), AA_SET(float), AA_SET(double),
     LIST_SET(float, 19), LIST_SET(double, 19), LIST_SET(float, 27), LIST_SET(double, 27),
     TMA_SET, SEG_SET(float), SEG_SET(double), TMAROW_SET(float), TMAROW_SET(double) KE_SET(float) KE_SET(double)
-        COOP_SET(float) COOP_SET(double) TMABLK_SET MB_SET
+        COOP_SET(float) COOP_SET(double) TMABLK_SET MB_SET XREC_SET(float) XREC_SET(double)
 };
 
 const KernelEntry* kernel_table(int* n) {

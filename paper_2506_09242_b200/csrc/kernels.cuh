@@ -11,7 +11,12 @@
 
 namespace dlb {
 
+// Recipes of the first kMaxSlots registry instances travel in kernel
+// parameter space (constant bank); larger registries (up to kMaxInstances,
+// the u8 slot array's range) use the KM_XREC kernels, which read the whole
+// table from global memory.
 constexpr int kMaxSlots = 16;
+constexpr int kMaxInstances = 256;
 
 // Device layout of one direction array (SoA, envelope-inclusive):
 //   element (x, y, z) of direction i, with x in [-1, nx], y in [-1, ny],
@@ -67,7 +72,16 @@ struct StepArgs {
     // set writes nothing (a timed-out halo wait fails the step and every later
     // one, so the last completed state stays intact)
     const unsigned long long* err;
+    // KM_XREC kernels: the full recipe table (any registry size) in global memory
+    const DevRecipe<T>* xrec;
 };
+
+// Recipe of slot s as the instantiation reads it.
+template <unsigned KM, typename T>
+__device__ __forceinline__ const DevRecipe<T>& recipe_of(const StepArgs<T>& a, int s) {
+    if constexpr ((KM & KM_XREC) != 0) return a.xrec[s];
+    else return a.rec[s];
+}
 
 // kernel families: dense two-population, AA even / odd, sparse lists (fluid / masked walls)
 enum Layout : int { LAYOUT_TWO_POP = 0, LAYOUT_AA = 1, LAYOUT_AA_ODD = 2, LAYOUT_LIST = 3, LAYOUT_LIST_MASKED = 4,

@@ -252,7 +252,8 @@ const KernelEntry* find_kernel(int arith, int bits, int q, unsigned km, int layo
     for (int k = 0; k < n; ++k) {
         const KernelEntry& e = t[k];
         if (e.precision_bits != bits || e.q != q || e.layout != layout || e.minb != 0) continue;
-        if ((e.km & km) != km || (e.km & (KM_SKIP | KM_KE)) != (km & (KM_SKIP | KM_KE))) continue;
+        constexpr unsigned variant = KM_SKIP | KM_KE | KM_XREC;
+        if ((e.km & km) != km || (e.km & variant) != (km & variant)) continue;
         if (!best || __builtin_popcount(e.km) < __builtin_popcount(best->km)) best = &e;
     }
     return best;
@@ -329,10 +330,11 @@ Lattice::Lattice(const dlb_lattice_desc& desc, const DynamicsRegistry& reg) : d_
         if (d_.dims[a] < 1) throw std::invalid_argument("block extents must be >= 1");
     if (d_.global_nz < d_.dims[2] || d_.z_origin < 0 || d_.z_origin + d_.dims[2] > d_.global_nz)
         throw std::invalid_argument("slab z range outside the global domain");
-    if (reg.num_instances() > kMaxSlots)
+    if (reg.num_instances() > kMaxInstances)
         throw std::invalid_argument("registry holds " + std::to_string(reg.num_instances()) +
-                                    " instances; the device recipe table holds at most " +
-                                    std::to_string(kMaxSlots));
+                                    " instances; the per-cell u8 slot array addresses at most " +
+                                    std::to_string(kMaxInstances));
+    xrec_ = reg.num_instances() > kMaxSlots;
     for (int s = 0; s < reg.num_instances(); ++s) {
         chains_.push_back(reg.chain_at_slot(s));
         tag_of_slot_.push_back(reg.tag_of_slot(s));
@@ -402,6 +404,22 @@ Lattice::Lattice(const dlb_lattice_desc& desc, const DynamicsRegistry& reg) : d_
     cuda_check(cudaMemsetAsync(d_counter_, 0, sizeof(unsigned int), stream_), "memset");
     staging_bytes_ = kStagingBytes;
     cuda_check(cudaMalloc(&staging_, staging_bytes_), "cudaMalloc staging");
+    if (xrec_) {
+        // the whole recipe table in global memory for the KM_XREC kernels
+        const std::size_t rb = d_.precision_bits == 64 ? sizeof(DevRecipe<double>) : sizeof(DevRecipe<float>);
+        std::vector<uint8_t> host(rb * chains_.size());
+        for (std::size_t k = 0; k < chains_.size(); ++k) {
+            if (d_.precision_bits == 64) {
+                const DevRecipe<double> r = compile_recipe<double>(chains_[k]);
+                std::memcpy(host.data() + k * rb, &r, rb);
+            } else {
+                const DevRecipe<float> r = compile_recipe<float>(chains_[k]);
+                std::memcpy(host.data() + k * rb, &r, rb);
+            }
+        }
+        cuda_check(cudaMalloc(&d_xrec_, host.size()), "cudaMalloc recipes");
+        cuda_check(cudaMemcpy(d_xrec_, host.data(), host.size(), cudaMemcpyHostToDevice), "upload recipes");
+    }
     setup_tma();
     cuda_check(cudaStreamSynchronize(stream_), "init");
 }
@@ -423,6 +441,7 @@ Lattice::~Lattice() {
     cudaFree(d_ke_);
     cudaFree(d_fix_);
     cudaFree(d_tmap_);
+    cudaFree(d_xrec_);
     cudaFree(d_flags_);
     cudaFree(d_counter_);
     cudaFree(staging_);
@@ -509,6 +528,7 @@ void Lattice::set_slots(const int32_t* slots) {
         // that hold at least one non-NoDynamics cell (k_pull KM_SKIP rule)
         std::vector<uint8_t> nodyn(chains_.size(), 0);
         for (std::size_t k = 0; k < chains_.size(); ++k) nodyn[k] = kind_bits(chains_[k]) == KM_NODYN;
+        if (!untagged_) check_skip_precondition(u8, nodyn);
         const int G = skip_group_;
         const long long nsx = (geo_.nx + G - 1) / G;
         // compacted segment list for the single-slab masked sweep (k_seg)
@@ -540,7 +560,7 @@ void Lattice::set_slots(const int32_t* slots) {
             nseg_ = (long long)segs.size();
         }
     }
-    sparse_ = (d_.flags & DLB_FLAG_SPARSE_LISTS) && !split() && !aa() && !(uniform && first >= 0) &&
+    sparse_ = (d_.flags & DLB_FLAG_SPARSE_LISTS) && !split() && !aa() && !(uniform && first >= 0) && !xrec_ &&
               !untagged_ && geo_.nx <= 8192 && geo_.ny <= 8192 && geo_.nz <= 4096;
     if (sparse_) {
         uniform_slot_ = 0;
@@ -562,6 +582,52 @@ void Lattice::set_slots(const int32_t* slots) {
     }
     slots_set_ = true;
     select_kernel();
+}
+
+// The masked / sparse porous sweeps never update NoDynamics cells, which is
+// exact only when no collision (Collide-kind) cell pulls from one: the
+// reference's porous setup guarantees it (a solid cell with a fluid neighbour
+// is BounceBack, cases.cpp:239-249), and bounce-back cells only ever return a
+// cell's own populations to it. Reject layouts that break it (within this
+// slab; z neighbours in other slabs are not visible here).
+void Lattice::check_skip_precondition(const std::vector<uint8_t>& u8, const std::vector<uint8_t>& nodyn) const {
+    std::vector<uint8_t> collide(chains_.size(), 0);
+    for (std::size_t k = 0; k < chains_.size(); ++k)
+        collide[k] = (kind_bits(chains_[k]) & (KM_BGK | KM_TRT | KM_RR)) != 0;
+    const int nx = geo_.nx, ny = geo_.ny, nz = geo_.nz, q = d_.q;
+    const int* cx = q == 19 ? kCx19 : kCx27;
+    const int* cy = q == 19 ? kCy19 : kCy27;
+    const int* cz = q == 19 ? kCz19 : kCz27;
+    const bool px = geo_.per_x, py = geo_.per_y, pz = d_.periodic[2] && !split();
+    const int nw = std::max(1, std::min<int>(nz, int(std::thread::hardware_concurrency())));
+    std::vector<long long> bad(std::size_t(nw), -1);
+    std::vector<std::thread> th;
+    for (int w = 0; w < nw; ++w)
+        th.emplace_back([&, w] {
+            for (int z = nz * w / nw; z < nz * (w + 1) / nw && bad[std::size_t(w)] < 0; ++z)
+                for (int y = 0; y < ny; ++y)
+                    for (int x = 0; x < nx; ++x) {
+                        const long long c = (long long)(z * ny + y) * nx + x;
+                        if (!collide[u8[std::size_t(c)]]) continue;
+                        for (int i = 1; i < q; ++i) {
+                            int X = x - cx[i], Y = y - cy[i], Z = z - cz[i];
+                            if (X < 0 || X >= nx) { if (!px) continue; X = (X + nx) % nx; }
+                            if (Y < 0 || Y >= ny) { if (!py) continue; Y = (Y + ny) % ny; }
+                            if (Z < 0 || Z >= nz) { if (!pz) continue; Z = (Z + nz) % nz; }
+                            if (nodyn[u8[std::size_t((long long)(Z * ny + Y) * nx + X)]]) {
+                                bad[std::size_t(w)] = c;
+                                return;
+                            }
+                        }
+                    }
+        });
+    for (auto& t : th) t.join();
+    for (long long c : bad)
+        if (c >= 0)
+            throw std::invalid_argument(
+                "skipping NoDynamics cells needs every collision cell's neighbours to be non-NoDynamics "
+                "(a solid cell next to fluid must bounce back, cases.cpp:239-249); cell " + std::to_string(c) +
+                " of this slab pulls from a NoDynamics cell");
 }
 
 // Sparse porous lists (see k_list): cells grouped by slot in row-major order,
@@ -652,7 +718,7 @@ void Lattice::build_fixups(const std::vector<uint8_t>& u8) {
     fixups_.clear();
     cudaFree(d_fix_);
     d_fix_ = nullptr;
-    if (aa()) return;
+    if (aa() || xrec_) return;
     std::vector<char> reg(chains_.size(), 0);
     bool any = false;
     for (std::size_t s = 0; s < chains_.size(); ++s)
@@ -890,7 +956,7 @@ void Lattice::select_kernel() {
     kernel_ke_ = nullptr;
     ke_requested_ = false;
     if (sparse_) return;
-    km_needed_ = 0;
+    km_needed_ = xrec_ ? KM_XREC : 0u;
     for (int32_t s : present_slots_) km_needed_ |= kind_bits(chains_[std::size_t(s)]);
     if ((d_.flags & (DLB_FLAG_SKIP_NODYNAMICS | DLB_FLAG_SPARSE_LISTS)) && (km_needed_ & KM_NODYN) && !aa())
         km_needed_ |= KM_SKIP;
@@ -1233,7 +1299,9 @@ void Lattice::fill_recipes(StepArgs<T>& a) const {
     a.slot = d_slot_;
     a.uniform_slot = uniform_slot_;
     a.skip_group = skip_group_;
-    for (std::size_t s = 0; s < chains_.size(); ++s) a.rec[s] = compile_recipe<T>(chains_[s]);
+    for (std::size_t s = 0; s < chains_.size() && s < std::size_t(kMaxSlots); ++s)
+        a.rec[s] = compile_recipe<T>(chains_[s]);
+    a.xrec = static_cast<const DevRecipe<T>*>(d_xrec_);
 }
 
 // Three-stage pipeline over z-chunks of a pinned host block (host layout kept
@@ -1440,7 +1508,9 @@ void Lattice::launch_coop(int64_t nsteps) {
     a.uniform_slot = uniform_slot_;
     a.skip_group = skip_group_;
     a.g = geo_;
-    for (std::size_t s = 0; s < chains_.size(); ++s) a.rec[s] = compile_recipe<T>(chains_[s]);
+    for (std::size_t s = 0; s < chains_.size() && s < std::size_t(kMaxSlots); ++s)
+        a.rec[s] = compile_recipe<T>(chains_[s]);
+    a.xrec = static_cast<const DevRecipe<T>*>(d_xrec_);
     if (coop_grid_ == 0) {
         int per_sm = 0, sms = 0;
         cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel_coop_->fn, 256, 0), "occupancy");
@@ -1478,7 +1548,9 @@ void Lattice::launch_step(int parity) {
     a.uniform_slot = uniform_slot_;
     a.skip_group = skip_group_;
     a.g = geo_;
-    for (std::size_t s = 0; s < chains_.size(); ++s) a.rec[s] = compile_recipe<T>(chains_[s]);
+    for (std::size_t s = 0; s < chains_.size() && s < std::size_t(kMaxSlots); ++s)
+        a.rec[s] = compile_recipe<T>(chains_[s]);
+    a.xrec = static_cast<const DevRecipe<T>*>(d_xrec_);
 
     const int bx = geo_.nx >= 128 ? 128 : (geo_.nx > 32 ? 64 : 32);
     const int by = 256 / bx;

@@ -202,6 +202,8 @@ class Lattice {
     std::vector<int> tag_of_slot_;
     std::vector<std::string> tag_names_;
     unsigned km_needed_ = 0;
+    bool xrec_ = false;          // more instances than the parameter-space table: KM_XREC kernels
+    void* d_xrec_ = nullptr;     // DevRecipe<T>[instances] in global memory (xrec_)
     const KernelEntry* kernel_ = nullptr;
     const KernelEntry* kernel_odd_ = nullptr;  // AA: odd-step kernel (kernel_ is the even one)
     bool aa_odd_layout_ = true;                // AA: state is in the odd / upload layout
@@ -233,6 +235,7 @@ class Lattice {
     unsigned long long* d_list_ = nullptr;
     int64_t step_bytes_ = 0;  // algorithmic bytes per step
     void build_lists(const std::vector<uint8_t>& u8);
+    void check_skip_precondition(const std::vector<uint8_t>& u8, const std::vector<uint8_t>& nodyn) const;
     // TMA-staged dense kernel (single slab): tensor maps of both buffers, and
     // whether the input buffer's envelope holds the periodic images
     const KernelEntry* kernel_tma_ = nullptr;

@@ -115,6 +115,7 @@ enum : unsigned {
     KM_ALL = 511u,
     KM_SKIP = 512u,  // variant flag: NoDynamics cells skipped (no loads / stores)
     KM_KE = 1024u,   // variant flag: also write the new state's per-cell kinetic energy (fused reduce input)
+    KM_XREC = 2048u, // variant flag: recipe table in global memory (registries beyond kMaxSlots instances)
 };
 
 template <typename T, int Q>
