@@ -14,6 +14,8 @@
 // contraction.
 #include <cooperative_groups.h>
 
+#include <algorithm>
+
 #include "kernels.cuh"
 
 #ifndef DLB_MODE
@@ -298,8 +300,8 @@ __global__ void __launch_bounds__(256, (min_blocks<T, Q, KM>()))
 // CPT cells per thread (cells t and t + 256 of a 256 * CPT-cell block range):
 // every thread issues the loads of all its cells before the first collision,
 // CPT times the bytes in flight per thread of the latency-bound fp64 sweep.
-template <typename T, int Q, unsigned KM, int CPT>
-__global__ void __launch_bounds__(256, (CPT == 1 ? min_blocks<T, Q, KM>() : 2))
+template <typename T, int Q, unsigned KM, int CPT, int MINB = 0>
+__global__ void __launch_bounds__(256, (MINB ? MINB : (CPT == 1 ? min_blocks<T, Q, KM>() : 2)))
     k_seg(const __grid_constant__ StepArgs<T> a, const unsigned* __restrict__ segs, long long nseg, int gshift) {
     const Geo& g = a.g;
     const unsigned nsx = unsigned((g.nx + (1 << gshift) - 1) >> gshift);
@@ -333,6 +335,110 @@ __global__ void __launch_bounds__(256, (CPT == 1 ? min_blocks<T, Q, KM>() : 2))
     }
 }
 
+
+// Fluid-segment porous sweep (single slab, after one k_seg step): only the
+// listed segments that hold a collision cell move. A bounce-back neighbour's
+// post-collision value in direction i is, bit for bit, the puller's own
+// population opp(i) of the step before (full-way bounce-back returns it after
+// one step in the wall cell: f_i(x_b, t) = f_opp(i)(x_b + c_i, t - 1)), which
+// is still in the output buffer (the two-population ping-pong holds state
+// t - 2 there) at the cell this thread is about to overwrite. So a collision
+// cell whose neighbour x - c_i is bounce-back (bit i of its link mask) loads
+// f_out[opp(i)][x] instead of f_in[i][x - c_i]: wall cells outside the listed
+// segments need not step at all (they are brought up to date lazily before the
+// state is read, k_bb_finalize) and their sectors -- and the solid sectors
+// behind them -- are never read. Every other cell of a listed segment runs its
+// dense update, so stores still cover whole segments.
+template <typename T, int Q, unsigned KM, int CPT>
+__global__ void __launch_bounds__(256, (CPT == 1 ? min_blocks<T, Q, KM>() : 2))
+    k_segbb(const __grid_constant__ StepArgs<T> a, const unsigned* __restrict__ segs,
+            const unsigned* __restrict__ links, long long nseg, int gshift) {
+    using L = Lat<Q>;
+    const Geo& g = a.g;
+    const unsigned nsx = unsigned((g.nx + (1 << gshift) - 1) >> gshift);
+    const long long n = nseg << gshift;
+    const long long base = static_cast<long long>(blockIdx.x) * (256 * CPT) + threadIdx.x;
+    int xs[CPT], ys[CPT], zs[CPT];
+    unsigned mk[CPT];
+    bool ok[CPT];
+    T f[CPT][Q];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+        const long long t = base + 256 * c;
+        ok[c] = t < n;
+        xs[c] = ys[c] = zs[c] = 0;
+        mk[c] = 0u;
+        if (ok[c]) {
+            const unsigned e = __ldg(segs + (t >> gshift));
+            mk[c] = __ldg(links + t);
+            const unsigned row = e / nsx;
+            xs[c] = int((e - row * nsx) << gshift) + int(t & ((1 << gshift) - 1));
+            zs[c] = int(row / unsigned(g.ny));
+            ys[c] = int(row - unsigned(zs[c]) * unsigned(g.ny));
+            ok[c] = xs[c] < g.nx;
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+        if (!ok[c]) continue;
+        const int x = xs[c], y = ys[c], z = zs[c];
+        const int xm = (x == 0 && g.per_x) ? g.nx - 1 : x - 1;
+        const int xp = (x == g.nx - 1 && g.per_x) ? 0 : x + 1;
+        const int ym = (y == 0 && g.per_y) ? g.ny - 1 : y - 1;
+        const int yp = (y == g.ny - 1 && g.per_y) ? 0 : y + 1;
+        const int zm = (z == 0 && g.per_z) ? g.nz - 1 : z - 1;
+        const int zp = (z == g.nz - 1 && g.per_z) ? 0 : z + 1;
+        const int center = z * g.plane + y * g.pitch + x;
+        sfor<Q>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            constexpr int cx = L::c[i][0], cy = L::c[i][1], cz = L::c[i][2];
+            const int sx = cx > 0 ? xm : (cx < 0 ? xp : x);
+            const int sy = cy > 0 ? ym : (cy < 0 ? yp : y);
+            const int sz = cz > 0 ? zm : (cz < 0 ? zp : z);
+            const T* src = a.fin[i] + (sz * g.plane + sy * g.pitch + sx);
+            if constexpr (i != 0) {
+                if ((mk[c] >> i) & 1u) src = a.fout[opp_of(i)] + center;
+            }
+            f[c][i] = *src;
+        });
+    }
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+        if (!ok[c]) continue;
+        const int s = a.slot ? a.slot[(static_cast<long long>(zs[c]) * g.ny + ys[c]) * g.nx + xs[c]] : a.uniform_slot;
+        collide_store_cell<T, Q, KM>(a, xs[c], ys[c], zs[c], s, f[c]);
+    }
+}
+
+// Lazy update of the wall cells the fluid-segment sweep leaves alone, before
+// the state is read: for every listed (cell, link j) whose reader x_b + c_j is
+// a collision cell, f_j(x_b) = f_opp(j)(x_b + c_j) of the previous state --
+// exactly the bounce-back cell's own update on those links. Entry: x | y << 13
+// | z << 26 | link mask << 38 (as k_list).
+template <typename T, int Q>
+__global__ void k_bb_finalize(T* cur, const T* prev, Geo g, const unsigned long long* __restrict__ list,
+                              long long n) {
+    using L = Lat<Q>;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+        const unsigned long long e = list[k];
+        const int x = int(e & 0x1fffull), y = int((e >> 13) & 0x1fffull), z = int((e >> 26) & 0xfffull);
+        const unsigned mask = unsigned(e >> 38);
+        const int center = z * g.plane + y * g.pitch + x;
+        sfor<Q>([&](auto I) {
+            constexpr int j = decltype(I)::value;
+            if constexpr (j != 0) {
+                if ((mask >> (j - 1)) & 1u) {
+                    constexpr int cx = L::c[j][0], cy = L::c[j][1], cz = L::c[j][2];
+                    int X = x + cx, Y = y + cy, Z = z + cz;
+                    if (g.per_x) X = X < 0 ? X + g.nx : (X >= g.nx ? X - g.nx : X);
+                    if (g.per_y) Y = Y < 0 ? Y + g.ny : (Y >= g.ny ? Y - g.ny : Y);
+                    if (g.per_z) Z = Z < 0 ? Z + g.nz : (Z >= g.nz ? Z - g.nz : Z);
+                    cur[j * g.dstride + center] = prev[opp_of(j) * g.dstride + Z * g.plane + Y * g.pitch + X];
+                }
+            }
+        });
+    }
+}
 
 // AA-pattern in-place streaming (PAPER.md:104 future work): one
 // population array A, two alternating kernels, every location read and
@@ -953,6 +1059,26 @@ __global__ void __launch_bounds__(NCW * 32 + 32, (NCW >= 16 ? 1 : 2))
             "k_seg<" #T ",D3Q" #Q "," #KM ",x" #CPT ">[" DLB_STR(DLB_MODE) "]", 0, 0, 0, CPT \
     }
 #define SEG_ENTRY(T, Q, KM) SEG_ENTRY1(T, Q, KM, 1), SEG_ENTRY1(T, Q, KM, 2)
+#define SEGBB_ENTRY1(T, Q, KM, CPT)                                                      \
+    KernelEntry {                                                                        \
+        int(sizeof(T) * 8), Q, unsigned(KM), LAYOUT_SEGBB,                                \
+            reinterpret_cast<const void*>(&k_segbb<T, Q, unsigned(KM), CPT>),             \
+            "k_segbb<" #T ",D3Q" #Q "," #KM ",x" #CPT ">[" DLB_STR(DLB_MODE) "]", 0, 0, 0, CPT \
+    }
+#define SEGBB_ENTRY(T, Q, KM) SEGBB_ENTRY1(T, Q, KM, 1), SEGBB_ENTRY1(T, Q, KM, 2)
+#define SEGBB_SET(T)                                                                      \
+    , SEGBB_ENTRY(T, 19, KM_BGK | KM_BB | KM_NODYN), SEGBB_ENTRY(T, 19, KM_TRT | KM_BB | KM_NODYN), \
+        SEGBB_ENTRY(T, 19, KM_RR | KM_BB | KM_NODYN), SEGBB_ENTRY(T, 27, KM_BGK | KM_BB | KM_NODYN), \
+        SEGBB_ENTRY(T, 27, KM_TRT | KM_BB | KM_NODYN), SEGBB_ENTRY(T, 27, KM_RR | KM_BB | KM_NODYN)
+#define SEG_MB(T, Q, KM, CPT, MB)                                                        \
+    KernelEntry {                                                                        \
+        int(sizeof(T) * 8), Q, unsigned(KM), LAYOUT_SEG,                                  \
+            reinterpret_cast<const void*>(&k_seg<T, Q, unsigned(KM), CPT, MB>),           \
+            "k_seg<" #T ",D3Q" #Q "," #KM ",x" #CPT ",b" #MB ">[" DLB_STR(DLB_MODE) "]", 0, 0, 0, CPT, 0, MB \
+    }
+#define SEG_MB_SET                                                                        \
+    , SEG_MB(double, 19, KM_TRT | KM_BB | KM_NODYN, 1, 4), SEG_MB(double, 19, KM_TRT | KM_BB | KM_NODYN, 1, 5), \
+        SEG_MB(double, 19, KM_TRT | KM_BB | KM_NODYN, 2, 3)
 #define SEG_SET(T)                                                                        \
     SEG_ENTRY(T, 19, KM_BGK | KM_BB | KM_NODYN), SEG_ENTRY(T, 19, KM_TRT | KM_BB | KM_NODYN), \
         SEG_ENTRY(T, 19, KM_RR | KM_BB | KM_NODYN),                                       \
@@ -1029,8 +1155,22 @@ static const KernelEntry kTable[] = {
     Q19_SET(float), Q19_SET(double), Q27_SET(float), Q27_SET(double), AA_SET(float), AA_SET(double),
     LIST_SET(float, 19), LIST_SET(double, 19), LIST_SET(float, 27), LIST_SET(double, 27),
     TMA_SET, SEG_SET(float), SEG_SET(double), TMAROW_SET(float), TMAROW_SET(double) KE_SET(float) KE_SET(double)
-        COOP_SET(float) COOP_SET(double) TMABLK_SET MB_SET XREC_SET(float) XREC_SET(double)
+        COOP_SET(float) COOP_SET(double) TMABLK_SET MB_SET XREC_SET(float) XREC_SET(double) SEG_MB_SET
+        SEGBB_SET(float) SEGBB_SET(double)
 };
+
+void launch_bb_finalize(int bits, int q, void* cur, const void* prev, const Geo& g,
+                        const unsigned long long* list, long long n, cudaStream_t st) {
+    if (n <= 0) return;
+    const int grid = int(std::min<long long>((n + 255) / 256, 148LL * 16));
+    if (bits == 64) {
+        if (q == 19) k_bb_finalize<double, 19><<<grid, 256, 0, st>>>((double*)cur, (const double*)prev, g, list, n);
+        else k_bb_finalize<double, 27><<<grid, 256, 0, st>>>((double*)cur, (const double*)prev, g, list, n);
+    } else {
+        if (q == 19) k_bb_finalize<float, 19><<<grid, 256, 0, st>>>((float*)cur, (const float*)prev, g, list, n);
+        else k_bb_finalize<float, 27><<<grid, 256, 0, st>>>((float*)cur, (const float*)prev, g, list, n);
+    }
+}
 
 const KernelEntry* kernel_table(int* n) {
     *n = int(sizeof(kTable) / sizeof(kTable[0]));

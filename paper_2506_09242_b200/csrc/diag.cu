@@ -375,6 +375,7 @@ int64_t Lattice::reduce_count(const dlb_reduce_args& a) const {
 
 void Lattice::reduce_parts(const dlb_reduce_args& a, int64_t n_total, int64_t seg_begin,
                            std::vector<dlb_tree_part>& out) {
+    finalize_walls();
     DeviceGuard dg(device_);
     check_args(d_, a);
     if (!slots_set_) throw std::invalid_argument("diagnostics: dynamics slots not set");
@@ -518,6 +519,7 @@ void Lattice::velocity_planes_impl(int z0, int np, double* dev_out) {
 }
 
 void Lattice::velocity_planes(int z0, int np, double* out) {
+    finalize_walls();
     DeviceGuard dg(device_);
     if (!slots_set_) throw std::invalid_argument("diagnostics: dynamics slots not set");
     if (z0 < 0 || np < 0 || z0 + np > d_.dims[2]) throw std::invalid_argument("velocity_planes: planes outside the slab");
@@ -536,6 +538,7 @@ void Lattice::velocity_planes(int z0, int np, double* out) {
 }
 
 void Lattice::snapshot_velocity() {
+    finalize_walls();
     DeviceGuard dg(device_);
     if (!slots_set_) throw std::invalid_argument("diagnostics: dynamics slots not set");
     cuda_check(cudaStreamSynchronize(stream_), "sync");

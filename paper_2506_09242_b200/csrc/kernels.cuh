@@ -86,7 +86,7 @@ __device__ __forceinline__ const DevRecipe<T>& recipe_of(const StepArgs<T>& a, i
 // kernel families: dense two-population, AA even / odd, sparse lists (fluid / masked walls)
 enum Layout : int { LAYOUT_TWO_POP = 0, LAYOUT_AA = 1, LAYOUT_AA_ODD = 2, LAYOUT_LIST = 3, LAYOUT_LIST_MASKED = 4,
                     LAYOUT_TMA = 5, LAYOUT_SEG = 6, LAYOUT_TMAROW = 7,
-                    LAYOUT_COOP = 8, LAYOUT_TMABLK = 9 };
+                    LAYOUT_COOP = 8, LAYOUT_TMABLK = 9, LAYOUT_SEGBB = 10 };
 
 struct KernelEntry {
     int precision_bits;
@@ -104,5 +104,11 @@ struct KernelEntry {
 // Kernel tables of the two arithmetic modes (one translation unit each).
 namespace exact { const KernelEntry* kernel_table(int* n); }
 namespace fast { const KernelEntry* kernel_table(int* n); }
+// Lazy wall-cell update of the fluid-segment sweep (k_bb_finalize); cur / prev
+// are the interior origins of direction 0 of the two buffers.
+namespace exact {
+void launch_bb_finalize(int bits, int q, void* cur, const void* prev, const Geo& g,
+                        const unsigned long long* list, long long n, cudaStream_t st);
+}
 
 }  // namespace dlb

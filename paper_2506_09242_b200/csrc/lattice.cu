@@ -438,6 +438,9 @@ Lattice::~Lattice() {
     cudaFree(d_slot_);
     cudaFree(d_list_);
     cudaFree(d_seg_);
+    cudaFree(d_fseg_);
+    cudaFree(d_flink_);
+    cudaFree(d_bbfin_);
     cudaFree(d_ke_);
     cudaFree(d_fix_);
     cudaFree(d_tmap_);
@@ -472,6 +475,8 @@ int64_t Lattice::bytes_per_cell() const {
 
 int64_t Lattice::step_bytes() const {
     if (sparse_) return step_bytes_;
+    if (kernel_segbb_ && !(lower_.linked || upper_.linked))  // listed cells: populations, slot, link mask; 4 B / segment
+        return (int64_t(2) * d_.q * (d_.precision_bits / 8) + 1 + 4) * fseg_cells_ + 4 * nfseg_;
     if (kernel_seg_ && !(lower_.linked || upper_.linked))  // listed cells + their slot bytes + 4 B per segment
         return (int64_t(2) * d_.q * (d_.precision_bits / 8) + 1) * masked_cells_ + 4 * nseg_;
     if ((km_needed_ & KM_SKIP) && masked_cells_ >= 0)
@@ -558,6 +563,9 @@ void Lattice::set_slots(const int32_t* slots) {
             cuda_check(cudaMemcpy(d_seg_, segs.data(), segs.size() * sizeof(uint32_t), cudaMemcpyHostToDevice),
                        "upload segments");
             nseg_ = (long long)segs.size();
+            build_fluid_segments(u8);
+        } else {
+            build_fluid_segments({});
         }
     }
     sparse_ = (d_.flags & DLB_FLAG_SPARSE_LISTS) && !split() && !aa() && !(uniform && first >= 0) && !xrec_ &&
@@ -628,6 +636,136 @@ void Lattice::check_skip_precondition(const std::vector<uint8_t>& u8, const std:
                 "skipping NoDynamics cells needs every collision cell's neighbours to be non-NoDynamics "
                 "(a solid cell next to fluid must bounce back, cases.cpp:239-249); cell " + std::to_string(c) +
                 " of this slab pulls from a NoDynamics cell");
+}
+
+// Fluid-segment sweep (k_segbb, single slab, DLB_FLUID_SEGMENTS=1): the
+// x-aligned segments holding a collision cell, a per-listed-cell mask of the
+// links whose source is a bounce-back cell (read from the puller's own previous
+// state instead), and the wall cells outside those segments that face a
+// collision cell (brought up to date by k_bb_finalize before the state is
+// read). Needs: no moving wall, no regularized cell next to a wall (its list
+// fix-up pulls directly), registry within the parameter-space table.
+void Lattice::build_fluid_segments(const std::vector<uint8_t>& u8) {
+    cudaFree(d_fseg_);
+    cudaFree(d_flink_);
+    cudaFree(d_bbfin_);
+    d_fseg_ = nullptr;
+    d_flink_ = nullptr;
+    d_bbfin_ = nullptr;
+    nfseg_ = nbbfin_ = fseg_cells_ = 0;
+    bb_prologue_ = true;
+    bb_dirty_ = false;
+    // opt-in (DLB_FLUID_SEGMENTS=1): on c4 it writes 23 % fewer bytes but reads
+    // 15 % more (the puller's own previous sector for every wall link), for the
+    // same time as k_seg (profiles/r02_summary.md)
+    const char* fe = std::getenv("DLB_FLUID_SEGMENTS");
+    if (u8.empty() || !(fe && fe[0] == '1') || xrec_ || aa() || split()) return;
+    const int nsl = int(chains_.size());
+    std::vector<uint8_t> collide(std::size_t(nsl), 0), bb(std::size_t(nsl), 0), reg(std::size_t(nsl), 0);
+    for (int k = 0; k < nsl; ++k) {
+        const unsigned kb = kind_bits(chains_[std::size_t(k)]);
+        if (kb & KM_MBB) return;
+        collide[std::size_t(k)] = (kb & (KM_BGK | KM_TRT | KM_RR)) != 0;
+        bb[std::size_t(k)] = kb == KM_BB;
+        reg[std::size_t(k)] = (kb & (KM_REGV | KM_REGP)) != 0;
+    }
+    const int nx = geo_.nx, ny = geo_.ny, nz = geo_.nz, q = d_.q, G = skip_group_;
+    if (nx > 8192 || ny > 8192 || nz > 4096) return;
+    const int* cx = q == 19 ? kCx19 : kCx27;
+    const int* cy = q == 19 ? kCy19 : kCy27;
+    const int* cz = q == 19 ? kCz19 : kCz27;
+    const bool px = geo_.per_x, py = geo_.per_y, pz = geo_.per_z;
+    auto at = [&](int x, int y, int z, int* out) {  // neighbour (x, y, z) inside the lattice, wrapped
+        if (x < 0 || x >= nx) { if (!px) return false; x = (x + nx) % nx; }
+        if (y < 0 || y >= ny) { if (!py) return false; y = (y + ny) % ny; }
+        if (z < 0 || z >= nz) { if (!pz) return false; z = (z + nz) % nz; }
+        *out = u8[std::size_t((long long)(z * ny + y) * nx + x)];
+        return true;
+    };
+    const long long nsx = (nx + G - 1) / G;
+    const int nw = std::max(1, std::min<int>(nz, int(std::thread::hardware_concurrency())));
+    struct Part {
+        std::vector<uint32_t> segs, links;
+        std::vector<unsigned long long> fin;
+        long long cells = 0;
+        bool bad = false;
+    };
+    std::vector<Part> part(static_cast<std::size_t>(nw));
+    std::vector<std::thread> th;
+    for (int w = 0; w < nw; ++w)
+        th.emplace_back([&, w] {
+            Part& P = part[std::size_t(w)];
+            for (int z = nz * w / nw; z < nz * (w + 1) / nw && !P.bad; ++z)
+                for (int y = 0; y < ny; ++y) {
+                    const uint8_t* row = u8.data() + (long long)(z * ny + y) * nx;
+                    for (int x0 = 0; x0 < nx; x0 += G) {
+                        const int x1 = std::min(nx, x0 + G);
+                        bool listed = false;
+                        for (int x = x0; x < x1 && !listed; ++x) listed = collide[row[x]];
+                        if (listed) {
+                            P.segs.push_back(uint32_t((long long)(z * ny + y) * nsx + x0 / G));
+                            P.cells += x1 - x0;
+                        }
+                        for (int x = x0; x < x0 + G; ++x) {
+                            const int sl = x < nx ? row[x] : -1;
+                            if (listed) {
+                                unsigned mask = 0;
+                                if (sl >= 0 && collide[std::size_t(sl)])
+                                    for (int i = 1; i < q; ++i) {
+                                        int nb;
+                                        if (at(x - cx[i], y - cy[i], z - cz[i], &nb) && bb[std::size_t(nb)]) {
+                                            if (reg[std::size_t(sl)]) P.bad = true;  // its list fix-up pulls directly
+                                            mask |= 1u << i;
+                                        }
+                                    }
+                                P.links.push_back(mask);
+                            } else if (sl >= 0 && bb[std::size_t(sl)]) {
+                                unsigned long long mask = 0;
+                                for (int j = 1; j < q; ++j) {
+                                    int nb;
+                                    if (at(x + cx[j], y + cy[j], z + cz[j], &nb) && collide[std::size_t(nb)])
+                                        mask |= 1ull << (j - 1);
+                                }
+                                if (mask)
+                                    P.fin.push_back((unsigned long long)x | ((unsigned long long)y << 13) |
+                                                    ((unsigned long long)z << 26) | (mask << 38));
+                            }
+                        }
+                    }
+                }
+        });
+    for (auto& t : th) t.join();
+    std::vector<uint32_t> segs, links;
+    std::vector<unsigned long long> fin;
+    for (auto& P : part) {
+        if (P.bad) return;
+        segs.insert(segs.end(), P.segs.begin(), P.segs.end());
+        links.insert(links.end(), P.links.begin(), P.links.end());
+        fin.insert(fin.end(), P.fin.begin(), P.fin.end());
+        fseg_cells_ += P.cells;
+    }
+    if (segs.empty() || segs.size() >= (1ull << 32) / std::size_t(G)) return;
+    cuda_check(cudaMalloc(&d_fseg_, segs.size() * 4), "cudaMalloc fluid segments");
+    cuda_check(cudaMemcpy(d_fseg_, segs.data(), segs.size() * 4, cudaMemcpyHostToDevice), "upload");
+    cuda_check(cudaMalloc(&d_flink_, links.size() * 4), "cudaMalloc link masks");
+    cuda_check(cudaMemcpy(d_flink_, links.data(), links.size() * 4, cudaMemcpyHostToDevice), "upload");
+    if (!fin.empty()) {
+        cuda_check(cudaMalloc(&d_bbfin_, fin.size() * 8), "cudaMalloc wall list");
+        cuda_check(cudaMemcpy(d_bbfin_, fin.data(), fin.size() * 8, cudaMemcpyHostToDevice), "upload");
+    }
+    nfseg_ = (long long)segs.size();
+    nbbfin_ = (long long)fin.size();
+}
+
+// Bring the wall cells the fluid-segment sweep skipped up to date (their
+// collision-facing links) before anything reads the state.
+void Lattice::finalize_walls() {
+    if (!bb_dirty_) return;
+    DeviceGuard dg(device_);
+    exact::launch_bb_finalize(d_.precision_bits, d_.q, origin(cur_), origin(1 - cur_), geo_, d_bbfin_, nbbfin_,
+                              stream_);
+    cuda_check(cudaGetLastError(), "k_bb_finalize");
+    bb_dirty_ = false;
 }
 
 // Sparse porous lists (see k_list): cells grouped by slot in row-major order,
@@ -943,6 +1081,7 @@ void Lattice::set_uniform_slot(int32_t slot) {
     cudaFree(d_seg_);
     d_seg_ = nullptr;
     nseg_ = 0;
+    build_fluid_segments({});
     masked_cells_ = -1;
     uniform_slot_ = slot;
     untagged_ = false;
@@ -992,14 +1131,26 @@ void Lattice::select_kernel() {
         // (c4: 24.96 vs 23.76 GLUPS, profiles/r01_summary.md), 1 for fp32
         const char* ce = std::getenv("DLB_SEG_CPT");
         const int cpt = ce ? std::atoi(ce) : (d_.precision_bits == 64 ? 2 : 1);
-        if (kernel_seg_ && kernel_seg_->cpt != cpt) {
+        const char* me = std::getenv("DLB_SEG_MINB");  // occupancy-target variant (tuning)
+        const int minb = me ? std::atoi(me) : 0;
+        if (kernel_seg_ && (kernel_seg_->cpt != cpt || minb)) {
             int nt = 0;
             const KernelEntry* t = d_.arith == DLB_ARITH_FAST ? fast::kernel_table(&nt) : exact::kernel_table(&nt);
             for (int k = 0; k < nt; ++k)
                 if (t[k].layout == LAYOUT_SEG && t[k].km == kernel_seg_->km && t[k].cpt == cpt &&
-                    t[k].precision_bits == kernel_seg_->precision_bits && t[k].q == kernel_seg_->q)
+                    t[k].minb == minb && t[k].precision_bits == kernel_seg_->precision_bits &&
+                    t[k].q == kernel_seg_->q)
                     kernel_seg_ = &t[k];
         }
+    }
+    kernel_segbb_ = nullptr;
+    if (kernel_seg_ && d_fseg_) {
+        int nt = 0;
+        const KernelEntry* t = d_.arith == DLB_ARITH_FAST ? fast::kernel_table(&nt) : exact::kernel_table(&nt);
+        for (int k = 0; k < nt; ++k)
+            if (t[k].layout == LAYOUT_SEGBB && t[k].km == kernel_seg_->km && t[k].cpt == kernel_seg_->cpt &&
+                t[k].precision_bits == kernel_seg_->precision_bits && t[k].q == kernel_seg_->q)
+                kernel_segbb_ = &t[k];
     }
     // fused kinetic-energy variant of the dense sweep (exact mode, single
     // two-population slab, no regularized fix-ups): used for the steps a
@@ -1080,6 +1231,8 @@ void Lattice::reset_aa() {
 
 void Lattice::fill_equilibrium(const double* rho, const double* ux, const double* uy,
                                const double* uz) {
+    bb_prologue_ = true;
+    bb_dirty_ = false;
     envelope_valid_ = false;
     DeviceGuard dg(device_);
     reset_aa();
@@ -1112,6 +1265,8 @@ void Lattice::fill_equilibrium(const double* rho, const double* ux, const double
 // Uniform equilibrium state (rho, u) in every cell: the chunked equilibrium
 // fill with constant staging arrays (same k_fill_eq arithmetic).
 void Lattice::fill_uniform(double rho, double ux, double uy, double uz) {
+    bb_prologue_ = true;
+    bb_dirty_ = false;
     const long long plane_cells = (long long)geo_.nx * geo_.ny;
     const int zc = int(std::max<long long>(1, std::min<long long>(geo_.nz, (long long)(staging_bytes_ / 32) / plane_cells)));
     const long long n = plane_cells * zc;
@@ -1145,6 +1300,8 @@ void Lattice::fill_uniform(double rho, double ux, double uy, double uz) {
 }
 
 void Lattice::fill_tgv(int64_t L, double u_inf) {
+    bb_prologue_ = true;
+    bb_dirty_ = false;
     if (d_.dims[0] != L || d_.dims[1] != L || d_.global_nz != L)
         throw std::invalid_argument("TGV fill needs an L^3 domain");
     DeviceGuard dg(device_);
@@ -1181,6 +1338,10 @@ void Lattice::copy_canonical(void* host, bool to_device, bool as_double, int ele
     if (to_device) {
         reset_aa();
         envelope_valid_ = false;
+        bb_prologue_ = true;
+        bb_dirty_ = false;
+    } else {
+        finalize_walls();
     }
     const long long plane_cells = (long long)geo_.nx * geo_.ny;
     const long long n = cells();
@@ -1234,6 +1395,8 @@ void Lattice::download_raw(void* canon) {
 // Envelope-inclusive AcceleratedBlock arrays: the whole (nx+2)(ny+2)(nz+2)
 // box of every direction, including the envelope the caller refreshed.
 void Lattice::upload_block(const void* f, const int64_t ext[3]) {
+    bb_prologue_ = true;
+    bb_dirty_ = false;
     envelope_valid_ = false;
     DeviceGuard dg(device_);
     const int s = d_.precision_bits / 8;
@@ -1591,8 +1754,23 @@ void Lattice::launch_step(int parity) {
         a.z_step = 1;
         void* args[] = {&a};
         const bool split_rare = kernel_main_ != nullptr && !fixups_.empty();
-        if (kernel_seg_) {
+        if (kernel_segbb_ && !bb_prologue_) {
+            // fluid-segment sweep: wall cells outside the listed segments skip
+            const unsigned* sp = d_fseg_;
+            const unsigned* lp = d_flink_;
+            long long ns = nfseg_;
+            int gshift = 0;
+            while ((1 << gshift) < skip_group_) ++gshift;
+            void* sargs[] = {&a, &sp, &lp, &ns, &gshift};
+            const long long threads = ns << gshift;
+            const long long per_block = 256LL * kernel_segbb_->cpt;
+            cuda_check(cudaLaunchKernel(kernel_segbb_->fn, dim3(unsigned((threads + per_block - 1) / per_block)),
+                                        dim3(256), sargs, 0, stream_), "launch fluid segments");
+            bb_dirty_ = true;
+        } else if (kernel_seg_) {
             // compacted masked sweep: one thread per cell of the listed segments
+            // (also the first step of the fluid-segment sweep: it leaves every
+            // listed cell current in both buffers)
             const unsigned* sp = d_seg_;
             long long ns = nseg_;
             int gshift = 0;
@@ -1602,6 +1780,8 @@ void Lattice::launch_step(int parity) {
             const long long per_block = 256LL * kernel_seg_->cpt;
             cuda_check(cudaLaunchKernel(kernel_seg_->fn, dim3(unsigned((threads + per_block - 1) / per_block)),
                                         dim3(256), sargs, 0, stream_), "launch segments");
+            bb_prologue_ = false;
+            bb_dirty_ = false;
         } else if (ke_requested_ && kernel_ke_) {
             if (!d_ke_) {
                 cuda_check(cudaMalloc(&d_ke_, std::size_t(cells()) * sizeof(double)), "cudaMalloc kinetic energy");
@@ -1721,6 +1901,7 @@ void Lattice::ensure_graph() {
     const int cur = cur_;
     const bool odd = aa_odd_layout_;
     const int64_t steps = steps_, halo_steps = halo_steps_;
+    const bool bb_dirty = bb_dirty_, bb_prologue = bb_prologue_;
     cudaGraph_t g = nullptr;
     cuda_check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "begin capture");
     enqueue_step();
@@ -1730,6 +1911,8 @@ void Lattice::ensure_graph() {
     aa_odd_layout_ = odd;
     steps_ = steps;
     halo_steps_ = halo_steps;
+    bb_dirty_ = bb_dirty;
+    bb_prologue_ = bb_prologue;
     // keep the halo branch's stream priority inside the replayed graph
     cuda_check(cudaGraphInstantiateWithFlags(&graph_, g, cudaGraphInstantiateFlagUseNodePriority),
                "graph instantiate");
@@ -1761,6 +1944,10 @@ void Lattice::step(int64_t nsteps) {
         else launch_coop<float>(nsteps);
         k = nsteps;
     }
+    if (kernel_segbb_ && bb_prologue_ && k < nsteps && !(lower_.linked || upper_.linked)) {
+        enqueue_step();  // the fluid-segment sweep's first step (k_seg) stays out of the graph
+        ++k;
+    }
     if (nsteps - k >= 4 && !trace_halo_) {
         const bool aligned = aa() ? aa_odd_layout_ : cur_ == 0;
         if (!aligned) {
@@ -1772,6 +1959,7 @@ void Lattice::step(int64_t nsteps) {
             cuda_check(cudaGraphLaunch(graph_, stream_), "graph launch");
             steps_ += 2;
             if (lower_.linked || upper_.linked) halo_steps_ += 2;
+            if (kernel_segbb_) bb_dirty_ = true;
         }
     }
     for (; k < nsteps; ++k) enqueue_step();
@@ -1823,6 +2011,7 @@ void Lattice::exchange() {
 
 void Lattice::checksum(unsigned long long* per_dir, bool active_only) {
     DeviceGuard dg(device_);
+    finalize_walls();
     cuda_check(cudaStreamSynchronize(stream_), "sync");
     unsigned long long* d = static_cast<unsigned long long*>(staging_);
     cuda_check(cudaMemsetAsync(d, 0, 27 * 8, stream_), "memset");
@@ -1852,6 +2041,7 @@ void Lattice::checksum(unsigned long long* per_dir, bool active_only) {
 
 void Lattice::gather_macroscopic(double* rho, double* ux, double* uy, double* uz) {
     DeviceGuard dg(device_);
+    finalize_walls();
     cuda_check(cudaStreamSynchronize(stream_), "sync");
     std::vector<MacroSlot> ms(std::max<std::size_t>(chains_.size(), 1));
     for (std::size_t s = 0; s < chains_.size(); ++s) {

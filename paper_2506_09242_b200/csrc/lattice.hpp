@@ -119,6 +119,7 @@ class Lattice {
     int launches_per_step() const;
     const char* kernel_name() const {
         if (kernel_tma_ && !(lower_.linked || upper_.linked)) return kernel_tma_->name;
+        if (kernel_segbb_ && !(lower_.linked || upper_.linked)) return kernel_segbb_->name;
         if (kernel_seg_ && !(lower_.linked || upper_.linked)) return kernel_seg_->name;
         if (kernel_main_ && !fixups_.empty() && !(lower_.linked || upper_.linked)) return kernel_main_->name;
         return kernel_ ? kernel_->name : "<none>";
@@ -175,6 +176,17 @@ class Lattice {
     unsigned* d_seg_ = nullptr;
     long long nseg_ = 0;
     const KernelEntry* kernel_seg_ = nullptr;
+    // fluid-segment sweep (k_segbb): segments with a collision cell, their
+    // per-cell bounce-back link masks, the wall cells finalized lazily
+    unsigned* d_fseg_ = nullptr;
+    unsigned* d_flink_ = nullptr;
+    unsigned long long* d_bbfin_ = nullptr;
+    long long nfseg_ = 0, nbbfin_ = 0, fseg_cells_ = 0;
+    const KernelEntry* kernel_segbb_ = nullptr;
+    bool bb_prologue_ = true;  // next step must be a full k_seg step (buffers not yet ping-pong current)
+    bool bb_dirty_ = false;    // wall cells outside the fluid segments are behind the state
+    void build_fluid_segments(const std::vector<uint8_t>& u8);
+    void finalize_walls();
     // fused kinetic energy (KM_KE variant): per-cell values of the state after
     // step ke_step_, consumed by the next DLB_Q_KINETIC reduction
     const KernelEntry* kernel_ke_ = nullptr;
