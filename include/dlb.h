@@ -177,7 +177,11 @@ DLB_API dlb_status dlb_lattice_kernel_name(dlb_lattice* lat, char* buf, size_t c
 
 /* ---- z-slab halo exchange over peer memory ---------------------------------- */
 /* Same process (any devices with peer access, or one device): the top plane of
- * `lower` feeds the bottom ghost plane of `upper` and vice versa. */
+ * `lower` feeds the bottom ghost plane of `upper` and vice versa. Both slabs
+ * must share the layout. AA slabs (one in-place array per slab) may be linked
+ * too: their odd steps store across the faces into the neighbour's boundary
+ * plane, so linking clears an AA slab's state (fill / upload after linking,
+ * then exchange, as MultiBlockRun does). */
 DLB_API dlb_status dlb_lattice_link_local(dlb_lattice* lower, dlb_lattice* upper);
 /* Envelope exchange only (MultiBlockRun::exchange, multiblock.hpp:142-143):
  * copy this slab's boundary planes into the linked neighbours' ghost planes of

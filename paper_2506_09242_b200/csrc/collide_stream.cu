@@ -41,6 +41,29 @@ constexpr int min_blocks() {
     return heavy ? 2 : 3;
 }
 
+// Completion signal of a boundary launch: publish this block's peer stores at
+// system scope, take a ticket; the last block bumps the slab's step counter and
+// release-stores it into both neighbours' flags (read by their k_halo_wait).
+template <typename T>
+__device__ __forceinline__ void signal_step(const StepArgs<T>& a) {
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+        const unsigned total = gridDim.x * gridDim.y * gridDim.z;
+        const unsigned ticket = atomicAdd(a.counter, 1u);
+        if (ticket == total - 1) {
+            __threadfence_system();
+            *a.counter = 0u;
+            const unsigned long long s = *a.my_step + 1ull;
+            *a.my_step = s;
+            if (a.sig_up != nullptr)
+                asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a.sig_up), "l"(s) : "memory");
+            if (a.sig_down != nullptr)
+                asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a.sig_down), "l"(s) : "memory");
+        }
+    }
+}
+
 // One cell of the two-population pull step: gather f_i(x) <- f_i(x - c_i)
 // from the input buffer (periodic axes wrap in-kernel, non-periodic faces
 // read the zero envelope / ghost planes), apply the slot's dynamics, store to
@@ -214,25 +237,7 @@ __global__ void __launch_bounds__(256, (MINB ? MINB : min_blocks<T, Q, KM>()))
     }
 
 
-    if (a.counter != nullptr) {
-        // Publish this block's peer stores at system scope, then take a ticket.
-        __threadfence_system();
-        __syncthreads();
-        if (threadIdx.x == 0 && threadIdx.y == 0) {
-            const unsigned total = gridDim.x * gridDim.y * gridDim.z;
-            const unsigned ticket = atomicAdd(a.counter, 1u);
-            if (ticket == total - 1) {
-                __threadfence_system();
-                *a.counter = 0u;
-                const unsigned long long s = *a.my_step + 1ull;
-                *a.my_step = s;
-                if (a.sig_up != nullptr)
-                    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a.sig_up), "l"(s) : "memory");
-                if (a.sig_down != nullptr)
-                    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a.sig_down), "l"(s) : "memory");
-            }
-        }
-    }
+    if (a.counter != nullptr) signal_step(a);
 }
 
 
@@ -452,71 +457,126 @@ __global__ void k_bb_finalize(T* cur, const T* prev, Geo g, const unsigned long 
 // A[i][x] (the location the next even step reads for that link); pushes
 // across a non-periodic face land in the envelope, where they stay part of the
 // canonical state but are never read.
-template <typename T, int Q, unsigned KM, bool ODD>
+//
+// Linked z-slabs (boundary launch, push_up / push_down set). Every location
+// of the global AA array is still touched by exactly one cell per step; the
+// ones across a slab face belong to the neighbour, so:
+//  * even step: nothing crosses a face; the top plane additionally stores its
+//    c_z = +1 populations f_i into the upper neighbour's A[i] at z = -1, the
+//    bottom plane its c_z = -1 ones into the lower neighbour's A[i] at z = nz
+//    (the two-population push; these ghost slots are never part of the state);
+//  * odd step: a pull from across the face reads that pushed value, A[i] of the
+//    own ghost plane (instead of A[opp(i)] of the neighbour's boundary plane,
+//    which holds the same number); the store A[i][x + c_i] across the face goes
+//    to the neighbour's boundary plane (z = 0 of the upper, z = nz - 1 of the
+//    lower), where its next even step reads it, and to the own ghost plane
+//    (the canonical odd-layout value of this slab's cell, read by downloads).
+// Linked slabs therefore rest in the even layout after a fill / upload (their
+// first step is odd), and the halo protocol of the two-population scheme
+// (wait for both neighbours' previous boundary launch, signal after ours)
+// orders every cross-face access. LINKED: the boundary-plane instantiation
+// (catch-all dispatch set; the interior launch runs the lean one, whose
+// register budget the face logic would overflow).
+template <typename T, int Q, unsigned KM, bool ODD, bool LINKED = false>
 __global__ void __launch_bounds__(256, (min_blocks<T, Q, KM>())) k_aa(const __grid_constant__ StepArgs<T> a) {
     using L = Lat<Q>;
     const Geo& g = a.g;
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int y = blockIdx.y * blockDim.y + threadIdx.y;
     const int z = a.z_begin + int(blockIdx.z) * a.z_step;
-    if (x >= g.nx || y >= g.ny) return;
-    const int center = z * g.plane + y * g.pitch + x;
-    T f[Q];
-    if constexpr (!ODD) {
-        sfor<Q>([&](auto I) {
-            constexpr int i = decltype(I)::value;
-            f[i] = a.fin[i][center];
-        });
-    } else {
-        const int xm = (x == 0 && g.per_x) ? g.nx - 1 : x - 1;
-        const int xp = (x == g.nx - 1 && g.per_x) ? 0 : x + 1;
-        const int ym = (y == 0 && g.per_y) ? g.ny - 1 : y - 1;
-        const int yp = (y == g.ny - 1 && g.per_y) ? 0 : y + 1;
-        const int zm = (z == 0 && g.per_z) ? g.nz - 1 : z - 1;
-        const int zp = (z == g.nz - 1 && g.per_z) ? 0 : z + 1;
-        const bool xlo = xm < 0, xhi = xp >= g.nx, ylo = ym < 0, yhi = yp >= g.ny;
-        const bool zlo = zm < 0, zhi = zp >= g.nz;
-        sfor<Q>([&](auto I) {
-            constexpr int i = decltype(I)::value;
-            constexpr int cx = L::c[i][0], cy = L::c[i][1], cz = L::c[i][2];
-            const bool out = (cx > 0 && xlo) || (cx < 0 && xhi) || (cy > 0 && ylo) ||
-                             (cy < 0 && yhi) || (cz > 0 && zlo) || (cz < 0 && zhi);
-            const int sx = cx > 0 ? xm : (cx < 0 ? xp : x);
-            const int sy = cy > 0 ? ym : (cy < 0 ? yp : y);
-            const int sz = cz > 0 ? zm : (cz < 0 ? zp : z);
-            f[i] = out ? T(0) : a.fin[opp_of(i)][sz * g.plane + sy * g.pitch + sx];
-        });
-    }
-    int s = a.uniform_slot;
-    if (a.slot != nullptr) s = a.slot[(static_cast<long long>(z) * g.ny + y) * g.nx + x];
-    Cell<T, Q>::template apply<KM>(f, recipe_of<KM>(a, s));
-    if constexpr (!ODD) {
-        sfor<Q>([&](auto I) {
-            constexpr int i = decltype(I)::value;
-            a.fout[opp_of(i)][center] = f[i];
-        });
-    } else {
-        const int xm = (x == 0 && g.per_x) ? g.nx - 1 : x - 1;
-        const int xp = (x == g.nx - 1 && g.per_x) ? 0 : x + 1;
-        const int ym = (y == 0 && g.per_y) ? g.ny - 1 : y - 1;
-        const int yp = (y == g.ny - 1 && g.per_y) ? 0 : y + 1;
-        const int zm = (z == 0 && g.per_z) ? g.nz - 1 : z - 1;
-        const int zp = (z == g.nz - 1 && g.per_z) ? 0 : z + 1;
-        const bool xlo = xm < 0, xhi = xp >= g.nx, ylo = ym < 0, yhi = yp >= g.ny;
-        const bool zlo = zm < 0, zhi = zp >= g.nz;
-        sfor<Q>([&](auto I) {
-            constexpr int i = decltype(I)::value;
-            constexpr int cx = L::c[i][0], cy = L::c[i][1], cz = L::c[i][2];
-            const int dx = cx > 0 ? xp : (cx < 0 ? xm : x);
-            const int dy = cy > 0 ? yp : (cy < 0 ? ym : y);
-            const int dz = cz > 0 ? zp : (cz < 0 ? zm : z);
-            a.fout[i][dz * g.plane + dy * g.pitch + dx] = f[i];
-            if constexpr (i != 0) {
+    if (a.err != nullptr && __ldca(a.err) != 0ull) return;  // failed exchange: write nothing
+    if (x < g.nx && y < g.ny) {
+        const int center = z * g.plane + y * g.pitch + x;
+        T f[Q];
+        // (neighbour coordinates are recomputed after the collision rather
+        // than kept live across it: the fp32 BGK / TRT sets run at 40-48
+        // registers and would spill)
+        if constexpr (!ODD) {
+            sfor<Q>([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                f[i] = a.fin[i][center];
+            });
+        } else {
+            const bool lo_link = LINKED && a.push_down != nullptr && z == 0;
+            const bool hi_link = LINKED && a.push_up != nullptr && z == g.nz - 1;
+            const int xm = (x == 0 && g.per_x) ? g.nx - 1 : x - 1;
+            const int xp = (x == g.nx - 1 && g.per_x) ? 0 : x + 1;
+            const int ym = (y == 0 && g.per_y) ? g.ny - 1 : y - 1;
+            const int yp = (y == g.ny - 1 && g.per_y) ? 0 : y + 1;
+            const int zm = (z == 0 && g.per_z) ? g.nz - 1 : z - 1;
+            const int zp = (z == g.nz - 1 && g.per_z) ? 0 : z + 1;
+            const bool xlo = xm < 0, xhi = xp >= g.nx, ylo = ym < 0, yhi = yp >= g.ny;
+            const bool zlo = zm < 0 && !lo_link, zhi = zp >= g.nz && !hi_link;
+            sfor<Q>([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                constexpr int cx = L::c[i][0], cy = L::c[i][1], cz = L::c[i][2];
                 const bool out = (cx > 0 && xlo) || (cx < 0 && xhi) || (cy > 0 && ylo) ||
                                  (cy < 0 && yhi) || (cz > 0 && zlo) || (cz < 0 && zhi);
-                if (out) a.fout[i][center] = T(0);
+                const int sx = cx > 0 ? xm : (cx < 0 ? xp : x);
+                const int sy = cy > 0 ? ym : (cy < 0 ? yp : y);
+                const int sz = cz > 0 ? zm : (cz < 0 ? zp : z);
+                // across a linked face: the neighbour's pushed value in the own ghost plane
+                const bool ghost = (cz > 0 && lo_link) || (cz < 0 && hi_link);
+                f[i] = out ? T(0) : a.fin[ghost ? i : opp_of(i)][sz * g.plane + sy * g.pitch + sx];
+            });
+        }
+        int s = a.uniform_slot;
+        if (a.slot != nullptr) s = a.slot[(static_cast<long long>(z) * g.ny + y) * g.nx + x];
+        Cell<T, Q>::template apply<KM>(f, recipe_of<KM>(a, s));
+        const bool lo_link = LINKED && a.push_down != nullptr && z == 0;
+        const bool hi_link = LINKED && a.push_up != nullptr && z == g.nz - 1;
+        if constexpr (!ODD) {
+            sfor<Q>([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                a.fout[opp_of(i)][center] = f[i];
+            });
+            if (LINKED && hi_link) {
+                const int ghost = -g.plane + y * g.pitch + x;
+                sfor<Q>([&](auto I) {
+                    constexpr int i = decltype(I)::value;
+                    if constexpr (L::c[i][2] > 0) a.push_up[i * a.up_dstride + ghost] = f[i];
+                });
             }
-        });
+            if (LINKED && lo_link) {
+                const int ghost = a.down_ghost_z * g.plane + y * g.pitch + x;
+                sfor<Q>([&](auto I) {
+                    constexpr int i = decltype(I)::value;
+                    if constexpr (L::c[i][2] < 0) a.push_down[i * a.down_dstride + ghost] = f[i];
+                });
+            }
+        } else {
+            const int xm = (x == 0 && g.per_x) ? g.nx - 1 : x - 1;
+            const int xp = (x == g.nx - 1 && g.per_x) ? 0 : x + 1;
+            const int ym = (y == 0 && g.per_y) ? g.ny - 1 : y - 1;
+            const int yp = (y == g.ny - 1 && g.per_y) ? 0 : y + 1;
+            const int zm = (z == 0 && g.per_z) ? g.nz - 1 : z - 1;
+            const int zp = (z == g.nz - 1 && g.per_z) ? 0 : z + 1;
+            const bool xlo = xm < 0, xhi = xp >= g.nx, ylo = ym < 0, yhi = yp >= g.ny;
+            const bool zlo = zm < 0 && !lo_link, zhi = zp >= g.nz && !hi_link;
+            sfor<Q>([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                constexpr int cx = L::c[i][0], cy = L::c[i][1], cz = L::c[i][2];
+                const int dx = cx > 0 ? xp : (cx < 0 ? xm : x);
+                const int dy = cy > 0 ? yp : (cy < 0 ? ym : y);
+                const int dz = cz > 0 ? zp : (cz < 0 ? zm : z);
+                a.fout[i][dz * g.plane + dy * g.pitch + dx] = f[i];
+                if constexpr (LINKED && cz > 0) {
+                    if (hi_link) a.push_up[i * a.up_dstride + dy * g.pitch + dx] = f[i];
+                }
+                if constexpr (LINKED && cz < 0) {
+                    if (lo_link)
+                        a.push_down[i * a.down_dstride + (a.down_ghost_z - 1) * g.plane + dy * g.pitch + dx] = f[i];
+                }
+                if constexpr (i != 0) {
+                    const bool out = (cx > 0 && xlo) || (cx < 0 && xhi) || (cy > 0 && ylo) ||
+                                     (cy < 0 && yhi) || (cz > 0 && zlo) || (cz < 0 && zhi);
+                    if (out) a.fout[i][center] = T(0);
+                }
+            });
+        }
+    }
+    if constexpr (LINKED) {
+        if (a.counter != nullptr) signal_step(a);
     }
 }
 
@@ -1015,6 +1075,18 @@ __global__ void __launch_bounds__(NCW * 32 + 32, (NCW >= 16 ? 1 : 2))
             "k_aa_" #ODD "<" #T ",D3Q" #Q "," #KM ">[" DLB_STR(DLB_MODE) "]"                  \
     }
 #define AA_PAIR(T, Q, KM) AA_ENTRY(T, Q, KM, false), AA_ENTRY(T, Q, KM, true)
+// boundary planes of linked AA slabs (catch-all sets only: two planes per step)
+#define AA_LINK_ENTRY(T, Q, KM, ODD)                                                     \
+    KernelEntry {                                                                        \
+        int(sizeof(T) * 8), Q, unsigned(KM), ODD ? LAYOUT_AA_ODD_LINK : LAYOUT_AA_LINK,     \
+            reinterpret_cast<const void*>(&k_aa<T, Q, unsigned(KM), ODD, true>),          \
+            "k_aa_link_" #ODD "<" #T ",D3Q" #Q "," #KM ">[" DLB_STR(DLB_MODE) "]"             \
+    }
+#define AA_LINK_SET(T)                                                                    \
+    , AA_LINK_ENTRY(T, 19, KM_ALL, false), AA_LINK_ENTRY(T, 19, KM_ALL, true),            \
+        AA_LINK_ENTRY(T, 27, KM_ALL, false), AA_LINK_ENTRY(T, 27, KM_ALL, true),          \
+        AA_LINK_ENTRY(T, 19, KM_ALL | KM_XREC, false), AA_LINK_ENTRY(T, 19, KM_ALL | KM_XREC, true), \
+        AA_LINK_ENTRY(T, 27, KM_ALL | KM_XREC, false), AA_LINK_ENTRY(T, 27, KM_ALL | KM_XREC, true)
 #define AA_SET(T)                                                                         \
     AA_PAIR(T, 19, KM_BGK), AA_PAIR(T, 19, KM_TRT), AA_PAIR(T, 19, KM_RR),               \
         AA_PAIR(T, 19, KM_TRT | KM_BB | KM_MBB), AA_PAIR(T, 19, KM_ALL), AA_PAIR(T, 27, KM_RR), \
@@ -1156,7 +1228,7 @@ static const KernelEntry kTable[] = {
     LIST_SET(float, 19), LIST_SET(double, 19), LIST_SET(float, 27), LIST_SET(double, 27),
     TMA_SET, SEG_SET(float), SEG_SET(double), TMAROW_SET(float), TMAROW_SET(double) KE_SET(float) KE_SET(double)
         COOP_SET(float) COOP_SET(double) TMABLK_SET MB_SET XREC_SET(float) XREC_SET(double) SEG_MB_SET
-        SEGBB_SET(float) SEGBB_SET(double)
+        SEGBB_SET(float) SEGBB_SET(double) AA_LINK_SET(float) AA_LINK_SET(double)
 };
 
 void launch_bb_finalize(int bits, int q, void* cur, const void* prev, const Geo& g,

@@ -29,8 +29,6 @@ DeviceRun::DeviceRun(std::array<int64_t, 3> dims, std::array<bool, 3> periodic, 
                      int precision_bits, int slabs, const std::vector<int>& devices, int arith, int flags,
                      int layout)
     : dims_(dims), periodic_(periodic), q_(q), bits_(precision_bits) {
-    if (layout == DLB_LAYOUT_AA && slabs != 1)
-        throw std::invalid_argument("the AA layout runs single-slab lattices (run.blocks 1,1,1)");
     parts_ = balanced_partition(dims[2], slabs);
     for (int k = 0; k < slabs; ++k) {
         dlb_lattice_desc d{};

@@ -86,7 +86,8 @@ __device__ __forceinline__ const DevRecipe<T>& recipe_of(const StepArgs<T>& a, i
 // kernel families: dense two-population, AA even / odd, sparse lists (fluid / masked walls)
 enum Layout : int { LAYOUT_TWO_POP = 0, LAYOUT_AA = 1, LAYOUT_AA_ODD = 2, LAYOUT_LIST = 3, LAYOUT_LIST_MASKED = 4,
                     LAYOUT_TMA = 5, LAYOUT_SEG = 6, LAYOUT_TMAROW = 7,
-                    LAYOUT_COOP = 8, LAYOUT_TMABLK = 9, LAYOUT_SEGBB = 10 };
+                    LAYOUT_COOP = 8, LAYOUT_TMABLK = 9, LAYOUT_SEGBB = 10,
+                    LAYOUT_AA_LINK = 11, LAYOUT_AA_ODD_LINK = 12 };
 
 struct KernelEntry {
     int precision_bits;

@@ -43,18 +43,21 @@ __device__ __forceinline__ long long lin(const Geo& g, int x, int y, int z) {
     return static_cast<long long>(z) * g.plane + static_cast<long long>(y) * g.pitch + x;
 }
 
+// Where a fill stores canonical f_i(x, y, z) (aa_mode as canon_load: 0
+// two-population, 1 AA even layout A[opp(i)][x], 2 AA odd layout A[i][x + c_i]).
 template <int Q, int i>
-__device__ __forceinline__ long long fill_pos(const Geo& g, int x, int y, int z, bool aa) {
+__device__ __forceinline__ long long fill_pos(const Geo& g, int x, int y, int z, int aa_mode) {
     using L = Lat<Q>;
     constexpr int cx = L::c[i][0], cy = L::c[i][1], cz = L::c[i][2];
-    if (aa) return shifted(g, x, y, z, cx, cy, cz);
-    return static_cast<long long>(z) * g.plane + static_cast<long long>(y) * g.pitch + x;
+    const long long dir = aa_mode == 1 ? opp_of(i) : i;
+    if (aa_mode == 2) return i * g.dstride + shifted(g, x, y, z, cx, cy, cz);
+    return dir * g.dstride + static_cast<long long>(z) * g.plane + static_cast<long long>(y) * g.pitch + x;
 }
 
 // Stored state := equilibrium2<T>(T(rho), T(u)) for planes [z0, z0 + nzc).
 template <typename T, int Q>
 __global__ void k_fill_eq(T* origin, Geo g, const double* rho, const double* ux,
-                          const double* uy, const double* uz, int z0, int nzc, bool aa) {
+                          const double* uy, const double* uz, int z0, int nzc, int aa) {
     const long long n = static_cast<long long>(g.nx) * g.ny * nzc;
     for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
          c += (long long)gridDim.x * blockDim.x) {
@@ -66,7 +69,7 @@ __global__ void k_fill_eq(T* origin, Geo g, const double* rho, const double* ux,
         const T usqr = Cell<T, Q>::usqr_of(u);
         sfor<Q>([&](auto I) {
             constexpr int i = decltype(I)::value;
-            origin[i * g.dstride + fill_pos<Q, i>(g, x, y, z, aa)] = Cell<T, Q>::template eq2<i>(r, u, usqr);
+            origin[fill_pos<Q, i>(g, x, y, z, aa)] = Cell<T, Q>::template eq2<i>(r, u, usqr);
         });
     }
 }
@@ -75,7 +78,7 @@ __global__ void k_fill_eq(T* origin, Geo g, const double* rho, const double* ux,
 // sin / cos / cos(2x) tables (glibc, as the reference), then equilibrium2<T>.
 template <typename T, int Q>
 __global__ void k_fill_tgv(T* origin, Geo g, const double* s1, const double* c1,
-                           const double* c2, long long z_origin, double u_inf, bool aa) {
+                           const double* c2, long long z_origin, double u_inf, int aa) {
     const long long n = static_cast<long long>(g.nx) * g.ny * g.nz;
     for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
          c += (long long)gridDim.x * blockDim.x) {
@@ -92,7 +95,7 @@ __global__ void k_fill_tgv(T* origin, Geo g, const double* s1, const double* c1,
         const T usqr = Cell<T, Q>::usqr_of(u);
         sfor<Q>([&](auto I) {
             constexpr int i = decltype(I)::value;
-            origin[i * g.dstride + fill_pos<Q, i>(g, x, y, z, aa)] = Cell<T, Q>::template eq2<i>(r, u, usqr);
+            origin[fill_pos<Q, i>(g, x, y, z, aa)] = Cell<T, Q>::template eq2<i>(r, u, usqr);
         });
     }
 }
@@ -322,8 +325,6 @@ Lattice::Lattice(const dlb_lattice_desc& desc, const DynamicsRegistry& reg) : d_
         throw std::invalid_argument("precision must be 32 or 64");
     if (d_.layout != DLB_LAYOUT_TWO_POP && d_.layout != DLB_LAYOUT_AA)
         throw std::invalid_argument("layout must be DLB_LAYOUT_TWO_POP or DLB_LAYOUT_AA");
-    if (d_.layout == DLB_LAYOUT_AA && d_.global_nz != d_.dims[2])
-        throw std::invalid_argument("the AA layout runs single-slab lattices (use two-population for z-slabs)");
     if (d_.arith != DLB_ARITH_EXACT && d_.arith != DLB_ARITH_FAST)
         throw std::invalid_argument("arith must be DLB_ARITH_EXACT or DLB_ARITH_FAST");
     for (int a = 0; a < 3; ++a)
@@ -352,6 +353,7 @@ Lattice::Lattice(const dlb_lattice_desc& desc, const DynamicsRegistry& reg) : d_
         cuda_check(cudaStreamCreateWithPriority(&halo_stream_, cudaStreamNonBlocking, hi), "cudaStreamCreate");
         cuda_check(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "cudaEventCreate");
         cuda_check(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming), "cudaEventCreate");
+        cuda_check(cudaEventCreateWithFlags(&ev_wait_, cudaEventDisableTiming), "cudaEventCreate");
         trace_halo_ = std::getenv("DLB_TRACE_HALO") != nullptr;
         const char* oe = std::getenv("DLB_HALO_OVERLAP");
         overlap_ = !(oe && oe[0] == '0');
@@ -459,6 +461,7 @@ Lattice::~Lattice() {
     for (cudaEvent_t e : trace_ev_) cudaEventDestroy(e);
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_join_) cudaEventDestroy(ev_join_);
+    if (ev_wait_) cudaEventDestroy(ev_wait_);
     if (halo_stream_) cudaStreamDestroy(halo_stream_);
     if (stream_) cudaStreamDestroy(stream_);
     if (prev >= 0) cudaSetDevice(prev);
@@ -1105,6 +1108,11 @@ void Lattice::select_kernel() {
         if (kernel_ && kernel_odd_ && kernel_->km != kernel_odd_->km) kernel_odd_ = nullptr;
         if (!kernel_ || !kernel_odd_)
             throw std::invalid_argument("no AA kernel instantiation covers this dynamics set");
+        // boundary planes of linked slabs: the face-crossing instantiations
+        kernel_link_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_, LAYOUT_AA_LINK);
+        kernel_odd_link_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_, LAYOUT_AA_ODD_LINK);
+        if (!kernel_link_ || !kernel_odd_link_)
+            throw std::invalid_argument("no linked AA kernel instantiation covers this dynamics set");
         return;
     }
     kernel_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_, LAYOUT_TWO_POP);
@@ -1224,9 +1232,12 @@ void Lattice::check_dispatch() const {
 void Lattice::reset_aa() {
     envelope_valid_ = false;
     if (!aa()) return;
+    DeviceGuard dg(device_);
     const std::size_t bytes = std::size_t(d_.q) * std::size_t(geo_.dstride) * (d_.precision_bits / 8);
     cuda_check(cudaMemsetAsync(buf_[0], 0, bytes, stream_), "memset");
-    aa_odd_layout_ = true;
+    // unlinked: the odd layout (the first step is even); linked z-slabs rest
+    // in the even layout, which needs no neighbour data (k_aa)
+    aa_odd_layout_ = !(lower_.linked || upper_.linked);
 }
 
 void Lattice::fill_equilibrium(const double* rho, const double* ux, const double* uy,
@@ -1251,11 +1262,11 @@ void Lattice::fill_equilibrium(const double* rho, const double* ux, const double
         const int grid = grid_for(n);
         void* o = origin(cur_);
         if (d_.precision_bits == 64) {
-            if (d_.q == 19) k_fill_eq<double, 19><<<grid, 256, 0, stream_>>>((double*)o, geo_, st, st + n, st + 2 * n, st + 3 * n, z0, nzc, aa());
-            else k_fill_eq<double, 27><<<grid, 256, 0, stream_>>>((double*)o, geo_, st, st + n, st + 2 * n, st + 3 * n, z0, nzc, aa());
+            if (d_.q == 19) k_fill_eq<double, 19><<<grid, 256, 0, stream_>>>((double*)o, geo_, st, st + n, st + 2 * n, st + 3 * n, z0, nzc, aa_fill_mode());
+            else k_fill_eq<double, 27><<<grid, 256, 0, stream_>>>((double*)o, geo_, st, st + n, st + 2 * n, st + 3 * n, z0, nzc, aa_fill_mode());
         } else {
-            if (d_.q == 19) k_fill_eq<float, 19><<<grid, 256, 0, stream_>>>((float*)o, geo_, st, st + n, st + 2 * n, st + 3 * n, z0, nzc, aa());
-            else k_fill_eq<float, 27><<<grid, 256, 0, stream_>>>((float*)o, geo_, st, st + n, st + 2 * n, st + 3 * n, z0, nzc, aa());
+            if (d_.q == 19) k_fill_eq<float, 19><<<grid, 256, 0, stream_>>>((float*)o, geo_, st, st + n, st + 2 * n, st + 3 * n, z0, nzc, aa_fill_mode());
+            else k_fill_eq<float, 27><<<grid, 256, 0, stream_>>>((float*)o, geo_, st, st + n, st + 2 * n, st + 3 * n, z0, nzc, aa_fill_mode());
         }
         cuda_check(cudaGetLastError(), "k_fill_eq");
         cuda_check(cudaStreamSynchronize(stream_), "fill_equilibrium");
@@ -1288,11 +1299,11 @@ void Lattice::fill_uniform(double rho, double ux, double uy, double uz) {
         const int grid = grid_for(m);
         void* o = origin(cur_);
         if (d_.precision_bits == 64) {
-            if (d_.q == 19) k_fill_eq<double, 19><<<grid, 256, 0, stream_>>>((double*)o, geo_, st, st + n, st + 2 * n, st + 3 * n, z0, nzc, aa());
-            else k_fill_eq<double, 27><<<grid, 256, 0, stream_>>>((double*)o, geo_, st, st + n, st + 2 * n, st + 3 * n, z0, nzc, aa());
+            if (d_.q == 19) k_fill_eq<double, 19><<<grid, 256, 0, stream_>>>((double*)o, geo_, st, st + n, st + 2 * n, st + 3 * n, z0, nzc, aa_fill_mode());
+            else k_fill_eq<double, 27><<<grid, 256, 0, stream_>>>((double*)o, geo_, st, st + n, st + 2 * n, st + 3 * n, z0, nzc, aa_fill_mode());
         } else {
-            if (d_.q == 19) k_fill_eq<float, 19><<<grid, 256, 0, stream_>>>((float*)o, geo_, st, st + n, st + 2 * n, st + 3 * n, z0, nzc, aa());
-            else k_fill_eq<float, 27><<<grid, 256, 0, stream_>>>((float*)o, geo_, st, st + n, st + 2 * n, st + 3 * n, z0, nzc, aa());
+            if (d_.q == 19) k_fill_eq<float, 19><<<grid, 256, 0, stream_>>>((float*)o, geo_, st, st + n, st + 2 * n, st + 3 * n, z0, nzc, aa_fill_mode());
+            else k_fill_eq<float, 27><<<grid, 256, 0, stream_>>>((float*)o, geo_, st, st + n, st + 2 * n, st + 3 * n, z0, nzc, aa_fill_mode());
         }
         cuda_check(cudaGetLastError(), "k_fill_eq");
     }
@@ -1321,11 +1332,11 @@ void Lattice::fill_tgv(int64_t L, double u_inf) {
     const int grid = grid_for(cells());
     void* o = origin(cur_);
     if (d_.precision_bits == 64) {
-        if (d_.q == 19) k_fill_tgv<double, 19><<<grid, 256, 0, stream_>>>((double*)o, geo_, st, st + L, st + 2 * L, d_.z_origin, u_inf, aa());
-        else k_fill_tgv<double, 27><<<grid, 256, 0, stream_>>>((double*)o, geo_, st, st + L, st + 2 * L, d_.z_origin, u_inf, aa());
+        if (d_.q == 19) k_fill_tgv<double, 19><<<grid, 256, 0, stream_>>>((double*)o, geo_, st, st + L, st + 2 * L, d_.z_origin, u_inf, aa_fill_mode());
+        else k_fill_tgv<double, 27><<<grid, 256, 0, stream_>>>((double*)o, geo_, st, st + L, st + 2 * L, d_.z_origin, u_inf, aa_fill_mode());
     } else {
-        if (d_.q == 19) k_fill_tgv<float, 19><<<grid, 256, 0, stream_>>>((float*)o, geo_, st, st + L, st + 2 * L, d_.z_origin, u_inf, aa());
-        else k_fill_tgv<float, 27><<<grid, 256, 0, stream_>>>((float*)o, geo_, st, st + L, st + 2 * L, d_.z_origin, u_inf, aa());
+        if (d_.q == 19) k_fill_tgv<float, 19><<<grid, 256, 0, stream_>>>((float*)o, geo_, st, st + L, st + 2 * L, d_.z_origin, u_inf, aa_fill_mode());
+        else k_fill_tgv<float, 27><<<grid, 256, 0, stream_>>>((float*)o, geo_, st, st + L, st + 2 * L, d_.z_origin, u_inf, aa_fill_mode());
     }
     cuda_check(cudaGetLastError(), "k_fill_tgv");
     cuda_check(cudaStreamSynchronize(stream_), "fill_tgv");
@@ -1720,9 +1731,9 @@ void Lattice::launch_step(int parity) {
     const dim3 block(bx, by, 1);
     const unsigned gx = unsigned((geo_.nx + bx - 1) / bx);
     const unsigned gy = unsigned((geo_.ny + by - 1) / by);
-    const void* fn = kernel_->fn;
-
     const bool linked = lower_.linked || upper_.linked;
+    // AA: the state's layout picks the kernel (odd layout -> even kernel)
+    const void* fn = !aa() ? kernel_->fn : (aa_odd_layout_ ? kernel_->fn : kernel_odd_->fn);
     if (sparse_) {
         for (const ListLaunch& l : lists_) {
             const unsigned long long* lp = d_list_ + l.offset;
@@ -1735,12 +1746,11 @@ void Lattice::launch_step(int parity) {
         }
         return;
     }
-    if (aa()) {
+    if (aa() && !linked) {
         a.z_begin = 0;
         a.z_step = 1;
         void* args[] = {&a};
-        const void* kfn = aa_odd_layout_ ? kernel_->fn : kernel_odd_->fn;  // odd layout -> even kernel
-        cuda_check(cudaLaunchKernel(kfn, dim3(gx, gy, geo_.nz), block, args, 0, stream_), "launch");
+        cuda_check(cudaLaunchKernel(fn, dim3(gx, gy, geo_.nz), block, args, 0, stream_), "launch");
         aa_odd_layout_ = !aa_odd_layout_;
         return;
     }
@@ -1844,6 +1854,14 @@ void Lattice::launch_step(int parity) {
     k_halo_wait<<<1, 1, 0, hs>>>(d_flags_, lower_.linked, upper_.linked, halo_timeout_ns_);
     cuda_check(cudaGetLastError(), "k_halo_wait");
     if (tr) cuda_check(cudaEventRecord(tr[1], hs), "trace");
+    // AA updates in place: the interior launch of a step whose halo wait fails
+    // would overwrite the kept state, so it starts after the wait (the wait
+    // returns within microseconds when the neighbours keep pace); the
+    // two-population interior writes the other buffer and need not wait
+    if (aa() && overlap_) {
+        cuda_check(cudaEventRecord(ev_wait_, hs), "wait event");
+        cuda_check(cudaStreamWaitEvent(stream_, ev_wait_, 0), "wait event");
+    }
     StepArgs<T> b = a;
     b.z_begin = 0;
     b.z_step = geo_.nz > 1 ? geo_.nz - 1 : 1;
@@ -1862,7 +1880,8 @@ void Lattice::launch_step(int parity) {
     b.my_step = d_flags_ + 2;
     {
         void* args[] = {&b};
-        cuda_check(cudaLaunchKernel(fn, dim3(gx, gy, geo_.nz > 1 ? 2 : 1), block, args, 0, hs),
+        const void* bfn = !aa() ? fn : (aa_odd_layout_ ? kernel_link_->fn : kernel_odd_link_->fn);
+        cuda_check(cudaLaunchKernel(bfn, dim3(gx, gy, geo_.nz > 1 ? 2 : 1), block, args, 0, hs),
                    "launch boundary");
     }
     if (tr) cuda_check(cudaEventRecord(tr[2], hs), "trace");
@@ -1877,6 +1896,7 @@ void Lattice::launch_step(int parity) {
     }
     if (tr) cuda_check(cudaEventRecord(tr[4], stream_), "trace");
     if (overlap_) cuda_check(cudaStreamWaitEvent(stream_, ev_join_, 0), "join");
+    if (aa()) aa_odd_layout_ = !aa_odd_layout_;
 }
 
 void Lattice::enqueue_step() {
@@ -1997,13 +2017,18 @@ void Lattice::exchange() {
     };
     for (int i = 0; i < d_.q; ++i) {
         const int cz = i == 0 ? 0 : (d_.q == 19 ? kCz19[i] : kCz27[i]);
+        // AA (linked slabs rest in the even layout, f_i(x) = A[opp(i)][x]): the
+        // neighbour's odd step reads our boundary cell's f_i from its ghost slot
+        // A[i] (k_aa); in the odd layout the next step is even and reads no ghost
+        const int src = aa() ? (i == 0 ? 0 : ((i & 1) ? i + 1 : i - 1)) : i;
+        if (aa() && aa_odd_layout_) break;
         if (cz > 0 && upper_.linked)
             cuda_check(cudaMemcpyAsync(plane_ptr(upper_.buf[cur_], upper_.dstride, i, -1),
-                                       plane_ptr(origin(cur_), geo_.dstride, i, geo_.nz - 1),
+                                       plane_ptr(origin(cur_), geo_.dstride, src, geo_.nz - 1),
                                        plane_bytes, cudaMemcpyDefault, stream_), "halo exchange");
         if (cz < 0 && lower_.linked)
             cuda_check(cudaMemcpyAsync(plane_ptr(lower_.buf[cur_], lower_.dstride, i, lower_.nz),
-                                       plane_ptr(origin(cur_), geo_.dstride, i, 0),
+                                       plane_ptr(origin(cur_), geo_.dstride, src, 0),
                                        plane_bytes, cudaMemcpyDefault, stream_), "halo exchange");
     }
     cuda_check(cudaStreamSynchronize(stream_), "halo exchange");
@@ -2098,7 +2123,10 @@ void Lattice::check_error_flag() {
     const int64_t done = int64_t(fl[3]) - 1;
     const int64_t failed = halo_steps_ - done;  // enqueued linked steps that wrote nothing
     if (failed > 0) {
-        if (failed & 1) cur_ = 1 - cur_;
+        if (failed & 1) {
+            if (aa()) aa_odd_layout_ = !aa_odd_layout_;
+            else cur_ = 1 - cur_;
+        }
         steps_ -= failed;
         halo_steps_ = done;
         invalidate_graph();
@@ -2168,7 +2196,7 @@ double Lattice::time_steps(int64_t nsteps) {
 void Lattice::link_lower(Lattice& lower) {
     invalidate_graph();
     lower.invalidate_graph();
-    if (aa() || lower.aa()) throw std::invalid_argument("AA-layout lattices cannot be linked");
+    if (aa() != lower.aa()) throw std::invalid_argument("linked slabs must share the storage layout");
     // `lower` sits directly below this slab: lower's top plane feeds our ghost
     // z = -1, our bottom plane feeds lower's ghost z = lower.nz.
     if (lower.geo_.nx != geo_.nx || lower.geo_.ny != geo_.ny || lower.d_.q != d_.q ||
@@ -2200,6 +2228,10 @@ void Lattice::link_lower(Lattice& lower) {
     lower.upper_.dstride = geo_.dstride;
     lower.upper_.nz = geo_.nz;
     lower.upper_.flag = d_flags_ + 0;  // lower is our lower neighbour
+    // an AA slab's state crosses the faces in the odd layout: linking clears
+    // the state (fill / upload after linking, as MultiBlockRun does)
+    reset_aa();
+    lower.reset_aa();
 }
 
 namespace {
@@ -2207,6 +2239,7 @@ struct IpcBlob {
     uint32_t magic;
     int32_t q, bits, nx, ny, nz;
     int32_t device;
+    int32_t aa;        // storage layout (AA slabs link only to AA slabs)
     char pci_bus[32];  // the exporting slab's GPU (reported by links(): peer on another GPU or not)
     long long dstride, base_off_bytes;
     cudaIpcMemHandle_t buf[2];
@@ -2223,6 +2256,7 @@ std::vector<uint8_t> Lattice::export_ipc() const {
     b.nx = geo_.nx;
     b.ny = geo_.ny;
     b.nz = geo_.nz;
+    b.aa = int(aa());
     b.dstride = geo_.dstride;
     b.base_off_bytes = base_off_ * (d_.precision_bits / 8);
     DeviceGuard dg(device_);
@@ -2237,20 +2271,22 @@ std::vector<uint8_t> Lattice::export_ipc() const {
 
 void Lattice::link_ipc(int side, const void* blob, std::size_t len) {
     invalidate_graph();
-    if (aa()) throw std::invalid_argument("AA-layout lattices cannot be linked");
     if (len != sizeof(IpcBlob)) throw std::invalid_argument("bad IPC blob size");
     IpcBlob b;
     std::memcpy(&b, blob, sizeof(b));
     if (b.magic != kIpcMagic) throw std::invalid_argument("bad IPC blob");
     if (b.nx != geo_.nx || b.ny != geo_.ny || b.q != d_.q || b.bits != d_.precision_bits)
         throw std::invalid_argument("linked slabs must share nx, ny, q and precision");
+    if (b.aa != int(aa())) throw std::invalid_argument("linked slabs must share the storage layout");
     DeviceGuard dg(device_);
     Peer& p = side == 0 ? lower_ : upper_;
     void* bases[3];
-    for (int k = 0; k < 2; ++k)
-        cuda_check(cudaIpcOpenMemHandle(&bases[k], b.buf[k], cudaIpcMemLazyEnablePeerAccess), "ipc open");
+    // an AA slab has one population array (both handles name it): open it once
+    cuda_check(cudaIpcOpenMemHandle(&bases[0], b.buf[0], cudaIpcMemLazyEnablePeerAccess), "ipc open");
+    if (b.aa) bases[1] = bases[0];
+    else cuda_check(cudaIpcOpenMemHandle(&bases[1], b.buf[1], cudaIpcMemLazyEnablePeerAccess), "ipc open");
     cuda_check(cudaIpcOpenMemHandle(&bases[2], b.flags, cudaIpcMemLazyEnablePeerAccess), "ipc open");
-    p.ipc_opened = {bases[0], bases[1], bases[2]};
+    p.ipc_opened = b.aa ? std::vector<void*>{bases[0], bases[2]} : std::vector<void*>{bases[0], bases[1], bases[2]};
     p.linked = true;
     p.buf[0] = static_cast<char*>(bases[0]) + b.base_off_bytes;
     p.buf[1] = static_cast<char*>(bases[1]) + b.base_off_bytes;
@@ -2261,6 +2297,7 @@ void Lattice::link_ipc(int side, const void* blob, std::size_t len) {
     p.other_gpu = std::strncmp(mine, b.pci_bus, sizeof(mine)) != 0;
     // we are the peer's upper neighbour if it is our lower one, and vice versa
     p.flag = static_cast<unsigned long long*>(bases[2]) + (side == 0 ? 1 : 0);
+    reset_aa();  // see link_lower
 }
 
 // ---------------------------------------------------------------------------

@@ -152,6 +152,8 @@ class Lattice {
     void* origin(int which) const;  // interior origin of direction 0 of buffer `which`
     bool split() const { return d_.global_nz != d_.dims[2]; }
     bool aa() const { return d_.layout == DLB_LAYOUT_AA; }
+    // layout of the current state for fills / canonical access (canon_load's aa_mode)
+    int aa_fill_mode() const { return !aa() ? 0 : (aa_odd_layout_ ? 2 : 1); }
     void reset_aa();
     void check_error_flag();
 
@@ -163,6 +165,7 @@ class Lattice {
     // concurrent with the interior launch on stream_, forked / joined per step
     cudaStream_t halo_stream_ = nullptr;
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+    cudaEvent_t ev_wait_ = nullptr;       // AA: the interior launch starts after the halo wait
     unsigned long long halo_timeout_ns_ = 20ull * 1000 * 1000 * 1000;  // DLB_HALO_TIMEOUT_MS / set_halo_timeout
     bool trace_halo_ = false;             // DLB_TRACE_HALO
     bool exchange_failed_ = false;        // a timed-out halo wait was reported (cleared by exchange)
@@ -218,6 +221,8 @@ class Lattice {
     void* d_xrec_ = nullptr;     // DevRecipe<T>[instances] in global memory (xrec_)
     const KernelEntry* kernel_ = nullptr;
     const KernelEntry* kernel_odd_ = nullptr;  // AA: odd-step kernel (kernel_ is the even one)
+    const KernelEntry* kernel_link_ = nullptr;      // AA linked slabs: boundary-plane even / odd kernels
+    const KernelEntry* kernel_odd_link_ = nullptr;
     bool aa_odd_layout_ = true;                // AA: state is in the odd / upload layout
     // halo
     Peer lower_, upper_;

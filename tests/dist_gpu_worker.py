@@ -21,7 +21,9 @@ def main():
     cfg = dlb.CaseConfig(kind=kind, L=L, Re=8.0 if kind == "tgv" else 1000.0, Ma=0.1, collision=lt)
     setup = dlb.init_tgv(cfg) if kind == "tgv" else dlb.init_cavity(cfg)
     dev = int(os.environ.get("DLB_WORKER_DEVICE", "0"))
-    run = dlb.build_run(setup, precision=64 if kind == "tgv" else 32, dist=(rank, world), devices=[dev])
+    layout = os.environ.get("DLB_WORKER_LAYOUT", "twopop")
+    run = dlb.build_run(setup, precision=64 if kind == "tgv" else 32, dist=(rank, world), devices=[dev],
+                        layout=layout)
     run.advance(steps)
     run.synchronize()
     np.save(os.path.join(out_dir, f"rank{rank}.npy"), run.gather_populations())

@@ -278,6 +278,8 @@ def test_fast_arith_and_device_keys(api, tmp_path):
     ("sphere48_trt_f64", {"run.porous": "lists"}, False),
     ("tgv16_bgk_f64", {"run.layout": "aa"}, True),             # in-place AA streaming
     ("cavity16_trt_f32", {"run.layout": "aa"}, False),
+    ("tgv16_blocks_f64", {"run.layout": "aa"}, False),         # AA on 3 linked z-slabs
+    ("c1_cavity64_bgk_f64", {"run.layout": "aa"}, True),       # config 1, 8 AA z-slabs
 ])
 def test_device_variants_keep_the_reference_series(api, name, extra, dumps, tmp_path):
     """Device-runtime variants behind run.porous / run.layout: series.csv (and,

@@ -9,7 +9,9 @@
    2-slab run -- halo wait and boundary launch on the high-priority halo
    stream against the interior launch on the main stream.
 
-    python tools/overlap_probe.py [L] [--trace | --self]
+    python tools/overlap_probe.py [L] [--trace | --self] [--aa]
+
+--aa: the same measurements on AA in-place slabs (one population array).
 
 3. --self: one slab linked to itself (z wrap through its own halo protocol),
    serialised (DLB_HALO_OVERLAP=0) vs overlapped, against the unlinked slab:
@@ -27,11 +29,12 @@ from paper_2506_09242_b200 import _capi  # noqa: E402
 
 L = int(next((a for a in sys.argv[1:] if a.isdigit()), 512))
 n = 40
+LAYOUT = "aa" if "--aa" in sys.argv else "twopop"
 
 
 def step_time(slabs):
     cfg = dlb.CaseConfig(kind="tgv", L=L, Re=1600.0, Ma=0.2)
-    run = dlb.build_run(dlb.init_tgv(cfg), precision=32, slabs=slabs)
+    run = dlb.build_run(dlb.init_tgv(cfg), precision=32, slabs=slabs, layout=LAYOUT)
     run.advance(6)
     run.synchronize()
     best = 1e9
@@ -50,10 +53,12 @@ def self_linked_time(link, overlap):
     GPU, vs the same lattice with in-kernel wrap."""
     os.environ["DLB_HALO_OVERLAP"] = "1" if overlap else "0"
     cfg = dlb.CaseConfig(kind="tgv", L=L, Re=1600.0, Ma=0.2)
-    run = dlb.build_run(dlb.init_tgv(cfg), precision=32, slabs=1)
+    run = dlb.build_run(dlb.init_tgv(cfg), precision=32, slabs=1, layout=LAYOUT)
     h = run.slabs[0].handle
     if link:
         _capi.check(_capi.lib().dlb_lattice_link_local(h, h))
+        if LAYOUT == "aa":  # linking clears an AA slab's state: refill
+            run.fill_tgv(L, 0.2 / 3 ** 0.5)
         _capi.check(_capi.lib().dlb_lattice_exchange(h))
     run.advance(6)
     run.synchronize()
@@ -65,10 +70,12 @@ def self_linked_time(link, overlap):
 
 def trace(slabs=2, steps=6, self_link=False):
     cfg = dlb.CaseConfig(kind="tgv", L=L, Re=1600.0, Ma=0.2)
-    run = dlb.build_run(dlb.init_tgv(cfg), precision=32, slabs=slabs)
+    run = dlb.build_run(dlb.init_tgv(cfg), precision=32, slabs=slabs, layout=LAYOUT)
     if self_link:
         h0 = run.slabs[0].handle
         _capi.check(_capi.lib().dlb_lattice_link_local(h0, h0))
+        if LAYOUT == "aa":
+            run.fill_tgv(L, 0.2 / 3 ** 0.5)
         _capi.check(_capi.lib().dlb_lattice_exchange(h0))
     run.advance(2)
     run.synchronize()
@@ -96,7 +103,7 @@ if "--self" in sys.argv and "--trace" not in sys.argv:
         ms, cs = self_linked_time(link, overlap)
         ref = ref or ms
         same = None
-        print(json.dumps({"L": L, "self_linked": link, "overlap": overlap if link else None,
+        print(json.dumps({"L": L, "layout": LAYOUT, "self_linked": link, "overlap": overlap if link else None,
                           "ms_per_step": round(ms, 4), "mlups": round(L ** 3 / ms / 1e3),
                           "vs_unlinked": round(ms / ref, 4), "checksum0": str(cs[0])}), flush=True)
 elif "--trace" in sys.argv:
@@ -108,5 +115,5 @@ else:
     for slabs in (1, 2, 4, 8):
         dt = step_time(slabs)
         base = base or dt
-        print(json.dumps({"L": L, "slabs": slabs, "ms_per_step": round(dt * 1e3, 4),
+        print(json.dumps({"L": L, "layout": LAYOUT, "slabs": slabs, "ms_per_step": round(dt * 1e3, 4),
                           "mlups": round(L ** 3 / dt / 1e6), "vs_single": round(dt / base, 4)}), flush=True)
