@@ -43,6 +43,7 @@ UNITS = [
     ("collide_stream.cu", "collide_stream_fast.o", ["-fmad=true", "-DDLB_MODE=fast"]),
     ("lattice.cu", "lattice.o", ["-fmad=false"]),
     ("diag.cu", "diag.o", ["-fmad=false"]),
+    ("porous_compact.cu", "porous_compact.o", ["-fmad=false"]),
     ("capi.cu", "capi.o", ["-fmad=false"]),
     ("tree.cpp", "tree.o", ["-x", "cu", "-fmad=false"]),
     ("chain.cpp", "chain.o", ["-x", "cu", "-fmad=false"]),

@@ -445,6 +445,82 @@ __global__ void k_bb_finalize(T* cur, const T* prev, Geo g, const unsigned long 
     }
 }
 
+// Compacted porous sweep (single slab, non-periodic x).
+// The masked sweep (k_seg) reads the listed segments where they lie in the
+// dense layout: its isolated 32-B sectors are fetched from DRAM as 64-B pairs
+// (ncu at c4 680x600^2: 30.9 GB read for 22 GB delivered to L1) and its
+// +-1-shifted pulls straddle unlisted sectors. Here the listed segments -- and
+// the segments they pull from -- are gathered into row-major compact arrays
+// once, so consecutive listed segments are consecutive in memory and the
+// x-neighbour of any source segment is the next / previous compact segment;
+// the rows above / below come from a per-segment table of 8 compact indices.
+// Same per-cell arithmetic and stores as k_seg (bit-identical); the dense
+// layout is brought up to date (k_cmp_scatter) before the state is read.
+// FIX: the regularized inlet / outlet cells, computed with the full dispatch
+// set by a second launch on a parallel graph branch (the main sweep leaves
+// them out: same input buffer, disjoint outputs); the lean main set keeps its
+// register budget.
+template <typename T, int Q, unsigned KM, int CPT, bool FIX>
+__global__ void __launch_bounds__(256, (CPT == 1 ? min_blocks<T, Q, KM>() : 2))
+    k_cmp(const __grid_constant__ StepArgs<T> a, const __grid_constant__ CmpArgs c) {
+    using L = Lat<Q>;
+    const int G = 1 << c.gshift;
+    const long long base = static_cast<long long>(blockIdx.x) * (256 * CPT) + threadIdx.x;
+    long long li[CPT], own[CPT];
+    int lane[CPT];
+    bool ok[CPT];
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+        const long long t = base + 256 * k;
+        ok[k] = t < c.n;
+        li[k] = 0;
+        lane[k] = 0;
+        own[k] = 0;
+        if (ok[k]) {
+            long long cell = t;
+            if constexpr (FIX) cell = __ldg(c.fix + t);
+            li[k] = cell >> c.gshift;
+            lane[k] = int(cell & (G - 1));
+            const unsigned e = __ldg(c.seg + li[k]);
+            own[k] = static_cast<long long>(e & 0x03ffffffu) * G + lane[k];
+            ok[k] = lane[k] < int(e >> 26);
+        }
+    }
+    T f[CPT][Q];
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+        if (!ok[k]) continue;
+        sfor<Q>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            constexpr int cx = L::c[i][0], cy = L::c[i][1], cz = L::c[i][2];
+            long long src;
+            if constexpr (cy == 0 && cz == 0) {
+                src = own[k] - cx;
+            } else {
+                constexpr int r = cmp_row(-cy, -cz);
+                const long long m = __ldg(c.rows + r * c.nlist + li[k]);
+                src = m * G + lane[k] - cx;
+            }
+            f[k][i] = __ldg(a.fin[i] + src);
+        });
+    }
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+        if (!ok[k]) continue;
+        const int s = c.slot[own[k]];
+        if constexpr (!FIX && (KM & (KM_REGV | KM_REGP)) == 0) {
+            // regularized cells belong to the FIX launch, which runs beside
+            // this one (same input buffer, disjoint outputs)
+            if (recipe_of<KM>(a, s).has_reg) continue;
+        }
+        Cell<T, Q>::template apply<KM>(f[k], recipe_of<KM>(a, s));
+        sfor<Q>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            a.fout[i][own[k]] = f[k][i];
+        });
+    }
+}
+
 // AA-pattern in-place streaming (PAPER.md:104 future work): one
 // population array A, two alternating kernels, every location read and
 // written by the same thread (race-free in place), the same 2*q*sizeof(T)
@@ -1223,12 +1299,26 @@ __global__ void __launch_bounds__(NCW * 32 + 32, (NCW >= 16 ? 1 : 2))
 #define KE_SET(T)
 #endif
 
+#define CMP_ENTRY(T, Q, KM, CPT, FIX)                                                    \
+    KernelEntry {                                                                        \
+        int(sizeof(T) * 8), Q, unsigned(KM), FIX ? LAYOUT_CMP_FIX : LAYOUT_CMP,             \
+            reinterpret_cast<const void*>(&k_cmp<T, Q, unsigned(KM), CPT, FIX>),          \
+            "k_cmp<" #T ",D3Q" #Q "," #KM ",x" #CPT ">[" DLB_STR(DLB_MODE) "]", 0, 0, 0, CPT \
+    }
+// main sweeps of the porous dispatch sets (regularized cells via the FIX list)
+// and the fix-up / catch-all sets
+#define CMP_SET(T)                                                                        \
+    , CMP_ENTRY(T, 19, KM_TRT | KM_BB | KM_NODYN, 1, false), CMP_ENTRY(T, 19, KM_TRT | KM_BB | KM_NODYN, 2, false), \
+        CMP_ENTRY(T, 19, KM_BGK | KM_BB | KM_NODYN, 1, false), CMP_ENTRY(T, 19, KM_BGK | KM_BB | KM_NODYN, 2, false), \
+        CMP_ENTRY(T, 19, KM_RR | KM_BB | KM_NODYN, 1, false), CMP_ENTRY(T, 19, KM_ALL, 1, false),          \
+        CMP_ENTRY(T, 27, KM_ALL, 1, false), CMP_ENTRY(T, 19, KM_ALL, 1, true), CMP_ENTRY(T, 27, KM_ALL, 1, true)
+
 static const KernelEntry kTable[] = {
     Q19_SET(float), Q19_SET(double), Q27_SET(float), Q27_SET(double), AA_SET(float), AA_SET(double),
     LIST_SET(float, 19), LIST_SET(double, 19), LIST_SET(float, 27), LIST_SET(double, 27),
     TMA_SET, SEG_SET(float), SEG_SET(double), TMAROW_SET(float), TMAROW_SET(double) KE_SET(float) KE_SET(double)
         COOP_SET(float) COOP_SET(double) TMABLK_SET MB_SET XREC_SET(float) XREC_SET(double) SEG_MB_SET
-        SEGBB_SET(float) SEGBB_SET(double) AA_LINK_SET(float) AA_LINK_SET(double)
+        SEGBB_SET(float) SEGBB_SET(double) AA_LINK_SET(float) AA_LINK_SET(double) CMP_SET(float) CMP_SET(double)
 };
 
 void launch_bb_finalize(int bits, int q, void* cur, const void* prev, const Geo& g,

@@ -76,6 +76,26 @@ struct StepArgs {
     const DevRecipe<T>* xrec;
 };
 
+// Compacted porous sweep (k_cmp): the populations of the listed skip segments
+// (and of the never-updated segments they pull from) stored contiguously in
+// row-major segment order, G = 1 << gshift cells per segment. Segment m's cell
+// `lane` of direction i sits at fin[i][m * G + lane]; because the order is
+// row-major, the x-neighbour segments of a source segment are m - 1 / m + 1.
+struct CmpArgs {
+    const unsigned* seg;    // per listed segment: compact index | (valid lanes << 26)
+    const unsigned* rows;   // [8][nlist]: compact index of the same-x segment in row (y + dy, z + dz)
+    const uint8_t* slot;    // per compact cell: registry slot
+    const unsigned* fix;    // k_cmp FIX variant: listed cells (listed segment << gshift | lane)
+    long long n;            // threads (cells) of the launch
+    long long nlist;        // listed segments
+    int gshift;
+};
+
+// Row-table index of the row offset (dy, dz) != (0, 0).
+__host__ __device__ constexpr int cmp_row(int dy, int dz) {
+    return (dz + 1) * 3 + (dy + 1) - (((dz + 1) * 3 + (dy + 1)) > 4 ? 1 : 0);
+}
+
 // Recipe of slot s as the instantiation reads it.
 template <unsigned KM, typename T>
 __device__ __forceinline__ const DevRecipe<T>& recipe_of(const StepArgs<T>& a, int s) {
@@ -87,7 +107,7 @@ __device__ __forceinline__ const DevRecipe<T>& recipe_of(const StepArgs<T>& a, i
 enum Layout : int { LAYOUT_TWO_POP = 0, LAYOUT_AA = 1, LAYOUT_AA_ODD = 2, LAYOUT_LIST = 3, LAYOUT_LIST_MASKED = 4,
                     LAYOUT_TMA = 5, LAYOUT_SEG = 6, LAYOUT_TMAROW = 7,
                     LAYOUT_COOP = 8, LAYOUT_TMABLK = 9, LAYOUT_SEGBB = 10,
-                    LAYOUT_AA_LINK = 11, LAYOUT_AA_ODD_LINK = 12 };
+                    LAYOUT_AA_LINK = 11, LAYOUT_AA_ODD_LINK = 12, LAYOUT_CMP = 13, LAYOUT_CMP_FIX = 14 };
 
 struct KernelEntry {
     int precision_bits;

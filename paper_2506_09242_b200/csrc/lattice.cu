@@ -362,6 +362,11 @@ Lattice::Lattice(const dlb_lattice_desc& desc, const DynamicsRegistry& reg) : d_
     }
     cuda_check(cudaEventCreate(&ev0_), "cudaEventCreate");
     cuda_check(cudaEventCreate(&ev1_), "cudaEventCreate");
+    if (const char* fg = std::getenv("DLB_L2_FETCH")) {
+        // L2 fetch granularity hint (bytes; tuning experiment for the sector-
+        // scattered porous sweep)
+        cuda_check(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, std::size_t(std::atoi(fg))), "L2 fetch limit");
+    }
 
     const int s = d_.precision_bits / 8;
     align_ = 128 / s;
@@ -447,6 +452,7 @@ Lattice::~Lattice() {
     cudaFree(d_fix_);
     cudaFree(d_tmap_);
     cudaFree(d_xrec_);
+    free_compact();
     cudaFree(d_flags_);
     cudaFree(d_counter_);
     cudaFree(staging_);
@@ -490,6 +496,7 @@ int64_t Lattice::step_bytes() const {
 int Lattice::launches_per_step() const {
     if (sparse_) return int(lists_.size());
     const bool linked = lower_.linked || upper_.linked;
+    if (kernel_cmp_ && !linked) return 1 + (kernel_cmp_fix_ ? 1 : 0);
     if (!linked) return 1 + ((kernel_main_ && !fixups_.empty()) ? int(fixups_.size()) : 0);
     return 1 + 1 + (geo_.nz > 2 ? 1 : 0);  // wait + boundary + interior
 }
@@ -531,6 +538,7 @@ void Lattice::set_slots(const int32_t* slots) {
     cudaFree(d_slot_);
     d_slot_ = nullptr;
     masked_cells_ = -1;
+    free_compact();
     if ((d_.flags & (DLB_FLAG_SKIP_NODYNAMICS | DLB_FLAG_SPARSE_LISTS)) && !aa()) {
         // cells the masked sweep moves: x-aligned groups of skip_group_ cells
         // that hold at least one non-NoDynamics cell (k_pull KM_SKIP rule)
@@ -567,6 +575,7 @@ void Lattice::set_slots(const int32_t* slots) {
                        "upload segments");
             nseg_ = (long long)segs.size();
             build_fluid_segments(u8);
+            build_compact(u8, nodyn);
         } else {
             build_fluid_segments({});
         }
@@ -657,6 +666,7 @@ void Lattice::build_fluid_segments(const std::vector<uint8_t>& u8) {
     d_bbfin_ = nullptr;
     nfseg_ = nbbfin_ = fseg_cells_ = 0;
     bb_prologue_ = true;
+    cmp_valid_ = false;
     bb_dirty_ = false;
     // opt-in (DLB_FLUID_SEGMENTS=1): on c4 it writes 23 % fewer bytes but reads
     // 15 % more (the puller's own previous sector for every wall link), for the
@@ -763,6 +773,7 @@ void Lattice::build_fluid_segments(const std::vector<uint8_t>& u8) {
 // Bring the wall cells the fluid-segment sweep skipped up to date (their
 // collision-facing links) before anything reads the state.
 void Lattice::finalize_walls() {
+    scatter_compact();
     if (!bb_dirty_) return;
     DeviceGuard dg(device_);
     exact::launch_bb_finalize(d_.precision_bits, d_.q, origin(cur_), origin(1 - cur_), geo_, d_bbfin_, nbbfin_,
@@ -1151,6 +1162,32 @@ void Lattice::select_kernel() {
                     kernel_seg_ = &t[k];
         }
     }
+    kernel_cmp_ = kernel_cmp_fix_ = nullptr;
+    if (kernel_seg_ && d_cseg_) {
+        // compacted sweep: the main set without the regularized kinds (they run
+        // as the FIX list with the full set), cells per thread as k_seg
+        unsigned km = km_needed_ & ~KM_SKIP;
+        const bool reg = (km & (KM_REGV | KM_REGP)) != 0;
+        if (reg) km &= ~(KM_REGV | KM_REGP);
+        const int cpt = kernel_seg_->cpt;
+        int nt = 0;
+        const KernelEntry* t = d_.arith == DLB_ARITH_FAST ? fast::kernel_table(&nt) : exact::kernel_table(&nt);
+        const KernelEntry* best = nullptr;
+        for (int k = 0; k < nt; ++k) {
+            const KernelEntry& e = t[k];
+            if (e.layout != LAYOUT_CMP || e.precision_bits != d_.precision_bits || e.q != d_.q) continue;
+            if ((e.km & km) != km || (e.km & KM_XREC)) continue;
+            const bool better = !best || __builtin_popcount(e.km) < __builtin_popcount(best->km) ||
+                                (__builtin_popcount(e.km) == __builtin_popcount(best->km) && e.cpt == cpt);
+            if (better) best = &e;
+        }
+        const KernelEntry* fix = reg ? find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_ & ~KM_SKIP,
+                                                   LAYOUT_CMP_FIX) : nullptr;
+        if (best && (!reg || (fix && ncfix_ > 0))) {
+            kernel_cmp_ = best;
+            kernel_cmp_fix_ = reg ? fix : nullptr;
+        }
+    }
     kernel_segbb_ = nullptr;
     if (kernel_seg_ && d_fseg_) {
         int nt = 0;
@@ -1243,6 +1280,7 @@ void Lattice::reset_aa() {
 void Lattice::fill_equilibrium(const double* rho, const double* ux, const double* uy,
                                const double* uz) {
     bb_prologue_ = true;
+    cmp_valid_ = false;
     bb_dirty_ = false;
     envelope_valid_ = false;
     DeviceGuard dg(device_);
@@ -1277,6 +1315,7 @@ void Lattice::fill_equilibrium(const double* rho, const double* ux, const double
 // fill with constant staging arrays (same k_fill_eq arithmetic).
 void Lattice::fill_uniform(double rho, double ux, double uy, double uz) {
     bb_prologue_ = true;
+    cmp_valid_ = false;
     bb_dirty_ = false;
     const long long plane_cells = (long long)geo_.nx * geo_.ny;
     const int zc = int(std::max<long long>(1, std::min<long long>(geo_.nz, (long long)(staging_bytes_ / 32) / plane_cells)));
@@ -1312,6 +1351,7 @@ void Lattice::fill_uniform(double rho, double ux, double uy, double uz) {
 
 void Lattice::fill_tgv(int64_t L, double u_inf) {
     bb_prologue_ = true;
+    cmp_valid_ = false;
     bb_dirty_ = false;
     if (d_.dims[0] != L || d_.dims[1] != L || d_.global_nz != L)
         throw std::invalid_argument("TGV fill needs an L^3 domain");
@@ -1350,6 +1390,7 @@ void Lattice::copy_canonical(void* host, bool to_device, bool as_double, int ele
         reset_aa();
         envelope_valid_ = false;
         bb_prologue_ = true;
+        cmp_valid_ = false;
         bb_dirty_ = false;
     } else {
         finalize_walls();
@@ -1407,6 +1448,7 @@ void Lattice::download_raw(void* canon) {
 // box of every direction, including the envelope the caller refreshed.
 void Lattice::upload_block(const void* f, const int64_t ext[3]) {
     bb_prologue_ = true;
+    cmp_valid_ = false;
     bb_dirty_ = false;
     envelope_valid_ = false;
     DeviceGuard dg(device_);
@@ -1764,6 +1806,30 @@ void Lattice::launch_step(int parity) {
         a.z_step = 1;
         void* args[] = {&a};
         const bool split_rare = kernel_main_ != nullptr && !fixups_.empty();
+        if (kernel_cmp_) {
+            // compacted porous sweep (+ the regularized cells with the full set)
+            prepare_compact();
+            StepArgs<T> c = a;
+            for (int i = 0; i < d_.q; ++i) {
+                c.fin[i] = static_cast<const T*>(cbuf_[parity]) + i * cstride_;
+                c.fout[i] = static_cast<T*>(cbuf_[1 - parity]) + i * cstride_;
+            }
+            c.slot = nullptr;
+            CmpArgs ca{d_cseg_, d_crows_, d_cslot_, d_cfix_, ncl_ << cgshift_, ncl_, cgshift_};
+            void* cargs[] = {&c, &ca};
+            const long long per_block = 256LL * kernel_cmp_->cpt;
+            cuda_check(cudaLaunchKernel(kernel_cmp_->fn, dim3(unsigned((ca.n + per_block - 1) / per_block)),
+                                        dim3(256), cargs, 0, stream_), "launch compact");
+            if (kernel_cmp_fix_) {
+                // (as a parallel high-priority branch it slowed the main sweep:
+                // 10.06 vs 9.65 ms per c4 step, profiles/r02b_summary.md)
+                ca.n = ncfix_;
+                cuda_check(cudaLaunchKernel(kernel_cmp_fix_->fn, dim3(unsigned((ca.n + 255) / 256)), dim3(256),
+                                            cargs, 0, stream_), "launch compact fix-up");
+            }
+            cmp_dirty_ = true;
+            return;
+        }
         if (kernel_segbb_ && !bb_prologue_) {
             // fluid-segment sweep: wall cells outside the listed segments skip
             const unsigned* sp = d_fseg_;
@@ -1914,6 +1980,7 @@ void Lattice::invalidate_graph() {
 
 void Lattice::ensure_graph() {
     if (graph_) return;
+    prepare_compact();  // the gather stays out of the replayed graph
     if (kernel_tma_ && !envelope_valid_ && !(lower_.linked || upper_.linked)) {
         refresh_envelope(cur_);  // keep the one-off refresh out of the replayed graph
         envelope_valid_ = true;
@@ -1921,7 +1988,7 @@ void Lattice::ensure_graph() {
     const int cur = cur_;
     const bool odd = aa_odd_layout_;
     const int64_t steps = steps_, halo_steps = halo_steps_;
-    const bool bb_dirty = bb_dirty_, bb_prologue = bb_prologue_;
+    const bool bb_dirty = bb_dirty_, bb_prologue = bb_prologue_, cmp_dirty = cmp_dirty_;
     cudaGraph_t g = nullptr;
     cuda_check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "begin capture");
     enqueue_step();
@@ -1933,6 +2000,7 @@ void Lattice::ensure_graph() {
     halo_steps_ = halo_steps;
     bb_dirty_ = bb_dirty;
     bb_prologue_ = bb_prologue;
+    cmp_dirty_ = cmp_dirty;
     // keep the halo branch's stream priority inside the replayed graph
     cuda_check(cudaGraphInstantiateWithFlags(&graph_, g, cudaGraphInstantiateFlagUseNodePriority),
                "graph instantiate");
@@ -1980,6 +2048,7 @@ void Lattice::step(int64_t nsteps) {
             steps_ += 2;
             if (lower_.linked || upper_.linked) halo_steps_ += 2;
             if (kernel_segbb_) bb_dirty_ = true;
+            if (kernel_cmp_) cmp_dirty_ = true;
         }
     }
     for (; k < nsteps; ++k) enqueue_step();

@@ -119,6 +119,7 @@ class Lattice {
     int launches_per_step() const;
     const char* kernel_name() const {
         if (kernel_tma_ && !(lower_.linked || upper_.linked)) return kernel_tma_->name;
+        if (kernel_cmp_ && !(lower_.linked || upper_.linked)) return kernel_cmp_->name;
         if (kernel_segbb_ && !(lower_.linked || upper_.linked)) return kernel_segbb_->name;
         if (kernel_seg_ && !(lower_.linked || upper_.linked)) return kernel_seg_->name;
         if (kernel_main_ && !fixups_.empty() && !(lower_.linked || upper_.linked)) return kernel_main_->name;
@@ -190,6 +191,27 @@ class Lattice {
     bool bb_dirty_ = false;    // wall cells outside the fluid segments are behind the state
     void build_fluid_segments(const std::vector<uint8_t>& u8);
     void finalize_walls();
+    // compacted porous sweep (k_cmp, porous_compact.cu): listed segments and the
+    // segments they pull from, gathered into row-major compact arrays
+    void* cbuf_[2] = {nullptr, nullptr};
+    long long cstride_ = 0;                        // elements per compact direction array
+    long long ncomp_ = 0, ncl_ = 0, ncfix_ = 0;    // compact segments, listed segments, fix-up cells
+    int cgshift_ = 0;
+    unsigned* d_cseg_ = nullptr;    // listed segment -> compact index | valid lanes << 26
+    unsigned* d_crows_ = nullptr;   // [8][ncl_] compact index of the same-x segment in the neighbouring rows
+    long long* d_coff_ = nullptr;   // compact segment -> dense offset of its first cell
+    int* d_cx0_ = nullptr;          // compact segment -> x of its first cell
+    uint8_t* d_cslot_ = nullptr;    // per compact cell
+    unsigned* d_cfix_ = nullptr;    // regularized cells (listed segment << gshift | lane)
+    const KernelEntry* kernel_cmp_ = nullptr;
+    const KernelEntry* kernel_cmp_fix_ = nullptr;
+    bool cmp_valid_ = false;        // the compact arrays hold the current state
+    bool cmp_dirty_ = false;        // the dense layout is behind them
+    int64_t cmp_bytes_ = 0;
+    void build_compact(const std::vector<uint8_t>& u8, const std::vector<uint8_t>& nodyn);
+    void free_compact();
+    void prepare_compact();   // gather before the first compact step after a state write
+    void scatter_compact();   // dense layout up to date (before reads)
     // fused kinetic energy (KM_KE variant): per-cell values of the state after
     // step ke_step_, consumed by the next DLB_Q_KINETIC reduction
     const KernelEntry* kernel_ke_ = nullptr;
