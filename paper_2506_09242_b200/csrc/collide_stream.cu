@@ -241,6 +241,103 @@ __global__ void __launch_bounds__(256, (MINB ? MINB : min_blocks<T, Q, KM>()))
 }
 
 
+// 128-bit vectorised dense sweep (opt-in, DLB_VEC=1; BASELINE north_star:
+// "coalesced, vectorised 128-bit HBM loads and stores"). Each thread owns
+// VW = 16 / sizeof(T) x-consecutive cells (4 fp32 / 2 fp64): per direction
+// one aligned 128-bit load of its own x-range in the source row; the +-1
+// x-shifted directions take the missing element from the neighbouring lane
+// (warp shuffle) or, at a warp's edge, one scalar load; one aligned 128-bit
+// store per direction. Per-cell arithmetic as k_pull (bit-identical). Single
+// slabs, nx % VW == 0, plain dispatch sets (no halo push / fused reduce).
+template <typename T>
+struct Vec16;
+template <>
+struct Vec16<float> {
+    using type = float4;
+    static constexpr int n = 4;
+};
+template <>
+struct Vec16<double> {
+    using type = double2;
+    static constexpr int n = 2;
+};
+
+template <typename T, int Q, unsigned KM>
+__global__ void __launch_bounds__(256, 2) k_vec(const __grid_constant__ StepArgs<T> a) {
+    using L = Lat<Q>;
+    using V = typename Vec16<T>::type;
+    constexpr int VW = Vec16<T>::n;
+    const Geo& g = a.g;
+    const unsigned lane = threadIdx.x & 31u;
+    const int xv = int(blockIdx.x * blockDim.x + threadIdx.x) * VW;
+    const int y = int(blockIdx.y * blockDim.y + threadIdx.y);
+    const int z = a.z_begin + int(blockIdx.z) * a.z_step;
+    const bool active = xv < g.nx && y < g.ny;
+    // inactive lanes of a partial warp still join the shuffles (clamped loads)
+    const int x0 = active ? xv : (xv < g.nx ? xv : g.nx - VW);
+    const int yc = y < g.ny ? y : g.ny - 1;
+    const int ym = (yc == 0 && g.per_y) ? g.ny - 1 : yc - 1;
+    const int yp = (yc == g.ny - 1 && g.per_y) ? 0 : yc + 1;
+    const int zm = (z == 0 && g.per_z) ? g.nz - 1 : z - 1;
+    const int zp = (z == g.nz - 1 && g.per_z) ? 0 : z + 1;
+    // the element left of x0 / right of the x-range (warp edges, row ends)
+    const int xl = (x0 == 0 && g.per_x) ? g.nx - 1 : x0 - 1;
+    const int xr = (x0 + VW == g.nx && g.per_x) ? 0 : x0 + VW;
+    const unsigned full = 0xffffffffu;
+    // lanes whose neighbour lane does not hold the adjacent x-range
+    const bool own_left = lane == 0 || x0 == 0;
+    const bool own_right = lane == 31 || x0 + VW >= g.nx;
+    T f[VW][Q];
+    sfor<Q>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        constexpr int cx = L::c[i][0], cy = L::c[i][1], cz = L::c[i][2];
+        const int sy = cy > 0 ? ym : (cy < 0 ? yp : yc);
+        const int sz = cz > 0 ? zm : (cz < 0 ? zp : z);
+        const T* row = a.fin[i] + (sz * g.plane + sy * g.pitch);
+        const V v = __ldg(reinterpret_cast<const V*>(row + x0));
+        T e[VW];
+        if constexpr (VW == 4) {
+            e[0] = v.x; e[1] = v.y; e[2] = v.z; e[3] = v.w;
+        } else {
+            e[0] = v.x; e[1] = v.y;
+        }
+        if constexpr (cx == 0) {
+#pragma unroll
+            for (int c = 0; c < VW; ++c) f[c][i] = e[c];
+        } else if constexpr (cx > 0) {  // f_i(x) <- f_i(x - 1)
+            T left = __shfl_up_sync(full, e[VW - 1], 1);
+            if (own_left) left = __ldg(row + xl);
+            f[0][i] = left;
+#pragma unroll
+            for (int c = 1; c < VW; ++c) f[c][i] = e[c - 1];
+        } else {  // f_i(x) <- f_i(x + 1)
+            T right = __shfl_down_sync(full, e[0], 1);
+            if (own_right) right = __ldg(row + xr);
+#pragma unroll
+            for (int c = 0; c < VW - 1; ++c) f[c][i] = e[c + 1];
+            f[VW - 1][i] = right;
+        }
+    });
+    if (!active) return;
+    const long long cell0 = (static_cast<long long>(z) * g.ny + y) * g.nx + x0;
+#pragma unroll
+    for (int c = 0; c < VW; ++c) {
+        const int s = a.slot != nullptr ? a.slot[cell0 + c] : a.uniform_slot;
+        Cell<T, Q>::template apply<KM>(f[c], recipe_of<KM>(a, s));
+    }
+    const int center = z * g.plane + y * g.pitch + x0;
+    sfor<Q>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        V v;
+        if constexpr (VW == 4) {
+            v.x = f[0][i]; v.y = f[1][i]; v.z = f[2][i]; v.w = f[3][i];
+        } else {
+            v.x = f[0][i]; v.y = f[1][i];
+        }
+        *reinterpret_cast<V*>(a.fout[i] + center) = v;
+    });
+}
+
 // Persistent multi-step sweep for small lattices (cooperative launch): the
 // whole grid stays resident for nsteps steps, each thread walks its cells
 // (grid stride), then grid-wide barrier and the buffers swap roles. For a
@@ -1319,12 +1416,23 @@ __global__ void __launch_bounds__(NCW * 32 + 32, (NCW >= 16 ? 1 : 2))
         CMP_ENTRY(T, 19, KM_RR | KM_BB | KM_NODYN, 1, false), CMP_ENTRY(T, 19, KM_ALL, 1, false),          \
         CMP_ENTRY(T, 27, KM_ALL, 1, false), CMP_ENTRY(T, 19, KM_ALL, 1, true), CMP_ENTRY(T, 27, KM_ALL, 1, true)
 
+#define VEC_ENTRY(T, Q, KM)                                                              \
+    KernelEntry {                                                                        \
+        int(sizeof(T) * 8), Q, unsigned(KM), LAYOUT_VEC,                                  \
+            reinterpret_cast<const void*>(&k_vec<T, Q, unsigned(KM)>),                    \
+            "k_vec<" #T ",D3Q" #Q "," #KM ">[" DLB_STR(DLB_MODE) "]"                       \
+    }
+#define VEC_SET(T)                                                                        \
+    , VEC_ENTRY(T, 19, KM_BGK), VEC_ENTRY(T, 19, KM_TRT), VEC_ENTRY(T, 19, KM_TRT | KM_BB | KM_MBB), \
+        VEC_ENTRY(T, 19, KM_BGK | KM_BB | KM_MBB), VEC_ENTRY(T, 27, KM_RR)
+
 static const KernelEntry kTable[] = {
     Q19_SET(float), Q19_SET(double), Q27_SET(float), Q27_SET(double), AA_SET(float), AA_SET(double),
     LIST_SET(float, 19), LIST_SET(double, 19), LIST_SET(float, 27), LIST_SET(double, 27),
     TMA_SET, SEG_SET(float), SEG_SET(double), TMAROW_SET(float), TMAROW_SET(double) KE_SET(float) KE_SET(double)
         COOP_SET(float) COOP_SET(double) TMABLK_SET MB_SET XREC_SET(float) XREC_SET(double) SEG_MB_SET
         SEGBB_SET(float) SEGBB_SET(double) AA_LINK_SET(float) AA_LINK_SET(double) CMP_SET(float) CMP_SET(double)
+        VEC_SET(float) VEC_SET(double)
 };
 
 void launch_bb_finalize(int bits, int q, void* cur, const void* prev, const Geo& g,

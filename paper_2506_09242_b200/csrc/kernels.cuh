@@ -107,7 +107,8 @@ __device__ __forceinline__ const DevRecipe<T>& recipe_of(const StepArgs<T>& a, i
 enum Layout : int { LAYOUT_TWO_POP = 0, LAYOUT_AA = 1, LAYOUT_AA_ODD = 2, LAYOUT_LIST = 3, LAYOUT_LIST_MASKED = 4,
                     LAYOUT_TMA = 5, LAYOUT_SEG = 6, LAYOUT_TMAROW = 7,
                     LAYOUT_COOP = 8, LAYOUT_TMABLK = 9, LAYOUT_SEGBB = 10,
-                    LAYOUT_AA_LINK = 11, LAYOUT_AA_ODD_LINK = 12, LAYOUT_CMP = 13, LAYOUT_CMP_FIX = 14 };
+                    LAYOUT_AA_LINK = 11, LAYOUT_AA_ODD_LINK = 12, LAYOUT_CMP = 13, LAYOUT_CMP_FIX = 14,
+                    LAYOUT_VEC = 15 };
 
 struct KernelEntry {
     int precision_bits;

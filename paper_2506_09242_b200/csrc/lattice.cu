@@ -1215,6 +1215,15 @@ void Lattice::select_kernel() {
         if (cells() <= maxc && !aa() && !split() && fixups_.empty() && !(km_needed_ & KM_SKIP))
             kernel_coop_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_, LAYOUT_COOP);
     }
+    // 128-bit vectorised dense sweep (opt-in): unlinked single slabs whose rows
+    // hold whole 16-B vectors, plain dispatch sets
+    kernel_vec_ = nullptr;
+    if (const char* ve = std::getenv("DLB_VEC")) {
+        const int vw = 16 / (d_.precision_bits / 8);
+        if (ve[0] == '1' && !aa() && !split() && fixups_.empty() && !(km_needed_ & (KM_SKIP | KM_XREC)) &&
+            geo_.nx % vw == 0)
+            kernel_vec_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_, LAYOUT_VEC);
+    }
     kernel_tma_ = nullptr;
     tma_grid_ = 0;
     if (tma_ok_ && fixups_.empty() && !(km_needed_ & KM_SKIP)) {
@@ -1868,6 +1877,11 @@ void Lattice::launch_step(int parity) {
                        "launch fused kinetic energy");
             ke_requested_ = false;
             ke_step_ = steps_ + 1;  // valid for the state after this step
+        } else if (kernel_vec_ && !split_rare) {
+            const int vw = 16 / int(sizeof(T));
+            const unsigned vx = unsigned((geo_.nx / vw + 63) / 64), vy = unsigned((geo_.ny + 3) / 4);
+            cuda_check(cudaLaunchKernel(kernel_vec_->fn, dim3(vx, vy, geo_.nz), dim3(64, 4, 1), args, 0, stream_),
+                       "launch vectorised");
         } else {
             cuda_check(cudaLaunchKernel(split_rare ? kernel_main_->fn : fn, dim3(gx, gy, geo_.nz), block, args, 0,
                                         stream_), "launch");

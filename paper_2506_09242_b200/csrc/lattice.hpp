@@ -120,6 +120,7 @@ class Lattice {
     const char* kernel_name() const {
         if (kernel_tma_ && !(lower_.linked || upper_.linked)) return kernel_tma_->name;
         if (kernel_cmp_ && !(lower_.linked || upper_.linked)) return kernel_cmp_->name;
+        if (kernel_vec_ && !(lower_.linked || upper_.linked)) return kernel_vec_->name;
         if (kernel_segbb_ && !(lower_.linked || upper_.linked)) return kernel_segbb_->name;
         if (kernel_seg_ && !(lower_.linked || upper_.linked)) return kernel_seg_->name;
         if (kernel_main_ && !fixups_.empty() && !(lower_.linked || upper_.linked)) return kernel_main_->name;
@@ -203,6 +204,7 @@ class Lattice {
     int* d_cx0_ = nullptr;          // compact segment -> x of its first cell
     uint8_t* d_cslot_ = nullptr;    // per compact cell
     unsigned* d_cfix_ = nullptr;    // regularized cells (listed segment << gshift | lane)
+    const KernelEntry* kernel_vec_ = nullptr;  // 128-bit vectorised dense sweep (DLB_VEC=1)
     const KernelEntry* kernel_cmp_ = nullptr;
     const KernelEntry* kernel_cmp_fix_ = nullptr;
     bool cmp_valid_ = false;        // the compact arrays hold the current state

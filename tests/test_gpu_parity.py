@@ -626,3 +626,45 @@ def test_fluid_segment_sweep_restarts_after_upload(oracle, monkeypatch):
     active = np.asarray(setup.chain_index).reshape(-1) != 2
     got = run.gather_populations().reshape(19, -1)
     assert np.array_equal(got[:, active], f.reshape(19, -1)[:, active])
+
+
+# ---------------------------------------------------------------- 128-bit vectorised sweep
+@pytest.mark.parametrize("name", ["tgv16_bgk_f64", "cavity32_trt_f32", "cavity64_bgk_f64_c1"])
+def test_vectorised_sweep_bit_identical_to_reference(golden, name, monkeypatch):
+    """k_vec (DLB_VEC=1): one 128-bit load / store per direction and thread
+    (4 fp32 or 2 fp64 cells), +-1 x shifts through warp shuffles; same per-cell
+    arithmetic as k_pull, so the reference's goldens hold bit for bit."""
+    monkeypatch.setenv("DLB_VEC", "1")
+    setup, bits, steps = product_setup(CASES[name])
+    run = dlb.build_run(setup, precision=bits)
+    assert "k_vec" in run.kernel_name(), run.kernel_name()
+    run.advance(steps)
+    assert canonical_hash(run.gather_populations()) == golden[name]["sha256"]
+
+
+@pytest.mark.parametrize("dims,periodic", [((36, 7, 5), (1, 1, 1)), ((40, 9, 6), (0, 1, 0)), ((8, 3, 3), (1, 0, 1))])
+@pytest.mark.parametrize("bits", [32, 64])
+def test_vectorised_sweep_ragged_vs_oracle(oracle, dims, periodic, bits, monkeypatch):
+    """Rows of 2-10 vectors, partial warps and blocks, periodic / walled x."""
+    monkeypatch.setenv("DLB_VEC", "1")
+    reg = dlb.DynamicsRegistry()
+    p = dlb.CollisionParams()
+    p.set_trt(1.3, 0.25)
+    s = reg.register_chain(dlb.make_collision_chain(LinkType.TRT, p))
+    run = dlb.DeviceRun(dims, periodic, reg, precision=bits)
+    run.fill_slots(s)
+    rng = np.random.default_rng(sum(dims) + bits)
+    n = dims[0] * dims[1] * dims[2]
+    f0 = rng.normal(0.0, 1e-3, 19 * n)
+    if bits == 32:
+        f0 = f0.astype(np.float32).astype(np.float64)
+    run.upload_populations(f0)
+    assert "k_vec" in run.kernel_name()
+    run.advance(5)
+    monkeypatch.setenv("DLB_VEC", "0")
+    ref2 = dlb.DeviceRun(dims, periodic, reg, precision=bits)
+    ref2.fill_slots(s)
+    ref2.upload_populations(f0)
+    ref2.advance(5)
+    assert "k_vec" not in ref2.kernel_name()
+    assert np.array_equal(run.gather_populations(), ref2.gather_populations())
