@@ -497,6 +497,7 @@ int Lattice::launches_per_step() const {
     if (sparse_) return int(lists_.size());
     const bool linked = lower_.linked || upper_.linked;
     if (kernel_cmp_ && !linked) return 1 + (kernel_cmp_fix_ ? 1 : 0);
+    if (kernel_seg_ && seg_fused_reg_ && !linked) return 1;
     if (!linked) return 1 + ((kernel_main_ && !fixups_.empty()) ? int(fixups_.size()) : 0);
     return 1 + 1 + (geo_.nz > 2 ? 1 : 0);  // wait + boundary + interior
 }
@@ -1142,9 +1143,19 @@ void Lattice::select_kernel() {
         kernel_main_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_ & ~(KM_REGV | KM_REGP),
                                    LAYOUT_TWO_POP);
     kernel_seg_ = nullptr;
+    seg_fused_reg_ = false;
     if (d_seg_ && (km_needed_ & KM_SKIP)) {
         unsigned km = km_needed_ & ~KM_SKIP;
-        if (kernel_main_) km &= ~(KM_REGV | KM_REGP);
+        // the regularized cells stay in the segment sweep when it runs two
+        // cells per thread (fp64): that instantiation has the same 126
+        // registers with or without them, and the separate fix-up launches
+        // re-read every source line of those isolated cells
+        const char* fr = std::getenv("DLB_SEG_FUSE_REG");
+        const char* ce0 = std::getenv("DLB_SEG_CPT");
+        const int cpt0 = ce0 ? std::atoi(ce0) : (d_.precision_bits == 64 ? 2 : 1);
+        const char* fs = std::getenv("DLB_FLUID_SEGMENTS");  // k_segbb has no regularized sets
+        seg_fused_reg_ = kernel_main_ && cpt0 == 2 && !(fr && fr[0] == '0') && !(fs && fs[0] == '1');
+        if (kernel_main_ && !seg_fused_reg_) km &= ~(KM_REGV | KM_REGP);
         kernel_seg_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km, LAYOUT_SEG);
         // cells per thread of the segment sweep (DLB_SEG_CPT): 2 for fp64
         // (c4: 24.96 vs 23.76 GLUPS, profiles/r01_summary.md), 1 for fp32
@@ -1814,7 +1825,7 @@ void Lattice::launch_step(int parity) {
         a.z_begin = 0;
         a.z_step = 1;
         void* args[] = {&a};
-        const bool split_rare = kernel_main_ != nullptr && !fixups_.empty();
+        bool split_rare = kernel_main_ != nullptr && !fixups_.empty();
         if (kernel_cmp_) {
             // compacted porous sweep (+ the regularized cells with the full set)
             prepare_compact();
@@ -1853,6 +1864,8 @@ void Lattice::launch_step(int parity) {
                                         dim3(256), sargs, 0, stream_), "launch fluid segments");
             bb_dirty_ = true;
         } else if (kernel_seg_) {
+            // (regularized cells fused: no fix-up launches after it)
+            if (seg_fused_reg_) split_rare = false;
             // compacted masked sweep: one thread per cell of the listed segments
             // (also the first step of the fluid-segment sweep: it leaves every
             // listed cell current in both buffers)
