@@ -346,14 +346,14 @@ def main():
                  "bounce_back_cells": int(kinds[1]), "no_dynamics_cells": int(kinds[2]),
                  "variant": {"lists": "sparse kind-sorted lists (NoDynamics not listed)",
                              "masked": "masked sweep: all-NoDynamics 32-B segments neither loaded nor "
-                                       "stored (regularized planes recomputed by list launches)",
+                                       "stored; regularized inlet / outlet cells inside the sweep",
                              "dense": "dense sweep of every cell (regularized planes recomputed by "
                                       "list launches)"}[variant]}
         del vox
     else:
         cfg = dlb.CaseConfig(kind=kind, L=L, Re=Re, Ma=Ma, collision=lt, q=q)
         setup = dlb.init_tgv(cfg) if kind == "tgv" else dlb.init_cavity(cfg)
-    layout = args.layout if world == 1 else "twopop"  # AA runs single-slab lattices
+    layout = args.layout  # AA slabs link like two-population ones (odd steps store across the faces)
     run = dlb.build_run(setup, precision=bits, arith=args.arith,
                         dist=(rank, world) if world > 1 else None, devices=[local], layout=layout,
                         skip_nodynamics=skip, tma=args.tma,

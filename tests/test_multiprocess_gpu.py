@@ -72,3 +72,18 @@ def test_bench_spawns_ranks_without_launcher():
         if cfg == "c5":
             assert d["e2e"]["value"] > 0 and d["e2e"]["finite"]
 
+
+
+def test_bench_two_aa_ranks():
+    """`bench.py --gpus 2 --layout aa`: one AA in-place slab per rank, linked
+    over CUDA IPC (odd steps store across the faces)."""
+    import json
+    env = dict(os.environ, DLB_SAME_DEVICE="1")
+    env.pop("WORLD_SIZE", None)
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--config", "c5", "--L", "128",
+           "--layout", "aa", "--steps", "4", "--warmup", "3", "--no-cpu", "--no-e2e"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][0])
+    assert d["n_gpus"] == 2 and d["config"]["layout"] == "AA in-place SoA" and "k_aa" in d["config"]["kernel"]
+    assert all(x["lower"] == x["upper"] == "same_gpu" for x in d["config"]["halo"]["per_rank"])
