@@ -509,9 +509,12 @@ DLB_API dlb_status dlb_lattice_link_ipc(dlb_lattice* lat, int32_t side, const vo
 DLB_API dlb_status dlb_lattices_step(dlb_lattice** lats, size_t n, int64_t nsteps) {
     DLB_REQUIRE(lats || n == 0);
     return guarded([&] {
-        for (size_t k = 0; k < n; ++k) lats[k]->lat->check_dispatch();
-        for (int64_t s = 0; s < nsteps; ++s)
-            for (size_t k = 0; k < n; ++k) lats[k]->lat->enqueue_step();
+        std::vector<dlb::Lattice*> group;
+        for (size_t k = 0; k < n; ++k) {
+            lats[k]->lat->check_dispatch();
+            group.push_back(lats[k]->lat.get());
+        }
+        dlb::Lattice::step_group(group, nsteps);
     });
 }
 

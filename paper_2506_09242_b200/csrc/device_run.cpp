@@ -80,9 +80,12 @@ void DeviceRun::advance(int64_t nsteps, bool kinetic_last) {
         slabs_.front()->step(nsteps);
     } else {
         // eager dispatch check on every slab before any of them writes
-        for (auto& s : slabs_) s->check_dispatch();
-        for (int64_t k = 0; k < nsteps; ++k)
-            for (auto& s : slabs_) s->enqueue_step();
+        std::vector<Lattice*> group;
+        for (auto& s : slabs_) {
+            s->check_dispatch();
+            group.push_back(s.get());
+        }
+        Lattice::step_group(group, nsteps);
     }
     steps_ += nsteps;
 }

@@ -2,6 +2,9 @@
 // initialisation kernels evaluate equilibrium2<T> and the TGV state with the
 // reference's operation order (multiblock.cpp:278-281, cases.cpp:145-156).
 #include "lattice.hpp"
+
+#include <atomic>
+#include <mutex>
 #include "canon.cuh"
 
 #include <cstddef>
@@ -2000,9 +2003,168 @@ void Lattice::enqueue_step() {
     ++steps_;
 }
 
+namespace {
+std::atomic<uint64_t> g_graph_version{1};
+}
+
 void Lattice::invalidate_graph() {
     if (graph_) cudaGraphExecDestroy(graph_);
     graph_ = nullptr;
+    graph_version_ = g_graph_version.fetch_add(1);
+}
+
+namespace {
+// The one cached multi-slab graph (dlb_lattices_step / DeviceRun::advance), kGroupSteps steps:
+// keyed by the slabs, their graph versions and buffer parities at capture.
+struct GroupGraph {
+    std::vector<const void*> lats;
+    std::vector<uint64_t> versions;
+    std::vector<int> parity;
+    cudaGraphExec_t exec = nullptr;
+    cudaEvent_t fork = nullptr;
+    std::vector<cudaEvent_t> join;
+    int device = -1;
+};
+GroupGraph g_group;
+std::mutex g_group_mu;
+}  // namespace
+
+void Lattice::step_group(const std::vector<Lattice*>& lats, int64_t nsteps) {
+    if (lats.empty() || nsteps <= 0) return;
+    if (lats.size() == 1) {
+        lats[0]->step(nsteps);
+        return;
+    }
+    // steps per replay: the slabs meet at the graph's end (the first slab's
+    // stream waits for all), so a longer graph keeps them pipelined longer
+    constexpr int kGroupSteps = 8;
+    const int dev = lats[0]->device_;
+    bool graphable = nsteps >= kGroupSteps;
+    for (Lattice* l : lats)
+        graphable = graphable && l->device_ == dev && !l->trace_halo_ && !l->ke_requested_ && !l->kernel_segbb_;
+    // Only where the host is the bottleneck: enqueueing a slab's step costs
+    // ~9 us of host time; slabs moving more than ~64 MB per step (~10 us of
+    // HBM time) keep the device busy without a graph, and there the graph's
+    // barrier every kGroupSteps steps costs more than it saves (8 slabs of a
+    // 256^3 fp32 lattice: 444 vs 429 us per step; 8 slabs of config 1's 64^3
+    // fp64 cavity: 37 vs 74 us per step, profiles/r02b_summary.md)
+    int64_t max_bytes = 0;
+    for (Lattice* l : lats) max_bytes = std::max(max_bytes, l->step_bytes());
+    const char* ge = std::getenv("DLB_GROUP_GRAPH");
+    if (ge) graphable = graphable && ge[0] == '1';
+    else graphable = graphable && max_bytes <= (int64_t(64) << 20);
+    int64_t k = 0;
+    auto eager = [&] {
+        for (Lattice* l : lats) l->enqueue_step();
+        ++k;
+    };
+    if (!graphable) {
+        for (; k < nsteps;) eager();
+        return;
+    }
+    for (Lattice* l : lats) {
+        DeviceGuard dg(l->device_);
+        l->prepare_compact();  // gathers stay out of the graph
+    }
+    auto parity_of = [](const Lattice* l) { return l->aa() ? int(l->aa_odd_layout_) : l->cur_; };
+    std::lock_guard<std::mutex> lock(g_group_mu);
+    GroupGraph& G = g_group;
+    auto matches = [&] {
+        if (!G.exec || G.lats.size() != lats.size() || G.device != dev) return false;
+        for (std::size_t i = 0; i < lats.size(); ++i)
+            if (G.lats[i] != lats[i] || G.versions[i] != lats[i]->graph_version_ ||
+                G.parity[i] != parity_of(lats[i]))
+                return false;
+        return true;
+    };
+    DeviceGuard dg(dev);
+    if (!matches()) {
+        // a graph of the other parity: one eager step aligns every slab with it
+        if (G.exec && G.lats.size() == lats.size()) {
+            bool same = G.device == dev;
+            for (std::size_t i = 0; same && i < lats.size(); ++i)
+                same = G.lats[i] == lats[i] && G.versions[i] == lats[i]->graph_version_;
+            if (same) eager();
+        }
+    }
+    if (!matches()) {
+        if (G.exec) cudaGraphExecDestroy(G.exec);
+        G.exec = nullptr;
+        if (!G.fork) cuda_check(cudaEventCreateWithFlags(&G.fork, cudaEventDisableTiming), "event");
+        while (G.join.size() < lats.size()) {
+            cudaEvent_t e;
+            cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+            G.join.push_back(e);
+        }
+        struct Saved {
+            int cur;
+            bool odd, bb_dirty, bb_prologue, cmp_dirty;
+            int64_t steps, halo_steps;
+        };
+        std::vector<Saved> saved;
+        for (Lattice* l : lats)
+            saved.push_back({l->cur_, l->aa_odd_layout_, l->bb_dirty_, l->bb_prologue_, l->cmp_dirty_, l->steps_,
+                             l->halo_steps_});
+        cudaStream_t origin = lats[0]->stream_;
+        cudaGraph_t g = nullptr;
+        cuda_check(cudaStreamBeginCapture(origin, cudaStreamCaptureModeThreadLocal), "begin capture");
+        cuda_check(cudaEventRecord(G.fork, origin), "fork");
+        for (std::size_t i = 1; i < lats.size(); ++i)
+            cuda_check(cudaStreamWaitEvent(lats[i]->stream_, G.fork, 0), "fork");
+        for (int s = 0; s < kGroupSteps; ++s)
+            for (Lattice* l : lats) {
+                if (l->d_.precision_bits == 64) l->launch_step<double>(l->cur_);
+                else l->launch_step<float>(l->cur_);
+                if (!l->aa()) l->cur_ = 1 - l->cur_;
+            }
+        for (std::size_t i = 1; i < lats.size(); ++i) {
+            cuda_check(cudaEventRecord(G.join[i], lats[i]->stream_), "join");
+            cuda_check(cudaStreamWaitEvent(origin, G.join[i], 0), "join");
+        }
+        cuda_check(cudaStreamEndCapture(origin, &g), "end capture");
+        for (std::size_t i = 0; i < lats.size(); ++i) {
+            Lattice* l = lats[i];
+            const Saved& v = saved[i];
+            l->cur_ = v.cur;
+            l->aa_odd_layout_ = v.odd;
+            l->bb_dirty_ = v.bb_dirty;
+            l->bb_prologue_ = v.bb_prologue;
+            l->cmp_dirty_ = v.cmp_dirty;
+            l->steps_ = v.steps;
+            l->halo_steps_ = v.halo_steps;
+        }
+        cuda_check(cudaGraphInstantiateWithFlags(&G.exec, g, cudaGraphInstantiateFlagUseNodePriority),
+                   "graph instantiate");
+        cudaGraphDestroy(g);
+        G.lats.assign(lats.begin(), lats.end());
+        G.versions.clear();
+        G.parity.clear();
+        for (Lattice* l : lats) {
+            G.versions.push_back(l->graph_version_);
+            G.parity.push_back(parity_of(l));
+        }
+        G.device = dev;
+    }
+    if (nsteps - k >= kGroupSteps) {
+        cudaStream_t origin = lats[0]->stream_;
+        // the graph runs on the first slab's stream: order it after every
+        // slab's earlier work, and every slab's later work after it
+        for (std::size_t i = 1; i < lats.size(); ++i) {
+            cuda_check(cudaEventRecord(G.join[i], lats[i]->stream_), "order");
+            cuda_check(cudaStreamWaitEvent(origin, G.join[i], 0), "order");
+        }
+        for (; k + kGroupSteps <= nsteps; k += kGroupSteps) {
+            cuda_check(cudaGraphLaunch(G.exec, origin), "graph launch");
+            for (Lattice* l : lats) {
+                l->steps_ += kGroupSteps;
+                if (l->lower_.linked || l->upper_.linked) l->halo_steps_ += kGroupSteps;
+                if (l->kernel_cmp_) l->cmp_dirty_ = true;
+            }
+        }
+        cuda_check(cudaEventRecord(G.fork, origin), "order");
+        for (std::size_t i = 1; i < lats.size(); ++i) cuda_check(cudaStreamWaitEvent(lats[i]->stream_, G.fork, 0), "order");
+    }
+    for (; k < nsteps;) eager();
 }
 
 void Lattice::ensure_graph() {

@@ -89,6 +89,11 @@ class Lattice {
     void abort_host_block();
     void step(int64_t nsteps);
     void enqueue_step();  // one step, no dispatch check (group stepping)
+    // Several slabs of one process in lockstep (MultiBlockRun::advance,
+    // multiblock.cpp:376-419): long runs replay one CUDA graph holding eight
+    // steps of every slab (slabs on one device), so the host does not enqueue
+    // ~5 operations per slab and step. Dispatch is checked by the caller.
+    static void step_group(const std::vector<Lattice*>& lats, int64_t nsteps);
     void check_dispatch() const;
     void synchronize();
     void checksum(unsigned long long* per_dir, bool active_only = false);
@@ -298,6 +303,7 @@ class Lattice {
     // CUDA graph of two consecutive steps (parity 0 -> 1 -> 0), replayed by
     // step() / time_steps(); invalidated whenever kernels, slots or links change
     cudaGraphExec_t graph_ = nullptr;
+    uint64_t graph_version_ = 0;  // changes whenever the captured work would change (group graph cache key)
     void invalidate_graph();
     void ensure_graph();
     // host-block (zero-copy) path
