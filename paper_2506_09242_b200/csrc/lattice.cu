@@ -2041,7 +2041,8 @@ void Lattice::step_group(const std::vector<Lattice*>& lats, int64_t nsteps) {
     const int dev = lats[0]->device_;
     bool graphable = nsteps >= kGroupSteps;
     for (Lattice* l : lats)
-        graphable = graphable && l->device_ == dev && !l->trace_halo_ && !l->ke_requested_ && !l->kernel_segbb_;
+        graphable = graphable && l->device_ == dev && !l->trace_halo_ && !l->ke_requested_ && !l->kernel_segbb_ &&
+                    !l->kernel_tma_;  // (the TMA kernels' one-off envelope refresh stays out of graphs)
     // Only where the host is the bottleneck: enqueueing a slab's step costs
     // ~9 us of host time; slabs moving more than ~64 MB per step (~10 us of
     // HBM time) keep the device busy without a graph, and there the graph's
