@@ -152,7 +152,7 @@ def run_reference_arm(args, cfgname):
     mean, reps_, workers = res
     sample = (f"{kind} {Ls}^3 D3Q{q} {coll} fp{bits}, {workers} workers x z-blocks, "
               f"warmup {args.warmup} + 3 repetitions x {args.steps} steps, mean (perf::measure_mlups "
-              f"semantics, perfmodel.cpp:94-121); per-repetition MLUPS {[round(v, 1) for v in reps_]}")
+              f"semantics, perfmodel.cpp:94-121); per-repetition MLUPS {[round(float(v), 1) for v in reps_]}")
     if Ls < L:
         sample += f"; {Ls}^3 instead of {L}^3: host RAM (the reference's full-size layout does not fit)"
     ms = Ls ** 3 / (mean * 1e6) * 1e3

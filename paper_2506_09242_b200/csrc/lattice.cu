@@ -875,6 +875,8 @@ void Lattice::build_fixups(const std::vector<uint8_t>& u8) {
     cudaFree(d_fix_);
     d_fix_ = nullptr;
     if (aa() || xrec_) return;
+    if (const char* rs = std::getenv("DLB_RARE_SPLIT"))  // 0: regularized cells in the main sweep (tuning)
+        if (rs[0] == '0') return;
     std::vector<char> reg(chains_.size(), 0);
     bool any = false;
     for (std::size_t s = 0; s < chains_.size(); ++s)
