@@ -51,7 +51,7 @@ def expect(name, key="checksum"):
     return [int(v) for v in GOLD[name][key]]
 
 
-@pytest.mark.parametrize("layout,slabs", [("twopop", 1), ("aa", 1), ("twopop", 4)])
+@pytest.mark.parametrize("layout,slabs", [("twopop", 1), ("aa", 1), ("twopop", 4), ("aa", 4)])
 def test_config5_896_matches_reference(layout, slabs):
     name = "tgv896_bgk_f32_c5_box"
     spec = GOLD[name]["spec"]
@@ -61,16 +61,20 @@ def test_config5_896_matches_reference(layout, slabs):
     assert run.checksum() == expect(name)
 
 
-@pytest.mark.parametrize("variant", ["dense", "masked"])
-def test_config4_bench_geometry_matches_reference(variant):
+@pytest.mark.parametrize("variant", ["dense", "masked", "compact"])
+def test_config4_bench_geometry_matches_reference(variant, monkeypatch):
     name = "porous680x600x600_trt_f64_c4_box"
     g = GOLD[name]
     spec = g["spec"]
     setup, sha, phi = setup_of(spec)
     # the geometry is the one the reference loaded (same generator, same bytes)
     assert sha == g["voxels_sha256"] and phi == g["porosity"]
-    run = dlb.build_run(setup, precision=64, skip_nodynamics=variant == "masked")
+    if variant == "compact":
+        monkeypatch.setenv("DLB_POROUS_COMPACT", "1")
+    run = dlb.build_run(setup, precision=64, skip_nodynamics=variant != "dense")
     del setup
+    if variant == "compact":
+        assert "k_cmp" in run.kernel_name()
     run.advance(spec["steps"])
     if variant == "dense":
         assert run.checksum() == expect(name)
