@@ -1,5 +1,15 @@
-import numpy as np, sys
-sys.path.insert(0,'/root/repo')
+"""Traffic model of 128-B brick layouts for the c4 porous sweep (listed
+bricks written whole, reads = bricks touched by the shifted listed set,
+perfect L2 reuse assumed; profiles/r02b_summary.md).
+
+    python tools/c4_brick_model.py
+"""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2506_09242_b200 as dlb
 L=600
 cfg = dlb.CaseConfig(kind="porous", L=L, Ma=0.01, collision=dlb.LinkType.TRT, q=19, tau=1.0, upstream=40, downstream=40)

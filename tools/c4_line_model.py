@@ -1,5 +1,15 @@
-import numpy as np, sys
-sys.path.insert(0,'/root/repo')
+"""Line-granular DRAM model of the compacted porous sweep (k_cmp) at the c4
+bench geometry: distinct 32-B sectors / 64-B pairs / 128-B lines read per
+pull direction over the compact arrays (profiles/r02b_summary.md).
+
+    python tools/c4_line_model.py [L]
+"""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2506_09242_b200 as dlb
 L=int(sys.argv[1]) if len(sys.argv)>1 else 600
 cfg = dlb.CaseConfig(kind="porous", L=L, Ma=0.01, collision=dlb.LinkType.TRT, q=19, tau=1.0, upstream=40, downstream=40)

@@ -1,5 +1,15 @@
-import numpy as np, sys
-sys.path.insert(0,'/root/repo')
+"""Line-granular DRAM model of the masked porous sweep (k_seg) on the dense
+layout at the c4 bench geometry: bytes read at 32-B sector and 128-B line
+granularity (ncu measures 30.9 GB per step; profiles/r02b_summary.md).
+
+    python tools/c4_line_model_dense.py
+"""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2506_09242_b200 as dlb
 L=600
 cfg = dlb.CaseConfig(kind="porous", L=L, Ma=0.01, collision=dlb.LinkType.TRT, q=19, tau=1.0, upstream=40, downstream=40)
