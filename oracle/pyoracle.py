@@ -294,6 +294,10 @@ class Oracle:
             if not os.path.exists(ORACLE_SO):
                 raise RuntimeError(f"oracle not built: {ORACLE_SO} (run make -C oracle)")
             lib = C.CDLL(ORACLE_SO)
+            # every pointer argument declared: an undeclared one is passed as a
+            # 32-bit C int (the descriptor call segfaulted whenever numpy placed
+            # its arrays above 4 GiB)
+            lib.orc_descriptor.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
             lib.orc_derive_omega_minus.restype = C.c_double
             lib.orc_derive_omega_minus.argtypes = [C.c_double, C.c_double]
             for fn in ("orc_equilibrium_d",):
