@@ -1667,7 +1667,11 @@ void Lattice::issue_block_chunk(int c) {
 void Lattice::block_copy(cudaStream_t st, void* host, void* dev, bool up, int p0, int p1) {
     if (p1 <= p0) return;
     const std::size_t plane_bytes = std::size_t(blk_.plane) * blk_.elem;
-    {
+    static const bool one_d = [] {
+        const char* e = std::getenv("DLB_BLOCK_1D");  // tuning: per-direction 1-D copies
+        return e && e[0] == '1';
+    }();
+    if (!one_d) {
         // all q direction arrays in one 2-D copy (rows = directions, pitch = one array)
         const std::size_t off = std::size_t(p0) * blk_.plane * blk_.elem;
         const std::size_t pitch = std::size_t(blk_.vol) * blk_.elem;
