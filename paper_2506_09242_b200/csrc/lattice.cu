@@ -596,6 +596,29 @@ void Lattice::set_slots(const int32_t* slots) {
         return;
     }
     build_fixups(u8);
+    // Dense porous sweep (every cell, the reference's behaviour) with
+    // regularized planes in fp64: the segment sweep over ALL segments runs it
+    // at two cells per thread with the regularized cells inside (126 registers
+    // either way), instead of the one-cell k_pull plus two fix-up list launches
+    // that re-read every source line of those isolated cells.
+    dense_seg_ = false;
+    if (!(d_.flags & (DLB_FLAG_SKIP_NODYNAMICS | DLB_FLAG_SPARSE_LISTS)) && !split() && !aa() && !xrec_ &&
+        !untagged_ && d_.precision_bits == 64 && !fixups_.empty()) {
+        const char* de = std::getenv("DLB_DENSE_SEG");
+        const long long nsx = (geo_.nx + skip_group_ - 1) / skip_group_;
+        const long long nseg = (n / geo_.nx) * nsx;
+        if (!(de && de[0] == '0') && nseg < (1LL << 32) - 1) {
+            std::vector<uint32_t> segs(static_cast<std::size_t>(nseg));
+            std::iota(segs.begin(), segs.end(), 0u);
+            cudaFree(d_seg_);
+            cuda_check(cudaMalloc(&d_seg_, segs.size() * sizeof(uint32_t)), "cudaMalloc segments");
+            cuda_check(cudaMemcpy(d_seg_, segs.data(), segs.size() * sizeof(uint32_t), cudaMemcpyHostToDevice),
+                       "upload segments");
+            nseg_ = nseg;
+            masked_cells_ = n;
+            dense_seg_ = true;
+        }
+    }
     if (uniform && first >= 0) {
         uniform_slot_ = first;
     } else {
@@ -1149,7 +1172,7 @@ void Lattice::select_kernel() {
                                    LAYOUT_TWO_POP);
     kernel_seg_ = nullptr;
     seg_fused_reg_ = false;
-    if (d_seg_ && (km_needed_ & KM_SKIP)) {
+    if (d_seg_ && ((km_needed_ & KM_SKIP) || dense_seg_)) {
         unsigned km = km_needed_ & ~KM_SKIP;
         // the regularized cells stay in the segment sweep when it runs two
         // cells per thread (fp64): that instantiation has the same 126
