@@ -28,6 +28,8 @@ void cuda_check(cudaError_t e, const char* what) {
 namespace {
 
 constexpr std::size_t kStagingBytes = std::size_t(256) << 20;
+// graph versions: unique across lattices (the multi-slab graph cache key)
+std::atomic<uint64_t> g_graph_version{1};
 constexpr int kCz19[19] = {0, 0, 0, 0, 0, -1, 1, 0, 0, 0, 0, -1, 1, 1, -1, -1, 1, 1, -1};
 constexpr int kCz27[27] = {0, 0, 0, 0, 0, -1, 1, 0, 0, 0, 0, -1, 1, 1, -1, -1, 1, 1, -1,
                            -1, 1, 1, -1, -1, 1, -1, 1};
@@ -346,6 +348,7 @@ Lattice::Lattice(const dlb_lattice_desc& desc, const DynamicsRegistry& reg) : d_
     for (int t = 0; t < reg.num_tags(); ++t) tag_names_.push_back(reg.chain_for(t));
 
     device_ = d_.device;
+    graph_version_ = g_graph_version.fetch_add(1);
     DeviceGuard dg(device_);
     cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
     {
@@ -2030,10 +2033,6 @@ void Lattice::enqueue_step() {
     else launch_step<float>(cur_);
     if (!aa()) cur_ = 1 - cur_;
     ++steps_;
-}
-
-namespace {
-std::atomic<uint64_t> g_graph_version{1};
 }
 
 void Lattice::invalidate_graph() {
