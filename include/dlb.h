@@ -218,7 +218,10 @@ DLB_API dlb_status dlb_lattice_export_ipc(dlb_lattice* lat, void* blob, size_t c
 DLB_API dlb_status dlb_lattice_link_ipc(dlb_lattice* lat, int32_t side, const void* blob,
                                         size_t len);
 /* Advance several slabs of ONE process in lockstep (one step of each in turn),
- * the single-process analogue of MultiBlockRun::advance (multiblock.cpp:376-419). */
+ * the single-process analogue of MultiBlockRun::advance (multiblock.cpp:376-419).
+ * Slabs on one device that move <= 64 MB per step replay one CUDA graph of
+ * eight steps of every slab (DLB_GROUP_GRAPH=0/1 overrides): the call then
+ * returns after enqueueing, as for single slabs. */
 DLB_API dlb_status dlb_lattices_step(dlb_lattice** lats, size_t n, int64_t nsteps);
 
 /* ---- GPU-resident diagnostics (the sampling step after the update) ----------
