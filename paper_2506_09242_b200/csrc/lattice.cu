@@ -2136,32 +2136,45 @@ void Lattice::step_group(const std::vector<Lattice*>& lats, int64_t nsteps) {
                              l->halo_steps_});
         cudaStream_t origin = lats[0]->stream_;
         cudaGraph_t g = nullptr;
-        cuda_check(cudaStreamBeginCapture(origin, cudaStreamCaptureModeThreadLocal), "begin capture");
-        cuda_check(cudaEventRecord(G.fork, origin), "fork");
-        for (std::size_t i = 1; i < lats.size(); ++i)
-            cuda_check(cudaStreamWaitEvent(lats[i]->stream_, G.fork, 0), "fork");
-        for (int s = 0; s < kGroupSteps; ++s)
-            for (Lattice* l : lats) {
-                if (l->d_.precision_bits == 64) l->launch_step<double>(l->cur_);
-                else l->launch_step<float>(l->cur_);
-                if (!l->aa()) l->cur_ = 1 - l->cur_;
+        auto restore = [&] {
+            for (std::size_t i = 0; i < lats.size(); ++i) {
+                Lattice* l = lats[i];
+                const Saved& v = saved[i];
+                l->cur_ = v.cur;
+                l->aa_odd_layout_ = v.odd;
+                l->bb_dirty_ = v.bb_dirty;
+                l->bb_prologue_ = v.bb_prologue;
+                l->cmp_dirty_ = v.cmp_dirty;
+                l->steps_ = v.steps;
+                l->halo_steps_ = v.halo_steps;
             }
-        for (std::size_t i = 1; i < lats.size(); ++i) {
-            cuda_check(cudaEventRecord(G.join[i], lats[i]->stream_), "join");
-            cuda_check(cudaStreamWaitEvent(origin, G.join[i], 0), "join");
+        };
+        cuda_check(cudaStreamBeginCapture(origin, cudaStreamCaptureModeThreadLocal), "begin capture");
+        try {
+            cuda_check(cudaEventRecord(G.fork, origin), "fork");
+            for (std::size_t i = 1; i < lats.size(); ++i)
+                cuda_check(cudaStreamWaitEvent(lats[i]->stream_, G.fork, 0), "fork");
+            for (int s = 0; s < kGroupSteps; ++s)
+                for (Lattice* l : lats) {
+                    if (l->d_.precision_bits == 64) l->launch_step<double>(l->cur_);
+                    else l->launch_step<float>(l->cur_);
+                    if (!l->aa()) l->cur_ = 1 - l->cur_;
+                }
+            for (std::size_t i = 1; i < lats.size(); ++i) {
+                cuda_check(cudaEventRecord(G.join[i], lats[i]->stream_), "join");
+                cuda_check(cudaStreamWaitEvent(origin, G.join[i], 0), "join");
+            }
+        } catch (...) {
+            // close the capture so the streams stay usable, then report
+            cudaGraph_t bad = nullptr;
+            cudaStreamEndCapture(origin, &bad);
+            if (bad) cudaGraphDestroy(bad);
+            cudaGetLastError();
+            restore();
+            throw;
         }
         cuda_check(cudaStreamEndCapture(origin, &g), "end capture");
-        for (std::size_t i = 0; i < lats.size(); ++i) {
-            Lattice* l = lats[i];
-            const Saved& v = saved[i];
-            l->cur_ = v.cur;
-            l->aa_odd_layout_ = v.odd;
-            l->bb_dirty_ = v.bb_dirty;
-            l->bb_prologue_ = v.bb_prologue;
-            l->cmp_dirty_ = v.cmp_dirty;
-            l->steps_ = v.steps;
-            l->halo_steps_ = v.halo_steps;
-        }
+        restore();
         cuda_check(cudaGraphInstantiateWithFlags(&G.exec, g, cudaGraphInstantiateFlagUseNodePriority),
                    "graph instantiate");
         cudaGraphDestroy(g);
@@ -2209,8 +2222,24 @@ void Lattice::ensure_graph() {
     const bool bb_dirty = bb_dirty_, bb_prologue = bb_prologue_, cmp_dirty = cmp_dirty_;
     cudaGraph_t g = nullptr;
     cuda_check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "begin capture");
-    enqueue_step();
-    enqueue_step();
+    try {
+        enqueue_step();
+        enqueue_step();
+    } catch (...) {
+        // close the capture so the stream stays usable, restore, report
+        cudaGraph_t bad = nullptr;
+        cudaStreamEndCapture(stream_, &bad);
+        if (bad) cudaGraphDestroy(bad);
+        cudaGetLastError();
+        cur_ = cur;
+        aa_odd_layout_ = odd;
+        steps_ = steps;
+        halo_steps_ = halo_steps;
+        bb_dirty_ = bb_dirty;
+        bb_prologue_ = bb_prologue;
+        cmp_dirty_ = cmp_dirty;
+        throw;
+    }
     cuda_check(cudaStreamEndCapture(stream_, &g), "end capture");
     cur_ = cur;
     aa_odd_layout_ = odd;
