@@ -404,11 +404,21 @@ __global__ void __launch_bounds__(256, (min_blocks<T, Q, KM>()))
 // CPT times the bytes in flight per thread of the latency-bound fp64 sweep.
 template <typename T, int Q, unsigned KM, int CPT, int MINB = 0>
 __global__ void __launch_bounds__(256, (MINB ? MINB : (CPT == 1 ? min_blocks<T, Q, KM>() : 2)))
-    k_seg(const __grid_constant__ StepArgs<T> a, const unsigned* __restrict__ segs, long long nseg, int gshift) {
+    k_seg(const __grid_constant__ StepArgs<T> a, const unsigned* __restrict__ segs, long long nseg, int gshift,
+          int pf) {
     const Geo& g = a.g;
     const unsigned nsx = unsigned((g.nx + (1 << gshift) - 1) >> gshift);
     const long long n = nseg << gshift;
     const long long base = static_cast<long long>(blockIdx.x) * (256 * CPT) + threadIdx.x;
+    if (segs && pf > 0 && threadIdx.x < 32) {
+        // the segment entries of the block pf launches ahead (about one wave of
+        // resident blocks) into L2: its threads' first, dependent load then
+        // hits L2 instead of DRAM (the list is streamed once per step)
+        const long long e0 = ((static_cast<long long>(blockIdx.x) + pf) * (256 * CPT)) >> gshift;
+        const long long e = e0 + threadIdx.x * 32;  // one 128-B line per lane
+        const long long e_end = e0 + ((256LL * CPT) >> gshift);
+        if (e < e_end && e < nseg) asm volatile("prefetch.global.L2 [%0];" ::"l"(segs + e));
+    }
     int xs[CPT], ys[CPT], zs[CPT];
     bool ok[CPT];
     T f[CPT][Q];
@@ -418,7 +428,8 @@ __global__ void __launch_bounds__(256, (MINB ? MINB : (CPT == 1 ? min_blocks<T, 
         ok[c] = t < n;
         xs[c] = ys[c] = zs[c] = 0;
         if (ok[c]) {
-            const unsigned e = __ldg(segs + (t >> gshift));
+            // segs == nullptr: every segment (the dense sweep), no list to chase
+            const unsigned e = segs ? __ldg(segs + (t >> gshift)) : unsigned(t >> gshift);
             const unsigned row = e / nsx;
             xs[c] = int((e - row * nsx) << gshift) + int(t & ((1 << gshift) - 1));
             zs[c] = int(row / unsigned(g.ny));

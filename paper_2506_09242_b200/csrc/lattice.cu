@@ -490,6 +490,7 @@ int64_t Lattice::bytes_per_cell() const {
 
 int64_t Lattice::step_bytes() const {
     if (sparse_) return step_bytes_;
+    if (dense_seg_ && !(lower_.linked || upper_.linked)) return bytes_per_cell() * cells();  // no list read
     if (kernel_segbb_ && !(lower_.linked || upper_.linked))  // listed cells: populations, slot, link mask; 4 B / segment
         return (int64_t(2) * d_.q * (d_.precision_bits / 8) + 1 + 4) * fseg_cells_ + 4 * nfseg_;
     if (kernel_seg_ && !(lower_.linked || upper_.linked))  // listed cells + their slot bytes + 4 B per segment
@@ -611,12 +612,9 @@ void Lattice::set_slots(const int32_t* slots) {
         const long long nsx = (geo_.nx + skip_group_ - 1) / skip_group_;
         const long long nseg = (n / geo_.nx) * nsx;
         if (!(de && de[0] == '0') && nseg < (1LL << 32) - 1) {
-            std::vector<uint32_t> segs(static_cast<std::size_t>(nseg));
-            std::iota(segs.begin(), segs.end(), 0u);
+            // no segment list: k_seg maps thread -> segment arithmetically
             cudaFree(d_seg_);
-            cuda_check(cudaMalloc(&d_seg_, segs.size() * sizeof(uint32_t)), "cudaMalloc segments");
-            cuda_check(cudaMemcpy(d_seg_, segs.data(), segs.size() * sizeof(uint32_t), cudaMemcpyHostToDevice),
-                       "upload segments");
+            d_seg_ = nullptr;
             nseg_ = nseg;
             masked_cells_ = n;
             dense_seg_ = true;
@@ -1128,6 +1126,16 @@ void Lattice::set_uniform_slot(int32_t slot) {
     d_seg_ = nullptr;
     nseg_ = 0;
     build_fluid_segments({});
+    // every per-cell structure of an earlier set_slots goes with it
+    free_compact();
+    dense_seg_ = false;
+    fixups_.clear();
+    cudaFree(d_fix_);
+    d_fix_ = nullptr;
+    sparse_ = false;
+    lists_.clear();
+    cudaFree(d_list_);
+    d_list_ = nullptr;
     masked_cells_ = -1;
     uniform_slot_ = slot;
     untagged_ = false;
@@ -1175,7 +1183,7 @@ void Lattice::select_kernel() {
                                    LAYOUT_TWO_POP);
     kernel_seg_ = nullptr;
     seg_fused_reg_ = false;
-    if (d_seg_ && ((km_needed_ & KM_SKIP) || dense_seg_)) {
+    if ((d_seg_ && (km_needed_ & KM_SKIP)) || dense_seg_) {
         unsigned km = km_needed_ & ~KM_SKIP;
         // the regularized cells stay in the segment sweep when it runs two
         // cells per thread (fp64): that instantiation has the same 126
@@ -1908,7 +1916,13 @@ void Lattice::launch_step(int parity) {
             long long ns = nseg_;
             int gshift = 0;
             while ((1 << gshift) < skip_group_) ++gshift;
-            void* sargs[] = {&a, &sp, &ns, &gshift};
+            // segment-entry prefetch distance in blocks (DLB_SEG_PREFETCH; 0 = off)
+            static const int pf_env = [] {
+                const char* e = std::getenv("DLB_SEG_PREFETCH");
+                return e ? std::atoi(e) : -1;
+            }();
+            int pf = pf_env >= 0 ? pf_env : 74;  // 37-148 measured best on c4 (27.6 vs 26.8 GLUPS without)
+            void* sargs[] = {&a, &sp, &ns, &gshift, &pf};
             const long long threads = ns << gshift;
             const long long per_block = 256LL * kernel_seg_->cpt;
             cuda_check(cudaLaunchKernel(kernel_seg_->fn, dim3(unsigned((threads + per_block - 1) / per_block)),

@@ -129,3 +129,27 @@ def test_compact_sweep_reports_launches_and_memory(monkeypatch):
     assert run.traffic(0)[2] == 2            # main sweep + regularized inlet / outlet cells
     assert run.traffic(0)[1] > ref.traffic(0)[1]  # compact arrays beside the dense layout
     assert run.step_bytes() == ref.step_bytes()   # same algorithmic bytes (listed cells)
+
+
+@pytest.mark.parametrize("flags", [{}, {"skip_nodynamics": True}, {"sparse_lists": True}])
+def test_slots_replaced_by_uniform_slot(flags, monkeypatch):
+    """A lattice whose porous slot field (regularized planes, NoDynamics
+    solids: fix-up lists, segment lists, compact arrays, sparse lists) is
+    replaced by one uniform slot steps exactly like a lattice built uniform."""
+    monkeypatch.setenv("DLB_POROUS_COMPACT", "1")
+    setup = sphere_setup(36, 16, 16, (0, 1, 1), seed=11)
+    reg = dlb.DynamicsRegistry()
+    slots = np.asarray([reg.register_chain(c) for c in setup.chains], np.int32)[setup.chain_index]
+    bulk = int(slots[0, 0, 2])  # upstream fluid buffer: the bulk chain
+    run = dlb.DeviceRun(setup.dims, setup.periodic, reg, precision=64, **flags)
+    run.fill_slots(slots)
+    run.fill_state()
+    run.advance(3)
+    run.fill_slots(bulk)
+    run.fill_state()
+    run.advance(9)
+    ref = dlb.DeviceRun(setup.dims, setup.periodic, reg, precision=64)
+    ref.fill_slots(bulk)
+    ref.fill_state()
+    ref.advance(9)
+    assert np.array_equal(run.gather_populations(), ref.gather_populations())
