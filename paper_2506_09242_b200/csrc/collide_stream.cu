@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(256, (min_blocks<T, Q, KM>()))
 template <typename T, int Q, unsigned KM, int CPT, int MINB = 0>
 __global__ void __launch_bounds__(256, (MINB ? MINB : (CPT == 1 ? min_blocks<T, Q, KM>() : 2)))
     k_seg(const __grid_constant__ StepArgs<T> a, const unsigned* __restrict__ segs, long long nseg, int gshift,
-          int pf) {
+          int pf, int pack) {
     const Geo& g = a.g;
     const unsigned nsx = unsigned((g.nx + (1 << gshift) - 1) >> gshift);
     const long long n = nseg << gshift;
@@ -430,10 +430,20 @@ __global__ void __launch_bounds__(256, (MINB ? MINB : (CPT == 1 ? min_blocks<T, 
         if (ok[c]) {
             // segs == nullptr: every segment (the dense sweep), no list to chase
             const unsigned e = segs ? __ldg(segs + (t >> gshift)) : unsigned(t >> gshift);
-            const unsigned row = e / nsx;
-            xs[c] = int((e - row * nsx) << gshift) + int(t & ((1 << gshift) - 1));
-            zs[c] = int(row / unsigned(g.ny));
-            ys[c] = int(row - unsigned(zs[c]) * unsigned(g.ny));
+            const int lane = int(t & ((1 << gshift) - 1));
+            if (pack != 0 && segs) {
+                // packed entry s | y << bs | z << (bs + by): no divisions on the
+                // path from the entry load to the population loads
+                const int bs = pack & 0xff, by = (pack >> 8) & 0xff;
+                xs[c] = int((e & ((1u << bs) - 1u)) << gshift) + lane;
+                ys[c] = int((e >> bs) & ((1u << by) - 1u));
+                zs[c] = int(e >> (bs + by));
+            } else {
+                const unsigned row = e / nsx;
+                xs[c] = int((e - row * nsx) << gshift) + lane;
+                zs[c] = int(row / unsigned(g.ny));
+                ys[c] = int(row - unsigned(zs[c]) * unsigned(g.ny));
+            }
             ok[c] = xs[c] < g.nx;
         }
     }

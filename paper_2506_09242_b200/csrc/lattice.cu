@@ -562,15 +562,23 @@ void Lattice::set_slots(const int32_t* slots) {
                                (n / G) < (1LL << 32) - 1;
         std::vector<uint32_t> segs;
         long long moved = 0;
+        // packed entries (segment | y << bs | z << (bs + by)) when they fit 32 bits
+        auto bits = [](long long v) { int b = 0; while ((1LL << b) < v) ++b; return b; };
+        const int bs = bits(nsx), by = bits(geo_.ny), bz = bits(geo_.nz);
+        const char* pe = std::getenv("DLB_SEG_PACK");  // 0: linear entries decoded by division (tuning)
+        seg_pack_ = (bs + by + bz <= 32 && bs < 32 && by < 32 && !(pe && pe[0] == '0')) ? (bs | (by << 8)) : 0;
         for (long long r = 0; r < n / geo_.nx; ++r) {
             const uint8_t* row = u8.data() + r * geo_.nx;
+            const long long ry = r % geo_.ny, rz = r / geo_.ny;
             for (int x0 = 0; x0 < geo_.nx; x0 += G) {
                 const int x1 = std::min(geo_.nx, x0 + G);
                 bool any = untagged_;
                 for (int x = x0; x < x1 && !any; ++x) any = !nodyn[row[x]];
                 if (!any) continue;
                 moved += x1 - x0;
-                if (want_segs) segs.push_back(uint32_t(r * nsx + x0 / G));
+                if (want_segs)
+                    segs.push_back(seg_pack_ ? uint32_t(x0 / G) | uint32_t(ry << bs) | uint32_t(rz << (bs + by))
+                                             : uint32_t(r * nsx + x0 / G));
             }
         }
         masked_cells_ = moved;
@@ -1922,7 +1930,8 @@ void Lattice::launch_step(int parity) {
                 return e ? std::atoi(e) : -1;
             }();
             int pf = pf_env >= 0 ? pf_env : 74;  // 37-148 measured best on c4 (27.6 vs 26.8 GLUPS without)
-            void* sargs[] = {&a, &sp, &ns, &gshift, &pf};
+            int pack = seg_pack_;
+            void* sargs[] = {&a, &sp, &ns, &gshift, &pf, &pack};
             const long long threads = ns << gshift;
             const long long per_block = 256LL * kernel_seg_->cpt;
             cuda_check(cudaLaunchKernel(kernel_seg_->fn, dim3(unsigned((threads + per_block - 1) / per_block)),

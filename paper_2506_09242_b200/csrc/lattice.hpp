@@ -187,6 +187,7 @@ class Lattice {
     long long nseg_ = 0;
     const KernelEntry* kernel_seg_ = nullptr;
     bool seg_fused_reg_ = false;  // k_seg runs the regularized cells itself (no fix-up launches)
+    int seg_pack_ = 0;            // k_seg entry packing (bs | by << 8), 0 = linear segment index
     bool dense_seg_ = false;      // dense porous sweep as k_seg over every segment (fp64 with regularized planes)
     // fluid-segment sweep (k_segbb): segments with a collision cell, their
     // per-cell bounce-back link masks, the wall cells finalized lazily
