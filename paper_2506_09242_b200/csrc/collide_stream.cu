@@ -409,14 +409,15 @@ __global__ void __launch_bounds__(256, (MINB ? MINB : (CPT == 1 ? min_blocks<T, 
     const Geo& g = a.g;
     const unsigned nsx = unsigned((g.nx + (1 << gshift) - 1) >> gshift);
     const long long n = nseg << gshift;
-    const long long base = static_cast<long long>(blockIdx.x) * (256 * CPT) + threadIdx.x;
+    const int bd = int(blockDim.x);  // 256 (or 128: finer-grained block turnover)
+    const long long base = static_cast<long long>(blockIdx.x) * (bd * CPT) + threadIdx.x;
     if (segs && pf > 0 && threadIdx.x < 32) {
         // the segment entries of the block pf launches ahead (about one wave of
         // resident blocks) into L2: its threads' first, dependent load then
         // hits L2 instead of DRAM (the list is streamed once per step)
-        const long long e0 = ((static_cast<long long>(blockIdx.x) + pf) * (256 * CPT)) >> gshift;
+        const long long e0 = ((static_cast<long long>(blockIdx.x) + pf) * (bd * CPT)) >> gshift;
         const long long e = e0 + threadIdx.x * 32;  // one 128-B line per lane
-        const long long e_end = e0 + ((256LL * CPT) >> gshift);
+        const long long e_end = e0 + ((static_cast<long long>(bd) * CPT) >> gshift);
         if (e < e_end && e < nseg) asm volatile("prefetch.global.L2 [%0];" ::"l"(segs + e));
     }
     int xs[CPT], ys[CPT], zs[CPT];
@@ -424,7 +425,7 @@ __global__ void __launch_bounds__(256, (MINB ? MINB : (CPT == 1 ? min_blocks<T, 
     T f[CPT][Q];
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
-        const long long t = base + 256 * c;
+        const long long t = base + bd * c;
         ok[c] = t < n;
         xs[c] = ys[c] = zs[c] = 0;
         if (ok[c]) {

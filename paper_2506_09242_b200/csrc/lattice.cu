@@ -1932,10 +1932,18 @@ void Lattice::launch_step(int parity) {
             int pf = pf_env >= 0 ? pf_env : 74;  // 37-148 measured best on c4 (27.6 vs 26.8 GLUPS without)
             int pack = seg_pack_;
             void* sargs[] = {&a, &sp, &ns, &gshift, &pf, &pack};
+            // threads per block: 128 for the every-segment dense sweep (finer-grained
+            // block turnover at 4 CTAs per SM: c4 dense 19.5 vs 18.8 GLUPS), 256 for
+            // the masked one (27.6 vs 27.5); DLB_SEG_BLOCK=128/256 overrides
+            static const int sb_env = [] {
+                const char* e = std::getenv("DLB_SEG_BLOCK");
+                return e ? std::atoi(e) : 0;
+            }();
+            const int sb = sb_env == 128 || sb_env == 256 ? sb_env : (dense_seg_ ? 128 : 256);
             const long long threads = ns << gshift;
-            const long long per_block = 256LL * kernel_seg_->cpt;
+            const long long per_block = (long long)sb * kernel_seg_->cpt;
             cuda_check(cudaLaunchKernel(kernel_seg_->fn, dim3(unsigned((threads + per_block - 1) / per_block)),
-                                        dim3(256), sargs, 0, stream_), "launch segments");
+                                        dim3(unsigned(sb)), sargs, 0, stream_), "launch segments");
             bb_prologue_ = false;
             bb_dirty_ = false;
         } else if (ke_requested_ && kernel_ke_) {
