@@ -1839,15 +1839,16 @@ void Lattice::launch_step(int parity) {
         a.rec[s] = compile_recipe<T>(chains_[s]);
     a.xrec = static_cast<const DevRecipe<T>*>(d_xrec_);
 
-    const int bx = geo_.nx >= 128 ? 128 : (geo_.nx > 32 ? 64 : 32);
+    const int bx0 = geo_.nx >= 128 ? 128 : (geo_.nx > 32 ? 64 : 32);
     // 128-thread blocks: the same occupancy as 256 (launch bounds are per 256
     // threads), but a retiring block frees its SM slot at half the
     // granularity -- the low-occupancy fp64 / D3Q27 sweeps gain (c2 14.4 ->
     // 14.9 GLUPS, c1 +1.8 %, c3 +0.6 %), c5 is unchanged; DLB_PULL_THREADS=256
     static const int pull_threads = [] {
         const char* e = std::getenv("DLB_PULL_THREADS");
-        return e && std::atoi(e) == 256 ? 256 : 128;
+        return e && (std::atoi(e) == 256 || std::atoi(e) == 64) ? std::atoi(e) : 128;
     }();
+    const int bx = std::min(bx0, pull_threads);
     const int by = std::max(1, pull_threads / bx);
     const dim3 block(bx, by, 1);
     const unsigned gx = unsigned((geo_.nx + bx - 1) / bx);
