@@ -46,9 +46,14 @@ constexpr int min_blocks() {
 // release-stores it into both neighbours' flags (read by their k_halo_wait).
 template <typename T>
 __device__ __forceinline__ void signal_step(const StepArgs<T>& a) {
-    __threadfence_system();
+    // One system-scope fence per block, by the thread that takes the ticket
+    // after the barrier: fences are cumulative, so it orders every thread's
+    // peer stores that the barrier ordered before it (the pattern of
+    // cooperative groups' grid sync, at system scope). A fence in every thread
+    // kept each boundary block resident for its own fence latency.
     __syncthreads();
     if (threadIdx.x == 0 && threadIdx.y == 0) {
+        __threadfence_system();
         const unsigned total = gridDim.x * gridDim.y * gridDim.z;
         const unsigned ticket = atomicAdd(a.counter, 1u);
         if (ticket == total - 1) {
