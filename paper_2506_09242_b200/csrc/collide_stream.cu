@@ -1281,15 +1281,20 @@ __global__ void __launch_bounds__(NCW * 32 + 32, (NCW >= 16 ? 1 : 2))
             "k_aa_" #ODD "<" #T ",D3Q" #Q "," #KM ">[" DLB_STR(DLB_MODE) "]"                  \
     }
 #define AA_PAIR(T, Q, KM) AA_ENTRY(T, Q, KM, false), AA_ENTRY(T, Q, KM, true)
-// boundary planes of linked AA slabs (catch-all sets only: two planes per step)
+// boundary planes of linked AA slabs: the common sets and the catch-alls (the
+// catch-all fp32 instantiation runs at 80 registers: its two planes took 40 us
+// per 512^2 step, beside a 3.3 ms interior)
 #define AA_LINK_ENTRY(T, Q, KM, ODD)                                                     \
     KernelEntry {                                                                        \
         int(sizeof(T) * 8), Q, unsigned(KM), ODD ? LAYOUT_AA_ODD_LINK : LAYOUT_AA_LINK,     \
             reinterpret_cast<const void*>(&k_aa<T, Q, unsigned(KM), ODD, true>),          \
             "k_aa_link_" #ODD "<" #T ",D3Q" #Q "," #KM ">[" DLB_STR(DLB_MODE) "]"             \
     }
+#define AA_LINK_PAIR(T, Q, KM) AA_LINK_ENTRY(T, Q, KM, false), AA_LINK_ENTRY(T, Q, KM, true)
 #define AA_LINK_SET(T)                                                                    \
-    , AA_LINK_ENTRY(T, 19, KM_ALL, false), AA_LINK_ENTRY(T, 19, KM_ALL, true),            \
+    , AA_LINK_PAIR(T, 19, KM_BGK), AA_LINK_PAIR(T, 19, KM_TRT), AA_LINK_PAIR(T, 19, KM_TRT | KM_BB | KM_MBB), \
+        AA_LINK_PAIR(T, 27, KM_RR),                                                       \
+        AA_LINK_ENTRY(T, 19, KM_ALL, false), AA_LINK_ENTRY(T, 19, KM_ALL, true),          \
         AA_LINK_ENTRY(T, 27, KM_ALL, false), AA_LINK_ENTRY(T, 27, KM_ALL, true),          \
         AA_LINK_ENTRY(T, 19, KM_ALL | KM_XREC, false), AA_LINK_ENTRY(T, 19, KM_ALL | KM_XREC, true), \
         AA_LINK_ENTRY(T, 27, KM_ALL | KM_XREC, false), AA_LINK_ENTRY(T, 27, KM_ALL | KM_XREC, true)
