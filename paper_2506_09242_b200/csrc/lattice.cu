@@ -1941,14 +1941,15 @@ void Lattice::launch_step(int parity) {
             int pf = pf_env >= 0 ? pf_env : 74;  // 37-148 measured best on c4 (27.6 vs 26.8 GLUPS without)
             int pack = seg_pack_;
             void* sargs[] = {&a, &sp, &ns, &gshift, &pf, &pack};
-            // threads per block: 128 for the every-segment dense sweep (finer-grained
-            // block turnover at 4 CTAs per SM: c4 dense 19.5 vs 18.8 GLUPS), 256 for
-            // the masked one (27.6 vs 27.5); DLB_SEG_BLOCK=128/256 overrides
+            // threads per block: 64 for the every-segment dense sweep (finer-grained
+            // block turnover at 8 CTAs per SM: c4 dense 20.0 / 19.5 / 18.8 GLUPS at
+            // 64 / 128 / 256; 32 the same as 64), 256 for the masked one (27.6 vs
+            // 27.5 at 128, 27.2 at 64); DLB_SEG_BLOCK=32/64/128/256 overrides
             static const int sb_env = [] {
                 const char* e = std::getenv("DLB_SEG_BLOCK");
                 return e ? std::atoi(e) : 0;
             }();
-            const int sb = sb_env == 128 || sb_env == 256 ? sb_env : (dense_seg_ ? 128 : 256);
+            const int sb = sb_env == 32 || sb_env == 64 || sb_env == 128 || sb_env == 256 ? sb_env : (dense_seg_ ? 64 : 256);
             const long long threads = ns << gshift;
             const long long per_block = (long long)sb * kernel_seg_->cpt;
             cuda_check(cudaLaunchKernel(kernel_seg_->fn, dim3(unsigned((threads + per_block - 1) / per_block)),
