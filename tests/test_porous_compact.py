@@ -153,3 +153,25 @@ def test_slots_replaced_by_uniform_slot(flags, monkeypatch):
     ref.fill_state()
     ref.advance(9)
     assert np.array_equal(run.gather_populations(), ref.gather_populations())
+
+
+@pytest.mark.parametrize("pack", ["1", "0"])
+@pytest.mark.parametrize("block", ["32", "64", "128", "256"])
+def test_segment_sweep_launch_variants(oracle, pack, block, monkeypatch):
+    """The segment sweep's packed / linear entries and every block size give
+    the reference's values on every non-NoDynamics cell, masked and dense."""
+    monkeypatch.setenv("DLB_SEG_PACK", pack)
+    monkeypatch.setenv("DLB_SEG_BLOCK", block)
+    spec = CASES["sphere48_trt_f64_c4"]
+    setup, bits, steps = product_setup(spec)
+    want = oracle.run_case(make_case(spec), np.float64, steps).reshape(19, -1)
+    active = np.asarray(setup.chain_index).reshape(-1) != 2
+    for skip in (True, False):
+        run = dlb.build_run(setup, precision=bits, skip_nodynamics=skip)
+        assert "k_seg" in run.kernel_name(), run.kernel_name()
+        run.advance(steps)
+        got = run.gather_populations().reshape(19, -1)
+        if skip:
+            assert np.array_equal(got[:, active], want[:, active])
+        else:
+            assert np.array_equal(got, want)
