@@ -1154,6 +1154,26 @@ void Lattice::set_uniform_slot(int32_t slot) {
 
 void Lattice::select_kernel() {
     invalidate_graph();
+    // launch-shape knobs, read whenever the kernels are chosen (per lattice)
+    {
+        // dense / AA sweeps: 128-thread blocks -- the same occupancy as 256 (launch
+        // bounds are per 256 threads), but a retiring block frees its SM slot at
+        // half the granularity: c2 14.4 -> 14.9 GLUPS, c1 +1.8 %, c3 +0.6 %, c5
+        // unchanged (DLB_PULL_THREADS = 64 / 128 / 256)
+        const char* e = std::getenv("DLB_PULL_THREADS");
+        const int v = e ? std::atoi(e) : 0;
+        pull_threads_ = (v == 64 || v == 256) ? v : 128;
+        // segment sweep: entry prefetch distance in blocks (37-148 best on c4:
+        // 27.6 vs 26.8 GLUPS without; DLB_SEG_PREFETCH, 0 = off)
+        const char* pe = std::getenv("DLB_SEG_PREFETCH");
+        seg_prefetch_ = pe ? std::max(0, std::atoi(pe)) : 74;
+        // segment sweep threads per block: 64 for the every-segment dense sweep
+        // (c4 dense 20.0 / 19.5 / 18.8 GLUPS at 64 / 128 / 256; 32 as 64), 256
+        // for the masked one (27.6 vs 27.5 at 128, 27.2 at 64); DLB_SEG_BLOCK
+        const char* be = std::getenv("DLB_SEG_BLOCK");
+        const int b = be ? std::atoi(be) : 0;
+        seg_block_ = (b == 32 || b == 64 || b == 128 || b == 256) ? b : (dense_seg_ ? 64 : 256);
+    }
     kernel_ke_ = nullptr;
     ke_requested_ = false;
     if (sparse_) return;
@@ -1840,16 +1860,8 @@ void Lattice::launch_step(int parity) {
     a.xrec = static_cast<const DevRecipe<T>*>(d_xrec_);
 
     const int bx0 = geo_.nx >= 128 ? 128 : (geo_.nx > 32 ? 64 : 32);
-    // 128-thread blocks: the same occupancy as 256 (launch bounds are per 256
-    // threads), but a retiring block frees its SM slot at half the
-    // granularity -- the low-occupancy fp64 / D3Q27 sweeps gain (c2 14.4 ->
-    // 14.9 GLUPS, c1 +1.8 %, c3 +0.6 %), c5 is unchanged; DLB_PULL_THREADS=256
-    static const int pull_threads = [] {
-        const char* e = std::getenv("DLB_PULL_THREADS");
-        return e && (std::atoi(e) == 256 || std::atoi(e) == 64) ? std::atoi(e) : 128;
-    }();
-    const int bx = std::min(bx0, pull_threads);
-    const int by = std::max(1, pull_threads / bx);
+    const int bx = std::min(bx0, pull_threads_);
+    const int by = std::max(1, pull_threads_ / bx);
     const dim3 block(bx, by, 1);
     const unsigned gx = unsigned((geo_.nx + bx - 1) / bx);
     const unsigned gy = unsigned((geo_.ny + by - 1) / by);
@@ -1934,22 +1946,10 @@ void Lattice::launch_step(int parity) {
             int gshift = 0;
             while ((1 << gshift) < skip_group_) ++gshift;
             // segment-entry prefetch distance in blocks (DLB_SEG_PREFETCH; 0 = off)
-            static const int pf_env = [] {
-                const char* e = std::getenv("DLB_SEG_PREFETCH");
-                return e ? std::atoi(e) : -1;
-            }();
-            int pf = pf_env >= 0 ? pf_env : 74;  // 37-148 measured best on c4 (27.6 vs 26.8 GLUPS without)
+            int pf = seg_prefetch_;
             int pack = seg_pack_;
             void* sargs[] = {&a, &sp, &ns, &gshift, &pf, &pack};
-            // threads per block: 64 for the every-segment dense sweep (finer-grained
-            // block turnover at 8 CTAs per SM: c4 dense 20.0 / 19.5 / 18.8 GLUPS at
-            // 64 / 128 / 256; 32 the same as 64), 256 for the masked one (27.6 vs
-            // 27.5 at 128, 27.2 at 64); DLB_SEG_BLOCK=32/64/128/256 overrides
-            static const int sb_env = [] {
-                const char* e = std::getenv("DLB_SEG_BLOCK");
-                return e ? std::atoi(e) : 0;
-            }();
-            const int sb = sb_env == 32 || sb_env == 64 || sb_env == 128 || sb_env == 256 ? sb_env : (dense_seg_ ? 64 : 256);
+            const int sb = seg_block_;
             const long long threads = ns << gshift;
             const long long per_block = (long long)sb * kernel_seg_->cpt;
             cuda_check(cudaLaunchKernel(kernel_seg_->fn, dim3(unsigned((threads + per_block - 1) / per_block)),

@@ -187,6 +187,9 @@ class Lattice {
     long long nseg_ = 0;
     const KernelEntry* kernel_seg_ = nullptr;
     bool seg_fused_reg_ = false;  // k_seg runs the regularized cells itself (no fix-up launches)
+    int pull_threads_ = 128;      // dense / AA sweep threads per block (DLB_PULL_THREADS)
+    int seg_prefetch_ = 74;       // segment-entry L2 prefetch distance in blocks (DLB_SEG_PREFETCH)
+    int seg_block_ = 256;         // segment sweep threads per block (DLB_SEG_BLOCK)
     int seg_pack_ = 0;            // k_seg entry packing (bs | by << 8), 0 = linear segment index
     bool dense_seg_ = false;      // dense porous sweep as k_seg over every segment (fp64 with regularized planes)
     // fluid-segment sweep (k_segbb): segments with a collision cell, their
