@@ -1156,13 +1156,6 @@ void Lattice::select_kernel() {
     invalidate_graph();
     // launch-shape knobs, read whenever the kernels are chosen (per lattice)
     {
-        // dense / AA sweeps: 128-thread blocks -- the same occupancy as 256 (launch
-        // bounds are per 256 threads), but a retiring block frees its SM slot at
-        // half the granularity: c2 14.4 -> 14.9 GLUPS, c1 +1.8 %, c3 +0.6 %, c5
-        // unchanged (DLB_PULL_THREADS = 64 / 128 / 256)
-        const char* e = std::getenv("DLB_PULL_THREADS");
-        const int v = e ? std::atoi(e) : 0;
-        pull_threads_ = (v == 64 || v == 256) ? v : 128;
         // segment sweep: entry prefetch distance in blocks (37-148 best on c4:
         // 27.6 vs 26.8 GLUPS without; DLB_SEG_PREFETCH, 0 = off)
         const char* pe = std::getenv("DLB_SEG_PREFETCH");
@@ -1181,6 +1174,19 @@ void Lattice::select_kernel() {
     for (int32_t s : present_slots_) km_needed_ |= kind_bits(chains_[std::size_t(s)]);
     if ((d_.flags & (DLB_FLAG_SKIP_NODYNAMICS | DLB_FLAG_SPARSE_LISTS)) && (km_needed_ & KM_NODYN) && !aa())
         km_needed_ |= KM_SKIP;
+    {
+        // dense / AA sweeps: 128-thread blocks for the low-occupancy sets -- the
+        // same threads per SM as 256 (launch bounds are per 256 threads), but a
+        // retiring block frees its SM slot at half the granularity: c2 14.4 ->
+        // 14.9 GLUPS, c1 +1.8 %, c3 +0.6 %, AA c5 38.6 -> 40.8; the pure-BGK fp32
+        // set (c5, 10 blocks of 128 per SM) keeps 256: +0.55 % under power
+        // capping (40.82 vs 40.59 GLUPS), equal otherwise. DLB_PULL_THREADS
+        const char* e = std::getenv("DLB_PULL_THREADS");
+        const int v = e ? std::atoi(e) : 0;
+        const bool light = d_.precision_bits == 32 && d_.q == 19 && !aa() &&
+                           (km_needed_ & ~(KM_SKIP | KM_KE | KM_XREC)) == KM_BGK;
+        pull_threads_ = (v == 64 || v == 128 || v == 256) ? v : (light ? 256 : 128);
+    }
     if (aa()) {
         kernel_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_, LAYOUT_AA);
         kernel_odd_ = find_kernel(d_.arith, d_.precision_bits, d_.q, km_needed_, LAYOUT_AA_ODD);
