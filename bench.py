@@ -237,8 +237,14 @@ def e2e_block(L, bits, steps, warmup, rank=0, world=1, barrier=lambda: None, max
         barrier()
         dt_max = max_over_ranks(t1 - t0)
         mlups = L ** 3 * steps / dt_max / 1e6
+        d2h_bytes = int(19 * L * L * nz * np.dtype(dt).itemsize)
+        link = pcie_ceiling()
+        per_rank_gbs = (nbytes + d2h_bytes) * steps / dt_max / 1e9
         return {"value": mlups, "unit": "MLUPS", "h2d_bytes_per_step": int(nbytes) * world,
-                "d2h_bytes_per_step": int(19 * L * L * nz * np.dtype(dt).itemsize) * world,
+                "d2h_bytes_per_step": d2h_bytes * world,
+                "pcie": {"achieved_gbs_per_gpu": per_rank_gbs, "ceiling_gbs_per_gpu": link,
+                         "frac": per_rank_gbs / link if link else None,
+                         "ceiling": "1 GiB pinned H2D + D2H copies at once on this GPU, measured in this run"},
                 "sample": f"host AcceleratedBlock {L}^3 (+envelope) fp{bits} as {world} z-slab block(s), one per "
                           f"GPU, pinned f_in + f_out swapped per call, {steps} steps, wall clock incl. envelope "
                           "refresh, H2D, step, D2H",
@@ -246,6 +252,34 @@ def e2e_block(L, bits, steps, warmup, rank=0, world=1, barrier=lambda: None, max
     finally:
         _capi.lib().dlb_host_free(p)
         _capi.lib().dlb_host_free(p2)
+
+
+def pcie_ceiling():
+    """Bidirectional host<->device copy rate (GB/s) of this GPU: 1 GiB pinned
+    buffers copied both ways at once, best of 3 -- the ceiling of the host-block
+    e2e loop, which moves the whole state over PCIe every step."""
+    import torch
+    n = 1 << 30
+    try:
+        h_in = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        h_out = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        d_a = torch.empty(n, dtype=torch.uint8, device="cuda")
+        d_b = torch.empty(n, dtype=torch.uint8, device="cuda")
+    except Exception:
+        return None
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    best = 0.0
+    for _ in range(4):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        with torch.cuda.stream(s1):
+            d_a.copy_(h_in, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h_out.copy_(d_b, non_blocking=True)
+        torch.cuda.synchronize()
+        best = max(best, 2 * n / (time.perf_counter() - t) / 1e9)
+    del h_in, h_out, d_a, d_b
+    return best
 
 
 def free_port():
