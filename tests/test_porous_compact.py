@@ -175,3 +175,19 @@ def test_segment_sweep_launch_variants(oracle, pack, block, monkeypatch):
             assert np.array_equal(got[:, active], want[:, active])
         else:
             assert np.array_equal(got, want)
+
+
+def test_masked_sweep_fast_mode_within_1e12(oracle):
+    """FMA ("fast") arithmetic in the fused masked sweep: every non-NoDynamics
+    population within the fp64 bar (max raw-relative error 1e-12)."""
+    spec = CASES["sphere48_trt_f64_c4"]
+    setup, bits, steps = product_setup(spec)
+    run = dlb.build_run(setup, precision=bits, skip_nodynamics=True, arith="fast")
+    assert "k_seg" in run.kernel_name() and "fast" in run.kernel_name()
+    run.advance(steps)
+    got = run.gather_populations().reshape(19, -1)
+    want = oracle.run_case(make_case(spec), np.float64, steps).reshape(19, -1)
+    active = np.asarray(setup.chain_index).reshape(-1) != 2
+    w = np.asarray(__import__("pyoracle").descriptor(19)[1])[:, None]
+    rel = np.abs(got[:, active] - want[:, active]) / (np.abs(want[:, active]) + w)
+    assert rel.max() <= 1e-12
