@@ -451,31 +451,34 @@ def test_checksum_matches_oracle():
         assert run.checksum() == want, (layout, slabs)
 
 
-def test_full_size_config3_matches_reference_checksum():
+@pytest.mark.parametrize("layout,slabs", [("twopop", 1), ("twopop", 4), ("aa", 1), ("aa", 2)])
+def test_full_size_config3_matches_reference_checksum(layout, slabs):
     """Config 3 at its full per-GPU size (cavity 512^3 D3Q19 TRT fp32): the
     device state after the reference's step count has the reference's exact
-    checksum (tests/golden/golden_full.json, made from oracle/_ref)."""
+    checksum (tests/golden/golden_full.json, made from oracle/_ref) -- also as
+    linked z-slabs (the walls and the lid land in different slabs) and in the
+    AA layout."""
     import json
     path = os.path.join(os.path.dirname(__file__), "golden", "golden_full.json")
     g = json.load(open(path))["cavity512_trt_f32_c3_full"]
     spec = dict(g["spec"])
     setup, bits, steps = product_setup(spec)
-    run = dlb.build_run(setup, precision=bits)
+    run = dlb.build_run(setup, precision=bits, layout=layout, slabs=slabs)
     run.advance(steps)
     assert run.checksum() == [int(v) for v in g["checksum"]]
 
 
 def test_full_size_config5_layout_and_decomposition_invariance():
     """Config 5 at full size (TGV D3Q19 BGK fp32 1024^3, 169 GB two-population):
-    two-population, AA in place, and 2 z-slabs give identical checksums."""
+    two-population, AA in place, and 2 z-slabs of either give identical checksums."""
     cfg = dlb.CaseConfig(kind="tgv", L=1024, Re=1600.0, Ma=0.2)
     sums = []
-    for layout, slabs in (("twopop", 1), ("aa", 1), ("twopop", 2)):
+    for layout, slabs in (("twopop", 1), ("aa", 1), ("twopop", 2), ("aa", 2)):
         run = dlb.build_run(dlb.init_tgv(cfg), precision=32, layout=layout, slabs=slabs)
         run.advance(5)
         sums.append(run.checksum())
         del run
-    assert sums[0] == sums[1] == sums[2]
+    assert sums[0] == sums[1] == sums[2] == sums[3]
 
 
 @pytest.mark.parametrize("layout", ["twopop", "aa"])
