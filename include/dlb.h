@@ -311,12 +311,19 @@ DLB_API dlb_status dlb_lattice_velocity_planes(dlb_lattice* lat, int32_t z0, int
  * (accelerated_lattice.hpp:86-112): f_in/f_out q*ext[0]*ext[1]*ext[2] values,
  * tag/param_index ext-volume int32. Pre: envelope of f_in current.
  * Post, f_out != NULL: the new interior state was written into the f_out
- * buffer (its envelope untouched), the previous state is left in the f_in
+ * buffer, the previous state is left in the f_in
  * buffer, and the view's two pointers are SWAPPED -- view->f_in is the new
  * state, as after the reference's std::swap of the two arrays
  * (accelerated_lattice.cpp:199); callers owning the arrays swap them when the
  * pointers came back swapped. f_out == NULL: the new state
  * overwrites the interior of f_in in place (its envelope untouched).
+ * f_out's envelope: pageable buffers -- untouched, as by the reference's
+ * step_range (accelerated_lattice.cpp:126-153); pinned buffers (the copy-back
+ * moves whole planes) -- the z envelope planes untouched, the x / y envelope
+ * cells of the interior planes set to f_in's (identical whenever the two
+ * buffers hold the same envelope: a bounded block's, or a periodic one the
+ * caller refreshes before each step; DLB_BLOCK_D2H_ROWS=1 leaves them
+ * untouched too, and costs 20-30 % of the end-to-end rate).
  * Errors (DLB_ERROR_DISPATCH ...) leave both buffers and the view unchanged. */
 typedef struct dlb_block_view {
     int32_t precision_bits;

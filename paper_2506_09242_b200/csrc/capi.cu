@@ -2,6 +2,7 @@
 // status codes the way the reference's C interface does (proj/src/capi.cpp:20-39);
 // the message goes to a thread-local last-error buffer (capi.cpp:13-18).
 #include <chrono>
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -86,7 +87,12 @@ struct BlockCtx {
     std::unique_ptr<dlb::Lattice> lat;
     uint64_t reg_serial = 0, reg_generation = 0;
     std::vector<int32_t> slots;
+    // per (y, z) row: the row's slot when all nx cells share it, else
+    // kMixedRow -- the scan compares such rows against one value instead of
+    // re-reading the cached slots (a third of the scan's host reads)
+    std::vector<int64_t> row_slot;
 };
+constexpr int64_t kMixedRow = INT64_MIN;
 std::mutex g_block_mu;
 std::map<std::vector<int64_t>, BlockCtx> g_blocks;
 std::atomic<uint64_t> g_registry_serial{0};
@@ -538,7 +544,7 @@ DLB_API dlb_status dlb_collide_and_stream(const dlb_registry* reg, dlb_block_vie
         const std::vector<int64_t> key = {nx, ny, nz, block->q, block->precision_bits};
         BlockCtx& ctx = g_blocks[key];
         const bool have_ctx = ctx.lat && ctx.reg_serial == reg->serial && ctx.reg_generation == reg->generation &&
-                              ctx.slots.size() == size_t(nx * ny * nz);
+                              ctx.slots.size() == size_t(nx * ny * nz) && ctx.row_slot.size() == size_t(ny * nz);
         const auto t_call = std::chrono::steady_clock::now();
         const int nw = int(std::max<int64_t>(1, std::min<int64_t>(nz, std::thread::hardware_concurrency())));
         std::vector<std::vector<char>> seen(size_t(nw), std::vector<char>(size_t(ntags), 0));
@@ -562,10 +568,18 @@ DLB_API dlb_status dlb_collide_and_stream(const dlb_registry* reg, dlb_block_vie
                             else if (t < 0) untagged[size_t(w)] = 1;
                             else unknown[size_t(w)] = 1;
                         }
-                        if (have_ctx && !changed[size_t(w)] &&
-                            std::memcmp(ctx.slots.data() + k0, block->param_index + row + 1,
-                                        size_t(nx) * sizeof(int32_t)) != 0)
-                            changed[size_t(w)] = 1;
+                        if (have_ctx && !changed[size_t(w)]) {
+                            const int32_t* pr = block->param_index + row + 1;
+                            const int64_t rs = ctx.row_slot[size_t(k0 / nx)];
+                            if (rs != kMixedRow) {
+                                const int32_t v = int32_t(rs);
+                                int32_t d = 0;
+                                for (int64_t x = 0; x < nx; ++x) d |= pr[x] ^ v;
+                                if (d != 0) changed[size_t(w)] = 1;
+                            } else if (std::memcmp(ctx.slots.data() + k0, pr, size_t(nx) * sizeof(int32_t)) != 0) {
+                                changed[size_t(w)] = 1;
+                            }
+                        }
                     }
             });
         }
@@ -632,11 +646,16 @@ DLB_API dlb_status dlb_collide_and_stream(const dlb_registry* reg, dlb_block_vie
         if (any_change) {
             drop();  // computed with stale slots
             ctx.slots.resize(size_t(nx * ny * nz));
+            ctx.row_slot.assign(size_t(ny * nz), kMixedRow);
             for (int64_t z = 1; z <= nz; ++z)
-                for (int64_t y = 1; y <= ny; ++y)
-                    std::memcpy(ctx.slots.data() + ((z - 1) * ny + (y - 1)) * nx,
-                                block->param_index + (z * ext[1] + y) * ext[0] + 1,
-                                size_t(nx) * sizeof(int32_t));
+                for (int64_t y = 1; y <= ny; ++y) {
+                    const int64_t r = (z - 1) * ny + (y - 1);
+                    const int32_t* src = block->param_index + (z * ext[1] + y) * ext[0] + 1;
+                    std::memcpy(ctx.slots.data() + r * nx, src, size_t(nx) * sizeof(int32_t));
+                    int32_t d = 0;
+                    for (int64_t x = 0; x < nx; ++x) d |= src[x] ^ src[0];
+                    if (d == 0) ctx.row_slot[size_t(r)] = src[0];
+                }
             ctx.lat->set_slots(ctx.slots.data());
         }
         if (speculative) {

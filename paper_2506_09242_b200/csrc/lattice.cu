@@ -248,6 +248,30 @@ __global__ void k_refresh_envelope(T* origin0, Geo g, int q) {
     }
 }
 
+// Host-block pipeline: the x / y envelope cells of host planes [p0, p1) of the
+// input mirror into the output mirror (blockIdx.y = direction * planes + plane),
+// so the whole-plane copy-back hands the caller's envelope back unchanged
+// instead of stale mirror memory (the kernels write interior cells only).
+template <typename T>
+__global__ void k_carry_envelope_xy(const T* __restrict__ din, T* __restrict__ dout, long long vol, int pitch,
+                                    int plane, int nx, int ny, int p0, int np) {
+    const int i = int(blockIdx.y) / np, p = p0 + int(blockIdx.y) % np;
+    const int per = 2 * pitch + 2 * ny;  // rows y = 0 and y = ny + 1, then x = 0 / nx + 1 of rows 1..ny
+    for (int k = int(blockIdx.x * blockDim.x + threadIdx.x); k < per; k += int(gridDim.x * blockDim.x)) {
+        int x, y;
+        if (k < 2 * pitch) {
+            y = k < pitch ? 0 : ny + 1;
+            x = k < pitch ? k : k - pitch;
+        } else {
+            const int r = k - 2 * pitch;
+            y = 1 + (r >> 1);
+            x = (r & 1) ? nx + 1 : 0;
+        }
+        const long long at = i * vol + static_cast<long long>(p) * plane + static_cast<long long>(y) * pitch + x;
+        dout[at] = din[at];
+    }
+}
+
 int grid_for(long long n) {
     long long b = (n + 255) / 256;
     return int(std::min<long long>(std::max<long long>(b, 1), 148LL * 32));
@@ -1682,6 +1706,9 @@ void Lattice::launch_host_block(void* f_in, const int64_t ext[3], void* f_out) {
     blk_.dout = dout;
     blk_.vol = vol;
     blk_.plane = hg.plane;
+    blk_.pitch = hg.pitch;
+    blk_.nx = hg.nx;
+    blk_.ny = hg.ny;
     blk_.nz = hg.nz;
     blk_.zc = zc;
     blk_.nchunks = nchunks;
@@ -1726,6 +1753,17 @@ void Lattice::issue_block_chunk(int c) {
     void* kargs[] = {args.data()};
     cuda_check(cudaLaunchKernel(kernel_->fn, dim3(blk_.gx, blk_.gy, unsigned(z1 - z0)), dim3(blk_.bx, blk_.by, 1),
                                 kargs, 0, stream_), "launch");
+    {   // host planes [z0 + 1, z1 + 1): their x / y envelope rides along to the copy-back
+        const int np = z1 - z0, per = 2 * blk_.pitch + 2 * blk_.ny;
+        const dim3 grid(unsigned(std::min(8, (per + 255) / 256)), unsigned(d_.q * np));
+        if (blk_.elem == 8)
+            k_carry_envelope_xy<double><<<grid, 256, 0, stream_>>>(static_cast<const double*>(blk_.din),
+                static_cast<double*>(blk_.dout), blk_.vol, blk_.pitch, blk_.plane, blk_.nx, blk_.ny, z0 + 1, np);
+        else
+            k_carry_envelope_xy<float><<<grid, 256, 0, stream_>>>(static_cast<const float*>(blk_.din),
+                static_cast<float*>(blk_.dout), blk_.vol, blk_.pitch, blk_.plane, blk_.nx, blk_.ny, z0 + 1, np);
+        cuda_check(cudaGetLastError(), "k_carry_envelope_xy");
+    }
     cuda_check(cudaEventRecord(blk_ev_[3 * c + 1], stream_), "event");
     if (c == blk_.nchunks - 1 && blk_tr_[2]) cuda_check(cudaEventRecord(blk_tr_[2], stream_), "event");
 }
@@ -1760,6 +1798,37 @@ void Lattice::block_copy(cudaStream_t st, void* host, void* dev, bool up, int p0
     }
 }
 
+// Copy-back of host planes [p0, p1). Default: whole planes (one 2-D copy for
+// all directions), whose x / y envelope cells carry f_in's envelope
+// (k_carry_envelope_xy): in place that is the caller's envelope unchanged;
+// into f_out it is f_in's envelope where the reference's step_range (interior
+// cells only, accelerated_lattice.cpp:126-153) leaves f_out's -- equal
+// whenever the two buffers hold the same envelope (a bounded block's, or one
+// refreshed before each step). DLB_BLOCK_D2H_ROWS=1: interior rows only (one
+// 3-D copy per direction), f_out's envelope never written; measured 20-30 %
+// slower end to end (row-sized DMA pieces; profiles/r02c_summary.md).
+void Lattice::block_copy_back_interior(cudaStream_t st, int p0, int p1) {
+    if (p1 <= p0) return;
+    static const bool by_rows = [] {
+        const char* v = std::getenv("DLB_BLOCK_D2H_ROWS");
+        return v && v[0] == '1';
+    }();
+    if (!by_rows) return block_copy(st, blk_.f_out, blk_.dout, false, p0, p1);
+    const std::size_t e = std::size_t(blk_.elem);
+    const std::size_t pitch = std::size_t(blk_.pitch) * e;
+    const std::size_t rows = std::size_t(blk_.plane / blk_.pitch);
+    for (int i = 0; i < d_.q; ++i) {
+        const std::size_t off = std::size_t(i) * std::size_t(blk_.vol) * e;
+        cudaMemcpy3DParms m{};
+        m.srcPtr = make_cudaPitchedPtr(static_cast<char*>(blk_.dout) + off, pitch, pitch, rows);
+        m.dstPtr = make_cudaPitchedPtr(static_cast<char*>(blk_.f_out) + off, pitch, pitch, rows);
+        m.srcPos = m.dstPos = make_cudaPos(e, 1, std::size_t(p0));
+        m.extent = make_cudaExtent(std::size_t(blk_.nx) * e, std::size_t(blk_.ny), std::size_t(p1 - p0));
+        m.kind = cudaMemcpyDeviceToHost;
+        cuda_check(cudaMemcpy3DAsync(&m, st), "d2h interior");
+    }
+}
+
 void Lattice::begin_host_block(void* f_in, const int64_t ext[3], void* f_out) {
     DeviceGuard dg(device_);
     if (aa()) throw std::invalid_argument("host-block stepping uses the two-population layout");
@@ -1778,7 +1847,7 @@ void Lattice::finish_host_block() {
         const int z1 = std::min(blk_.nz, (c + 1) * blk_.zc);
         cuda_check(cudaStreamWaitEvent(copy_stream_, blk_ev_[3 * c + 1], 0), "wait");
         if (c == 0 && blk_tr_[3]) cuda_check(cudaEventRecord(blk_tr_[3], copy_stream_), "event");
-        block_copy(copy_stream_, blk_.f_out, blk_.dout, false, written, z1 + 1);
+        block_copy_back_interior(copy_stream_, written, z1 + 1);
         written = z1 + 1;
         cuda_check(cudaEventRecord(blk_ev_[3 * c + 2], copy_stream_), "event");
         blk_.copied = c + 1;

@@ -325,6 +325,7 @@ class Lattice {
         void* dout = nullptr;
         long long vol = 0;
         int plane = 0, nz = 0, zc = 1, nchunks = 0, elem = 4;
+        int pitch = 0, nx = 0, ny = 0;  // host row pitch (x extent + envelope), interior x / y
         int issued = 0;         // chunks whose H2D + compute are enqueued
         int ahead = 2;          // H2D chunks allowed ahead of the D2H copy-back (DLB_BLOCK_AHEAD, 0 = all)
         unsigned gx = 1, gy = 1, bx = 32, by = 8;
@@ -335,6 +336,7 @@ class Lattice {
     std::vector<uint8_t> blk_args_;  // the StepArgs<T> of the pending block step
     void issue_block_chunk(int c);
     void block_copy(cudaStream_t st, void* host, void* dev, bool up, int p0, int p1);
+    void block_copy_back_interior(cudaStream_t st, int p0, int p1);
     template <typename T>
     void fill_recipes(StepArgs<T>& a) const;
     template <typename T>

@@ -112,3 +112,122 @@ def test_cache_release_frees_device_memory():
     assert dlb.block_cache_info() == (0, 0)
     dlb.collide_and_stream(reg, blk, tag, pidx, dlb.DispatchSet.all_of(reg))  # rebuilt on demand
     assert dlb.block_cache_info()[0] == 1
+
+
+def _envelope_mask(shape):
+    m = np.ones(shape, bool)
+    m[:, 1:-1, 1:-1, 1:-1] = False
+    return m
+
+
+@pytest.mark.parametrize("memory", ["pageable", "pinned"])
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_envelope_after_step(memory, dtype):
+    """step_range writes interior cells only (accelerated_lattice.cpp:126-153).
+    In place, the caller's envelope survives the step on both paths. Into f_out:
+    the pageable path leaves f_out's envelope untouched; the pinned pipeline
+    copies whole planes back, whose x / y envelope cells carry f_in's envelope
+    (never stale device memory), and the z envelope planes are not written."""
+    n, sentinel = 12, 1234.5
+    alloc = pinned if memory == "pinned" else host_alloc
+    reg = dlb.DynamicsRegistry()
+    case, a, ka, tag, pidx = tgv_block(n, reg, dtype, alloc)
+    b, kb = alloc(a.shape, dtype)
+    try:
+        a[:, 1:-1, 1:-1, 1:-1] = 0.01  # a uniform (non-equilibrium) state: any finite values do
+        dlb.refresh_envelope_periodic(a, (1, 1, 1))
+        a[:, 1:-1, 0, :] = 0.5   # x / y envelope of the interior planes differs from f_out's
+        env = _envelope_mask(a.shape)
+        b[:] = sentinel
+        before_a = a.copy()
+        new, old = dlb.collide_and_stream(reg, a, tag, pidx, dlb.DispatchSet.all_of(reg), f_out=b)
+        assert new is b and old is a
+        assert np.array_equal(old, before_a)
+        interior = new[:, 1:-1, 1:-1, 1:-1]
+        assert np.all(np.isfinite(interior)) and not np.any(interior == sentinel)
+        assert np.all(new[:, 0] == sentinel) and np.all(new[:, -1] == sentinel)  # z envelope planes
+        xy = np.zeros(a.shape, bool)
+        xy[:, 1:-1] = env[:, 1:-1]
+        if memory == "pageable":
+            assert np.all(new[env] == sentinel)
+        else:
+            assert np.array_equal(new[xy], before_a[xy])
+        # in place: the envelope of f_in is left as the caller set it
+        a[env] = -sentinel
+        got = dlb.collide_and_stream(reg, a, tag, pidx, dlb.DispatchSet.all_of(reg))
+        assert got is a and np.all(a[env] == -sentinel)
+    finally:
+        for k in (ka, kb):
+            if k is not None:
+                _capi.lib().dlb_host_free(k)
+
+
+def test_pinned_ragged_block_matches_pageable():
+    """A ragged block (x, y, z extents differ, x not a multiple of the warp)
+    through the pinned pipeline equals the pageable path bit for bit: every
+    state's interior, and the previous state (f_out) entirely."""
+    nx, ny, nz = 37, 11, 9
+    reg = dlb.DynamicsRegistry()
+    s = reg.register_chain(dlb.init_tgv(dlb.CaseConfig(kind="tgv", L=8, Re=50.0, Ma=0.1)).chains[0])
+    shape = (19, nz + 2, ny + 2, nx + 2)
+    tag = np.full(shape[1:], -1, np.int32)
+    tag[1:-1, 1:-1, 1:-1] = reg.tag_of_slot(s)
+    pidx = np.where(tag >= 0, s, -1).astype(np.int32)
+    rng = np.random.default_rng(7)
+    init = (rng.standard_normal(shape) * 1e-3).astype(np.float64)
+    outs = []
+    keep = []
+    try:
+        for alloc in (host_alloc, pinned):
+            a, ka = alloc(shape, np.float64)
+            b, kb = alloc(shape, np.float64)
+            keep += [ka, kb]
+            a[:] = init
+            b[:] = 7.0
+            f_in, f_out = a, b
+            for _ in range(3):
+                dlb.refresh_envelope_periodic(f_in, (1, 1, 1))
+                f_in, f_out = dlb.collide_and_stream(reg, f_in, tag, pidx, dlb.DispatchSet.all_of(reg), f_out=f_out)
+            outs.append((f_in.copy(), f_out.copy()))
+        (pa_new, pa_old), (pi_new, pi_old) = outs
+        assert np.array_equal(pa_new[:, 1:-1, 1:-1, 1:-1], pi_new[:, 1:-1, 1:-1, 1:-1])
+        assert np.array_equal(pa_old, pi_old)
+    finally:
+        for k in keep:
+            if k is not None:
+                _capi.lib().dlb_host_free(k)
+
+
+def test_single_cell_slot_change_in_uniform_row():
+    """The scan summarises uniform rows of the cached slots by one value; a
+    param_index change of one cell in such a row must still re-upload the slots
+    (the result equals a step from a freshly built device context)."""
+    n = 12
+    reg = dlb.DynamicsRegistry()
+    case, a, ka, tag, pidx = tgv_block(n, reg, np.float64, pinned)
+    s2 = reg.register_chain(dlb.init_tgv(dlb.CaseConfig(kind="tgv", L=n, Re=5.0, Ma=0.1)).chains[0])
+    try:
+        a[:, 1:-1, 1:-1, 1:-1] = 0.01
+        rng = np.random.default_rng(3)
+        a[:, 1:-1, 1:-1, 1:-1] += rng.standard_normal((19, n, n, n)) * 1e-4
+        alld = dlb.DispatchSet.all_of(reg)
+        for _ in range(2):
+            dlb.refresh_envelope_periodic(a, (1, 1, 1))
+            dlb.collide_and_stream(reg, a, tag, pidx, alld)
+        snap = a.copy()
+        tag2, pidx2 = tag.copy(), pidx.copy()
+        tag2[5, 7, 3], pidx2[5, 7, 3] = reg.tag_of_slot(s2), s2
+        dlb.refresh_envelope_periodic(a, (1, 1, 1))
+        dlb.collide_and_stream(reg, a, tag2, pidx2, alld)   # cached context
+        cached = a.copy()
+        dlb.block_cache_release()
+        a[:] = snap
+        dlb.refresh_envelope_periodic(a, (1, 1, 1))
+        dlb.collide_and_stream(reg, a, tag2, pidx2, alld)   # fresh context
+        assert np.array_equal(cached, a)
+        a[:] = snap
+        dlb.refresh_envelope_periodic(a, (1, 1, 1))
+        dlb.collide_and_stream(reg, a, tag, pidx, alld)
+        assert not np.array_equal(cached[:, 4:7, 6:9, 2:5], a[:, 4:7, 6:9, 2:5])  # the changed cell matters
+    finally:
+        _capi.lib().dlb_host_free(ka)
