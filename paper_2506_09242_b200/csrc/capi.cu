@@ -536,9 +536,6 @@ DLB_API dlb_status dlb_collide_and_stream(const dlb_registry* reg, dlb_block_vie
         const int64_t nx = block->interior[0], ny = block->interior[1], nz = block->interior[2];
         if (nx < 1 || ny < 1 || nz < 1) throw std::invalid_argument("block extents must be >= 1");
         const int64_t ext[3] = {nx + 2, ny + 2, nz + 2};
-        // Eager tag scan (accelerated_lattice.cpp:161-181): fail before any
-        // write. Parallel over z; the workers also compare param_index with
-        // the slots the cached device lattice holds (re-upload only on change).
         const int ntags = reg->reg.num_tags();
         std::lock_guard<std::mutex> lock(g_block_mu);
         const std::vector<int64_t> key = {nx, ny, nz, block->q, block->precision_bits};
@@ -546,17 +543,50 @@ DLB_API dlb_status dlb_collide_and_stream(const dlb_registry* reg, dlb_block_vie
         const bool have_ctx = ctx.lat && ctx.reg_serial == reg->serial && ctx.reg_generation == reg->generation &&
                               ctx.slots.size() == size_t(nx * ny * nz) && ctx.row_slot.size() == size_t(ny * nz);
         const auto t_call = std::chrono::steady_clock::now();
+        auto is_pinned = [](const void* p) {
+            cudaPointerAttributes attr{};
+            const bool ok = cudaPointerGetAttributes(&attr, p) == cudaSuccess && attr.type == cudaMemoryTypeHost &&
+                            attr.devicePointer == p;
+            cudaGetLastError();
+            return ok;
+        };
+        const bool pinned = is_pinned(block->f_in) && (!block->f_out || is_pinned(block->f_out));
+        // With a cached device lattice and pinned buffers the pipeline starts
+        // speculatively with the cached slots while the tags are scanned; the
+        // param_index comparison then runs plane by plane beside the copy-back,
+        // which it gates chunk by chunk (a changed plane recomputes from its
+        // chunk on). Otherwise the scan compares param_index too, up front.
+        const bool spec_path = have_ctx && pinned;
+        // one interior plane of param_index against the cached slots (uniform
+        // rows against one value): true when any cell's slot changed
+        auto plane_changed = [&](int64_t z) {
+            for (int64_t y = 1; y <= ny; ++y) {
+                const int64_t row = (z * ext[1] + y) * ext[0];
+                const int64_t r = (z - 1) * ny + (y - 1);
+                const int32_t* pr = block->param_index + row + 1;
+                const int64_t rs = ctx.row_slot[size_t(r)];
+                if (rs != kMixedRow) {
+                    const int32_t v = int32_t(rs);
+                    int32_t d = 0;
+                    for (int64_t x = 0; x < nx; ++x) d |= pr[x] ^ v;
+                    if (d != 0) return true;
+                } else if (std::memcmp(ctx.slots.data() + r * nx, pr, size_t(nx) * sizeof(int32_t)) != 0) {
+                    return true;
+                }
+            }
+            return false;
+        };
+        // Eager tag scan (accelerated_lattice.cpp:161-181): fail before any
+        // write. Parallel over z.
         const int nw = int(std::max<int64_t>(1, std::min<int64_t>(nz, std::thread::hardware_concurrency())));
         std::vector<std::vector<char>> seen(size_t(nw), std::vector<char>(size_t(ntags), 0));
         std::vector<char> untagged(size_t(nw), 0), unknown(size_t(nw), 0), changed(size_t(nw), 0);
         std::vector<std::thread> th;
         for (int w = 0; w < nw; ++w) {
             th.emplace_back([&, w] {
-                for (int64_t z = 1 + nz * w / nw; z < 1 + nz * (w + 1) / nw; ++z)
+                for (int64_t z = 1 + nz * w / nw; z < 1 + nz * (w + 1) / nw; ++z) {
                     for (int64_t y = 1; y <= ny; ++y) {
-                        const int64_t row = (z * ext[1] + y) * ext[0];
-                        const int64_t k0 = ((z - 1) * ny + (y - 1)) * nx;
-                        const int32_t* tr = block->tag + row + 1;
+                        const int32_t* tr = block->tag + (z * ext[1] + y) * ext[0] + 1;
                         // fast path: a row of one tag (vectorised compare)
                         const int32_t t0 = tr[0];
                         int32_t diff = 0;
@@ -568,34 +598,13 @@ DLB_API dlb_status dlb_collide_and_stream(const dlb_registry* reg, dlb_block_vie
                             else if (t < 0) untagged[size_t(w)] = 1;
                             else unknown[size_t(w)] = 1;
                         }
-                        if (have_ctx && !changed[size_t(w)]) {
-                            const int32_t* pr = block->param_index + row + 1;
-                            const int64_t rs = ctx.row_slot[size_t(k0 / nx)];
-                            if (rs != kMixedRow) {
-                                const int32_t v = int32_t(rs);
-                                int32_t d = 0;
-                                for (int64_t x = 0; x < nx; ++x) d |= pr[x] ^ v;
-                                if (d != 0) changed[size_t(w)] = 1;
-                            } else if (std::memcmp(ctx.slots.data() + k0, pr, size_t(nx) * sizeof(int32_t)) != 0) {
-                                changed[size_t(w)] = 1;
-                            }
-                        }
                     }
+                    if (have_ctx && !spec_path && !changed[size_t(w)] && plane_changed(z)) changed[size_t(w)] = 1;
+                }
             });
         }
-        auto is_pinned = [](const void* p) {
-            cudaPointerAttributes attr{};
-            const bool ok = cudaPointerGetAttributes(&attr, p) == cudaSuccess && attr.type == cudaMemoryTypeHost &&
-                            attr.devicePointer == p;
-            cudaGetLastError();
-            return ok;
-        };
-        const bool pinned = is_pinned(block->f_in) && (!block->f_out || is_pinned(block->f_out));
-        // While the scan runs, speculatively start the pinned pipeline with the
-        // cached slots: host->device copies and the step write device memory
-        // only; the copy-back into the caller's block waits for the verdict.
         bool speculative = false;
-        if (have_ctx && pinned) {
+        if (spec_path) {
             try {
                 ctx.lat->begin_host_block(block->f_in, ext, block->f_out);
                 speculative = true;
@@ -605,6 +614,7 @@ DLB_API dlb_status dlb_collide_and_stream(const dlb_registry* reg, dlb_block_vie
             }
         }
         for (auto& t : th) t.join();
+        th.clear();
         const auto t_scan = std::chrono::steady_clock::now();
         auto drop = [&] {
             if (speculative) ctx.lat->abort_host_block();
@@ -641,10 +651,8 @@ DLB_API dlb_status dlb_collide_and_stream(const dlb_registry* reg, dlb_block_vie
             ctx.reg_generation = reg->generation;
             ctx.slots.clear();
         }
-        bool any_change = !have_ctx;
-        for (char c : changed) any_change = any_change || c;
-        if (any_change) {
-            drop();  // computed with stale slots
+        // the block's param_index as the device lattice's slots (+ the row summary)
+        auto load_slots = [&] {
             ctx.slots.resize(size_t(nx * ny * nz));
             ctx.row_slot.assign(size_t(ny * nz), kMixedRow);
             for (int64_t z = 1; z <= nz; ++z)
@@ -657,24 +665,62 @@ DLB_API dlb_status dlb_collide_and_stream(const dlb_registry* reg, dlb_block_vie
                     if (d == 0) ctx.row_slot[size_t(r)] = src[0];
                 }
             ctx.lat->set_slots(ctx.slots.data());
-        }
+        };
         if (speculative) {
-            ctx.lat->finish_host_block();
+            // param_index vs the cached slots, planes handed out in z order,
+            // beside the copy-back: state[z] 0 pending / 1 same / 2 changed
+            std::unique_ptr<std::atomic<char>[]> state(new std::atomic<char>[size_t(nz)]);
+            for (int64_t z = 0; z < nz; ++z) state[size_t(z)].store(0, std::memory_order_relaxed);
+            std::atomic<int64_t> next{0};
+            for (int w = 0; w < nw; ++w)
+                th.emplace_back([&] {
+                    for (int64_t z; (z = next.fetch_add(1)) < nz;)
+                        state[size_t(z)].store(plane_changed(z + 1) ? 2 : 1, std::memory_order_release);
+                });
+            auto join_all = [&] {
+                for (auto& t : th)
+                    if (t.joinable()) t.join();
+            };
+            int64_t confirmed = 0;  // interior planes [0, confirmed) known unchanged
+            auto gate = [&](int z_end) {
+                for (; confirmed < z_end; ++confirmed) {
+                    char v;
+                    while ((v = state[size_t(confirmed)].load(std::memory_order_acquire)) == 0) std::this_thread::yield();
+                    if (v == 2) return int(confirmed);
+                }
+                return -1;
+            };
+            auto reslot = [&] {
+                join_all();
+                load_slots();
+            };
+            try {
+                ctx.lat->finish_host_block(gate, reslot);
+            } catch (...) {
+                join_all();
+                throw;
+            }
+            join_all();
             if (std::getenv("DLB_TRACE_BLOCK")) {
                 const auto t_end = std::chrono::steady_clock::now();
                 std::fprintf(stderr, "[dlb block] scan %.1f ms, total %.1f ms\n",
                              std::chrono::duration<double, std::milli>(t_scan - t_call).count(),
                              std::chrono::duration<double, std::milli>(t_end - t_call).count());
             }
-        } else if (pinned) {
-            // pinned: 3-stage H2D / compute / D2H pipeline (Lattice::step_host_block)
-            ctx.lat->step_host_block(block->f_in, ext, block->f_out);
         } else {
-            // pageable memory: staged copies through device memory
-            ctx.lat->upload_block(block->f_in, ext);
-            ctx.lat->enqueue_step();
-            ctx.lat->download_block_interior(block->f_out ? block->f_out : block->f_in, ext, 0);
-            ctx.lat->synchronize();
+            bool any_change = !have_ctx;
+            for (char c : changed) any_change = any_change || c;
+            if (any_change) load_slots();
+            if (pinned) {
+                // pinned: 3-stage H2D / compute / D2H pipeline (Lattice::step_host_block)
+                ctx.lat->step_host_block(block->f_in, ext, block->f_out);
+            } else {
+                // pageable memory: staged copies through device memory
+                ctx.lat->upload_block(block->f_in, ext);
+                ctx.lat->enqueue_step();
+                ctx.lat->download_block_interior(block->f_out ? block->f_out : block->f_in, ext, 0);
+                ctx.lat->synchronize();
+            }
         }
         // the reference's swap (accelerated_lattice.cpp:199): the buffer that
         // received the new state becomes f_in, the untouched previous state f_out

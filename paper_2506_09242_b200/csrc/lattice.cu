@@ -1839,12 +1839,27 @@ void Lattice::begin_host_block(void* f_in, const int64_t ext[3], void* f_out) {
 
 // Copy-back: finished planes go back as soon as their chunk is computed, on a
 // second copy engine, interleaved with the remaining H2D chunks.
-void Lattice::finish_host_block() {
+void Lattice::finish_host_block(const std::function<int(int)>& gate, const std::function<void()>& reslot) {
     DeviceGuard dg(device_);
     if (!blk_.pending) throw std::logic_error("finish_host_block without begin_host_block");
     int written = 1;  // host planes [1, written) copied back (plane 0 is envelope)
+    bool gated = static_cast<bool>(gate);
     for (int c = 0; c < blk_.nchunks; ++c) {
         const int z1 = std::min(blk_.nz, (c + 1) * blk_.zc);
+        if (gated && gate(z1) >= 0) {
+            // the slots of a plane of chunk c (or later) changed: the chunks
+            // before c were stepped with their confirmed slots and stay; drain,
+            // install the new slots, recompute from chunk c on
+            cuda_check(cudaStreamSynchronize(h2d_stream_), "block reslot");
+            cuda_check(cudaStreamSynchronize(stream_), "block reslot");
+            cuda_check(cudaStreamSynchronize(copy_stream_), "block reslot");
+            reslot();
+            if (d_.precision_bits == 64) refill_block_recipes<double>();
+            else refill_block_recipes<float>();
+            blk_.issued = c;
+            while (blk_.issued < blk_.nchunks && blk_.issued <= c + blk_.ahead) issue_block_chunk(blk_.issued++);
+            gated = false;
+        }
         cuda_check(cudaStreamWaitEvent(copy_stream_, blk_ev_[3 * c + 1], 0), "wait");
         if (c == 0 && blk_tr_[3]) cuda_check(cudaEventRecord(blk_tr_[3], copy_stream_), "event");
         block_copy_back_interior(copy_stream_, written, z1 + 1);
@@ -1864,6 +1879,16 @@ void Lattice::finish_host_block() {
                      t[1], t[2], t[3], t[4]);
     }
     ++steps_;
+}
+
+// The pending block step's kernel arguments after new slots: the recipe /
+// slot fields again, geometry and mirror pointers kept.
+template <typename T>
+void Lattice::refill_block_recipes() {
+    StepArgs<T> a;
+    std::memcpy(&a, blk_args_.data(), sizeof(a));
+    fill_recipes(a);
+    std::memcpy(blk_args_.data(), &a, sizeof(a));
 }
 
 // Drop a begun step: nothing was written to the caller's block.

@@ -11,6 +11,7 @@
 
 #include <array>
 #include <cstdint>
+#include <functional>
 #include <memory>
 #include <set>
 #include <string>
@@ -85,7 +86,12 @@ class Lattice {
     // caller's block; abort drops a begun step. Lets the caller's eager
     // dispatch scan overlap the transfers while still failing before any write.
     void begin_host_block(void* f_in, const int64_t ext[3], void* f_out = nullptr);
-    void finish_host_block();
+    // gate(z_end), when given, is asked before the copy-back of the chunk that
+    // ends at interior plane z_end: -1 when the slots of planes [0, z_end) are
+    // confirmed, else the first plane whose slots changed -- then the pipeline
+    // drains, reslot() installs the new slots, and the chunks from that one on
+    // are recomputed (the input mirror still holds the whole input state).
+    void finish_host_block(const std::function<int(int)>& gate = {}, const std::function<void()>& reslot = {});
     void abort_host_block();
     void step(int64_t nsteps);
     void enqueue_step();  // one step, no dispatch check (group stepping)
@@ -335,6 +341,8 @@ class Lattice {
     } blk_;
     std::vector<uint8_t> blk_args_;  // the StepArgs<T> of the pending block step
     void issue_block_chunk(int c);
+    template <typename T>
+    void refill_block_recipes();
     void block_copy(cudaStream_t st, void* host, void* dev, bool up, int p0, int p1);
     void block_copy_back_interior(cudaStream_t st, int p0, int p1);
     template <typename T>

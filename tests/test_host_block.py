@@ -198,36 +198,50 @@ def test_pinned_ragged_block_matches_pageable():
                 _capi.lib().dlb_host_free(k)
 
 
-def test_single_cell_slot_change_in_uniform_row():
-    """The scan summarises uniform rows of the cached slots by one value; a
-    param_index change of one cell in such a row must still re-upload the slots
-    (the result equals a step from a freshly built device context)."""
+@pytest.mark.parametrize("plane", [1, 5, 12])
+@pytest.mark.parametrize("in_place", [True, False])
+def test_single_cell_slot_change_in_uniform_row(plane, in_place):
+    """The scan summarises uniform rows of the cached slots by one value, and
+    on a cached pinned block compares param_index plane by plane beside the
+    copy-back (which it gates chunk by chunk). A one-cell slot change in the
+    first / a middle / the last plane must recompute from that plane's chunk:
+    the result equals a step from a freshly built device context, and the
+    change matters."""
     n = 12
     reg = dlb.DynamicsRegistry()
     case, a, ka, tag, pidx = tgv_block(n, reg, np.float64, pinned)
+    b, kb = pinned(a.shape, np.float64)
     s2 = reg.register_chain(dlb.init_tgv(dlb.CaseConfig(kind="tgv", L=n, Re=5.0, Ma=0.1)).chains[0])
+    alld = dlb.DispatchSet.all_of(reg)
+
+    def step(src, t, p):
+        dlb.refresh_envelope_periodic(src, (1, 1, 1))
+        if in_place:
+            return dlb.collide_and_stream(reg, src, t, p, alld).copy()
+        new, _ = dlb.collide_and_stream(reg, src, t, p, alld, f_out=b)
+        return new.copy()
+
     try:
         a[:, 1:-1, 1:-1, 1:-1] = 0.01
         rng = np.random.default_rng(3)
         a[:, 1:-1, 1:-1, 1:-1] += rng.standard_normal((19, n, n, n)) * 1e-4
-        alld = dlb.DispatchSet.all_of(reg)
         for _ in range(2):
             dlb.refresh_envelope_periodic(a, (1, 1, 1))
             dlb.collide_and_stream(reg, a, tag, pidx, alld)
         snap = a.copy()
         tag2, pidx2 = tag.copy(), pidx.copy()
-        tag2[5, 7, 3], pidx2[5, 7, 3] = reg.tag_of_slot(s2), s2
-        dlb.refresh_envelope_periodic(a, (1, 1, 1))
-        dlb.collide_and_stream(reg, a, tag2, pidx2, alld)   # cached context
-        cached = a.copy()
+        tag2[plane, 7, 3], pidx2[plane, 7, 3] = reg.tag_of_slot(s2), s2
+        cached = step(a, tag2, pidx2)                       # cached context, gated copy-back
         dlb.block_cache_release()
         a[:] = snap
-        dlb.refresh_envelope_periodic(a, (1, 1, 1))
-        dlb.collide_and_stream(reg, a, tag2, pidx2, alld)   # fresh context
-        assert np.array_equal(cached, a)
+        fresh = step(a, tag2, pidx2)                        # fresh context
+        assert np.array_equal(cached[:, 1:-1, 1:-1, 1:-1], fresh[:, 1:-1, 1:-1, 1:-1])
         a[:] = snap
-        dlb.refresh_envelope_periodic(a, (1, 1, 1))
-        dlb.collide_and_stream(reg, a, tag, pidx, alld)
-        assert not np.array_equal(cached[:, 4:7, 6:9, 2:5], a[:, 4:7, 6:9, 2:5])  # the changed cell matters
+        same = step(a, tag, pidx)
+        near = (slice(None), slice(plane - 1, plane + 2), slice(6, 9), slice(2, 5))
+        assert not np.array_equal(cached[near], same[near])  # the changed cell matters
+        far = (slice(None), slice(1, -1), slice(1, 4), slice(8, -1))
+        assert np.array_equal(cached[far], same[far])
     finally:
-        _capi.lib().dlb_host_free(ka)
+        for k in (ka, kb):
+            _capi.lib().dlb_host_free(k)
