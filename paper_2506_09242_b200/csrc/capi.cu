@@ -730,50 +730,46 @@ DLB_API dlb_status dlb_collide_and_stream(const dlb_registry* reg, dlb_block_vie
 
 // refresh_envelope_periodic<T> (accelerated_lattice.cpp:202-238) on a host
 // block: axis-by-axis, later axes spanning the full extent of earlier ones.
-// Three phases (x, y, z) with a barrier between them; inside a phase the
-// (direction, z-range) pieces run on all host threads.
 }  // extern "C"
 namespace {
 template <typename T>
 void refresh_host_envelope(T* base, const int64_t n[3], const int32_t* periodic, int q) {
     const int64_t e0 = n[0] + 2, e1 = n[1] + 2, e2 = n[2] + 2;
-    const int64_t vol = e0 * e1 * e2;
+    const int64_t vol = e0 * e1 * e2, plane = e0 * e1;
     const int nt = int(std::max(1u, std::min(64u, std::thread::hardware_concurrency())));
-    auto parallel = [&](int64_t items, const std::function<void(int64_t, int64_t)>& fn) {
-        const int64_t per = (items + nt - 1) / nt;
-        std::vector<std::thread> th;
-        for (int64_t b = 0; b < items; b += per) th.emplace_back(fn, b, std::min(items, b + per));
-        for (auto& t : th) t.join();
-    };
-    const int64_t rows = int64_t(q) * n[2];  // (direction, interior z) pairs
-    if (periodic[0])  // x: interior y, z
-        parallel(rows, [&](int64_t r0, int64_t r1) {
-            for (int64_t r = r0; r < r1; ++r) {
-                T* f = base + (r / n[2]) * vol + ((r % n[2]) + 1) * e0 * e1;
+    // One parallel pass over the (direction, interior z) planes: the x sweep
+    // of the plane's interior rows, then its y sweep over full x rows (which
+    // reads the x-envelope cells just written), then -- for the planes z = 1
+    // and z = n -- the z sweep's copy of the whole finished plane into the
+    // opposite envelope plane. The reference's axis order (later axes span
+    // the full extent of earlier ones) holds per plane, so no barrier between
+    // the axes is needed, and each plane is refreshed while it is in cache.
+    const int64_t items = int64_t(q) * n[2];
+    auto work = [&](int64_t r0, int64_t r1) {
+        for (int64_t r = r0; r < r1; ++r) {
+            const int64_t zi = (r % n[2]) + 1;
+            T* f = base + (r / n[2]) * vol + zi * plane;
+            if (periodic[0])
                 for (int64_t y = 1; y <= n[1]; ++y) {
                     T* row = f + y * e0;
                     row[0] = row[n[0]];
                     row[n[0] + 1] = row[1];
                 }
-            }
-        });
-    if (periodic[1])  // y: full x rows, interior z
-        parallel(rows, [&](int64_t r0, int64_t r1) {
-            for (int64_t r = r0; r < r1; ++r) {
-                T* f = base + (r / n[2]) * vol + ((r % n[2]) + 1) * e0 * e1;
+            if (periodic[1]) {
                 std::memcpy(f, f + n[1] * e0, std::size_t(e0) * sizeof(T));
                 std::memcpy(f + (n[1] + 1) * e0, f + e0, std::size_t(e0) * sizeof(T));
             }
-        });
-    if (periodic[2])  // z: full planes
-        parallel(int64_t(q) * 2, [&](int64_t k0, int64_t k1) {
-            for (int64_t k = k0; k < k1; ++k) {
-                T* f = base + (k / 2) * vol;
-                const std::size_t pb = std::size_t(e0 * e1) * sizeof(T);
-                if (k % 2 == 0) std::memcpy(f, f + n[2] * e0 * e1, pb);
-                else std::memcpy(f + (n[2] + 1) * e0 * e1, f + e0 * e1, pb);
+            if (periodic[2]) {
+                T* d = base + (r / n[2]) * vol;
+                if (zi == n[2]) std::memcpy(d, f, std::size_t(plane) * sizeof(T));
+                if (zi == 1) std::memcpy(d + (n[2] + 1) * plane, f, std::size_t(plane) * sizeof(T));
             }
-        });
+        }
+    };
+    const int64_t per = (items + nt - 1) / nt;
+    std::vector<std::thread> th;
+    for (int64_t b = 0; b < items; b += per) th.emplace_back(work, b, std::min(items, b + per));
+    for (auto& t : th) t.join();
     (void)e2;
 }
 }  // namespace

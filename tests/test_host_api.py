@@ -182,15 +182,17 @@ def test_no_cpu_fallback_without_gpu():
 
 
 def test_refresh_envelope_periodic_matches_wrap():
-    """dlb_refresh_envelope_periodic == refresh_envelope_periodic (host-only)."""
+    """dlb_refresh_envelope_periodic == refresh_envelope_periodic (host-only),
+    every combination of periodic axes, one-plane and ragged extents; envelope
+    cells of non-periodic axes keep what they held."""
+    import itertools
     rng = np.random.default_rng(3)
-    for dt, per in ((np.float64, (1, 1, 1)), (np.float32, (0, 1, 1)), (np.float64, (1, 0, 0))):
-        inner = rng.standard_normal((19, 5, 6, 7)).astype(dt)
-        blk = np.zeros((19, 7, 8, 9), dt)
-        blk[:, 1:-1, 1:-1, 1:-1] = inner
+    for (dt, shape), per in itertools.product(((np.float64, (5, 6, 7)), (np.float32, (1, 4, 3)),
+                                               (np.float32, (3, 1, 9))),
+                                              itertools.product((0, 1), repeat=3)):
+        blk = rng.standard_normal((19,) + tuple(k + 2 for k in shape)).astype(dt)
+        want = blk.copy()
         dlb.refresh_envelope_periodic(blk, per)
-        want = np.zeros_like(blk)
-        want[:, 1:-1, 1:-1, 1:-1] = inner
         # axis sweeps x, y, z with later axes spanning earlier ones (accelerated_lattice.cpp:202-238)
         if per[0]:
             want[:, 1:-1, 1:-1, 0] = want[:, 1:-1, 1:-1, -2]
@@ -201,7 +203,7 @@ def test_refresh_envelope_periodic_matches_wrap():
         if per[2]:
             want[:, 0] = want[:, -2]
             want[:, -1] = want[:, 1]
-        assert np.array_equal(blk, want)
+        assert np.array_equal(blk, want), (dt, shape, per)
 
 
 def test_capi_null_arguments_and_buffer_protocol():
