@@ -653,18 +653,25 @@ DLB_API dlb_status dlb_collide_and_stream(const dlb_registry* reg, dlb_block_vie
         }
         // the block's param_index as the device lattice's slots (+ the row summary)
         auto load_slots = [&] {
-            ctx.slots.resize(size_t(nx * ny * nz));
-            ctx.row_slot.assign(size_t(ny * nz), kMixedRow);
+            // committed to the context only once the device lattice accepted
+            // them: a rejected param_index (unregistered slot) must not leave
+            // the cache believing the device holds it
+            std::vector<int32_t> slots(size_t(nx * ny * nz));
+            std::vector<int64_t> row_slot(size_t(ny * nz), kMixedRow);
             for (int64_t z = 1; z <= nz; ++z)
                 for (int64_t y = 1; y <= ny; ++y) {
                     const int64_t r = (z - 1) * ny + (y - 1);
                     const int32_t* src = block->param_index + (z * ext[1] + y) * ext[0] + 1;
-                    std::memcpy(ctx.slots.data() + r * nx, src, size_t(nx) * sizeof(int32_t));
+                    std::memcpy(slots.data() + r * nx, src, size_t(nx) * sizeof(int32_t));
                     int32_t d = 0;
                     for (int64_t x = 0; x < nx; ++x) d |= src[x] ^ src[0];
-                    if (d == 0) ctx.row_slot[size_t(r)] = src[0];
+                    if (d == 0) row_slot[size_t(r)] = src[0];
                 }
-            ctx.lat->set_slots(ctx.slots.data());
+            ctx.slots.clear();  // (invalid until set_slots succeeds)
+            ctx.row_slot.clear();
+            ctx.lat->set_slots(slots.data());
+            ctx.slots = std::move(slots);
+            ctx.row_slot = std::move(row_slot);
         };
         if (speculative) {
             // param_index vs the cached slots, planes handed out in z order,

@@ -245,3 +245,39 @@ def test_single_cell_slot_change_in_uniform_row(plane, in_place):
     finally:
         for k in (ka, kb):
             _capi.lib().dlb_host_free(k)
+
+
+@pytest.mark.parametrize("memory", ["pageable", "pinned"])
+def test_unregistered_slot_rejected_then_recovers(memory):
+    """A param_index naming an unregistered slot is rejected (the reference
+    would index past its recipe table); the cached context must not keep the
+    rejected slots, so the next valid call steps with the right ones."""
+    n = 12
+    alloc = pinned if memory == "pinned" else host_alloc
+    reg = dlb.DynamicsRegistry()
+    case, a, ka, tag, pidx = tgv_block(n, reg, np.float64, alloc)
+    s2 = reg.register_chain(dlb.init_tgv(dlb.CaseConfig(kind="tgv", L=n, Re=5.0, Ma=0.1)).chains[0])
+    alld = dlb.DispatchSet.all_of(reg)
+    try:
+        a[:, 1:-1, 1:-1, 1:-1] = 0.01
+        for _ in range(2):
+            dlb.refresh_envelope_periodic(a, (1, 1, 1))
+            dlb.collide_and_stream(reg, a, tag, pidx, alld)
+        snap = a.copy()
+        bad = pidx.copy()
+        bad[9, 4, 4] = 99
+        with pytest.raises(Exception):
+            dlb.collide_and_stream(reg, a, tag, bad, alld)
+        tag2, pidx2 = tag.copy(), pidx.copy()
+        tag2[9, 4, 4], pidx2[9, 4, 4] = reg.tag_of_slot(s2), s2
+        a[:] = snap
+        dlb.refresh_envelope_periodic(a, (1, 1, 1))
+        got = dlb.collide_and_stream(reg, a, tag2, pidx2, alld).copy()
+        dlb.block_cache_release()
+        a[:] = snap
+        dlb.refresh_envelope_periodic(a, (1, 1, 1))
+        want = dlb.collide_and_stream(reg, a, tag2, pidx2, alld)
+        assert np.array_equal(got[:, 1:-1, 1:-1, 1:-1], want[:, 1:-1, 1:-1, 1:-1])
+    finally:
+        if ka is not None:
+            _capi.lib().dlb_host_free(ka)
