@@ -1659,14 +1659,25 @@ void Lattice::launch_host_block(void* f_in, const int64_t ext[3], void* f_out) {
     hg.dstride = vol;
     hg.per_x = hg.per_y = hg.per_z = 0;  // the caller's envelope is authoritative
     const std::size_t bytes = std::size_t(d_.q) * vol * sizeof(T);
-    if (blk_out_bytes_ < 2 * bytes) {
-        cudaFree(blk_out_);
-        blk_out_ = nullptr;
-        cuda_check(cudaMalloc(&blk_out_, 2 * bytes), "cudaMalloc block mirrors");
-        blk_out_bytes_ = 2 * bytes;
+    T* din;
+    T* dout;
+    if (!aa() && std::size_t(d_.q) * std::size_t(geo_.dstride) * sizeof(T) >= bytes) {
+        // the lattice's own two population buffers hold the host-layout
+        // mirrors (each call uploads the whole input state, so nothing else
+        // lives there between calls): no second pair of state-sized buffers
+        din = static_cast<T*>(buf_[0]);
+        dout = static_cast<T*>(buf_[1]);
+        envelope_valid_ = false;
+    } else {
+        if (blk_out_bytes_ < 2 * bytes) {
+            cudaFree(blk_out_);
+            blk_out_ = nullptr;
+            cuda_check(cudaMalloc(&blk_out_, 2 * bytes), "cudaMalloc block mirrors");
+            blk_out_bytes_ = 2 * bytes;
+        }
+        din = static_cast<T*>(blk_out_);
+        dout = din + std::size_t(d_.q) * vol;
     }
-    T* din = static_cast<T*>(blk_out_);
-    T* dout = din + std::size_t(d_.q) * vol;
     if (!copy_stream_) cuda_check(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking), "stream");
     if (!h2d_stream_) cuda_check(cudaStreamCreateWithFlags(&h2d_stream_, cudaStreamNonBlocking), "stream");
     StepArgs<T> a{};

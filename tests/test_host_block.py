@@ -281,3 +281,32 @@ def test_unregistered_slot_rejected_then_recovers(memory):
     finally:
         if ka is not None:
             _capi.lib().dlb_host_free(ka)
+
+
+def test_pinned_pipeline_uses_the_lattice_buffers():
+    """The pinned pipeline's host-layout mirrors live in the cached lattice's
+    own two population buffers: a host-block context costs one two-population
+    lattice (+ staging), not a second pair of state-sized buffers."""
+    import torch
+    n = 192
+    reg = dlb.DynamicsRegistry()
+    _, a, ka, tag, pidx = tgv_block(n, reg, np.float32, pinned)
+    b, kb = pinned(a.shape, np.float32)
+    try:
+        dlb.block_cache_release()
+        torch.cuda.init()
+        torch.cuda.synchronize()
+        free0 = torch.cuda.mem_get_info()[0]
+        a[:, 1:-1, 1:-1, 1:-1] = 0.01
+        dlb.refresh_envelope_periodic(a, (1, 1, 1))
+        dlb.collide_and_stream(reg, a, tag, pidx, dlb.DispatchSet.all_of(reg), f_out=b)
+        dlb.refresh_envelope_periodic(b, (1, 1, 1))
+        dlb.collide_and_stream(reg, b, tag, pidx, dlb.DispatchSet.all_of(reg), f_out=a)  # cached: pinned pipeline
+        used = free0 - torch.cuda.mem_get_info()[0]
+        lattice_bytes = dlb.block_cache_info()[1]
+        mirror_pair = 2 * a.nbytes
+        assert used < lattice_bytes + mirror_pair // 2, (used, lattice_bytes, mirror_pair)
+    finally:
+        dlb.block_cache_release()
+        for k in (ka, kb):
+            _capi.lib().dlb_host_free(k)
