@@ -132,6 +132,8 @@ def cpu_reference(kind, L, Re, Ma, collision, q, bits, warmup, steps, reps=3):
 
 def run_reference_arm(args, cfgname):
     kind, L, Re, Ma, coll, q, bits, scaling, desc = CONFIGS[cfgname]
+    if args.L:
+        L = args.L
     rank = env_int("RANK", 0)
     if rank != 0:
         return
@@ -444,7 +446,9 @@ def main():
             mean, reps_, workers = res
             cpu = {"value": mean, "unit": "MLUPS", "cores": workers, "kind": "reference",
                    "sample": f"{kind} {Ls}^3 D3Q{q} {coll} fp{bits}: reference MultiBlockRun, "
-                             f"{workers} workers x z-blocks, warmup 2, 3 reps x 8 steps (mean)"}
+                             f"{workers} workers x z-blocks, warmup 2, 3 reps x 8 steps (mean)"
+                             + (f"; {Ls}^3 instead of {L}^3: a bounded sample (host RAM / run time)"
+                                if Ls < L else "")}
     e2e = None
     if not args.no_e2e and q == 19 and kind == "tgv":
         del run

@@ -21,3 +21,28 @@ def test_bench_spawn_command_uses_loopback():
     m = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(m)
     assert 1024 <= m.free_port() < 65536
+
+
+def test_reference_arm_line():
+    """bench.py --impl reference: one JSON line with the contract's keys (the
+    reference compiled from its sources, timed on the host cores); rank > 0
+    of a torchrun launch prints nothing and exits 0."""
+    import json
+    import pytest
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--L", "24", "--steps", "2",
+           "--warmup", "1"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference"
+    if "unavailable" in line:
+        pytest.skip(line["unavailable"])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert k in line, k
+    assert line["metric"] == "MLUPS" and line["value"] > 0 and line["higher_is_better"] is True
+    assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+    r1 = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
+                        env=dict(os.environ, RANK="1", WORLD_SIZE="2"))
+    assert r1.returncode == 0 and r1.stdout.strip() == ""
