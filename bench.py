@@ -453,7 +453,9 @@ def main():
     if not args.no_e2e and q == 19 and kind == "tgv":
         del run
         torch.cuda.empty_cache()
-        e2e = e2e_block(args.e2e_L or min(L, 512), bits, max(2, min(args.steps, 5)), 1, rank, world,
+        # up to 10 timed calls after 2 warm-up calls (~0.25 s each at 512^3 fp32): the
+        # PCIe-bound rate varies by a few percent from call to call
+        e2e = e2e_block(args.e2e_L or min(L, 512), bits, max(2, min(args.steps, 10)), 2, rank, world,
                         barrier, max_over_ranks)
     if rank == 0:
         line = {
